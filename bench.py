@@ -1,0 +1,435 @@
+"""MG-WFBP iteration benchmark on B200 (driver contract: one JSON line).
+
+One step = one synchronous data-parallel iteration of the hot path on the
+named model's layer trace: the backward pass replayed from B200-measured
+per-tensor times (traces/<model>.json) on a compute stream, and every merge
+group's fused pack -> NVLink all-reduce -> unpack+SGD kernel launched on a
+comm stream the moment its head layer is ready (paper Algorithm 2), the
+whole iteration one CUDA graph. Gradients are synthetic uniform[-1,1) fp32
+(seed 0x5EED0000 + rank), weights uniform (seed 0xC0FFEE), lr 0.01.
+
+  value   = N * K / (max over ranks of the device time of K MG-WFBP
+            iterations)  [worker-iterations/s; driver scaling efficiency =
+            value_N / (N * value_1) = t_iter(1) / t_iter(N), the paper's]
+  plan    = optimal_plan(trace, (a, b)) with (a, b) fitted (fit_model) to
+            an on-box calibration sweep of the same fused kernel at this N
+  strategies: MG-WFBP (optimal), WFBP (all normal), single buffer (all
+            merged), greedy (paper Algorithm 1) on the same pipeline
+
+usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--trace googlenet]
+       python bench.py --impl reference ...   (CPU Algorithm 2 on host cores)
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N (one rank per GPU).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "iter time & scaling eff. @1/2/4/8 B200 vs WFBP; merged allreduce bus GB/s"
+UNIT = "worker-iters/s"
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction, /opt/skills/guides/B200_PROFILING.md
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mgwfbp", choices=["mgwfbp", "reference"])
+    ap.add_argument("--trace", default="googlenet")
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot"])
+    ap.add_argument("--oneshot-max", type=int, default=512 * 1024)
+    ap.add_argument("--l2-flush-mib", type=int, default=256)
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def trace_path(name: str) -> str:
+    return name if name.endswith(".json") else os.path.join(ROOT, "traces", f"{name}.json")
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        finally:
+            os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# -------------------------------------------------------------- CPU legs
+def cpu_pipeline_sample(trace, tags, P, lr, threads, budget_s, iters_cap=None):
+    """The CPU restatement of Algorithm 2 (oracle port) on host buffers."""
+    import numpy as np
+
+    from oracle import pyoracle
+
+    counts = [l.params for l in trace.layers]
+    rng = np.random.default_rng(0x5EED0000)
+    g = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(P)]
+    w = [[np.full(c, 0.5, np.float32) for c in counts] for _ in range(P)]
+    t_b = [l.backward_time for l in trace.layers]
+    first = pyoracle.pipeline_run(g, w, counts, t_b, trace.forward_time, tags, lr, threads, 1)[0]
+    iters = max(3, min(200, int(budget_s / max(first, 1e-6))))
+    if iters_cap is not None:
+        iters = min(iters, iters_cap)
+    times = pyoracle.pipeline_run(g, w, counts, t_b, trace.forward_time, tags, lr, threads, iters)
+    return times
+
+
+def ref_solver_us(trace, model, reps=200):
+    import ctypes
+
+    from oracle import pyoracle
+
+    if pyoracle.REF is None:
+        return None
+    params = [l.params for l in trace.layers]
+    t_b = [l.backward_time for l in trace.layers]
+    L = len(params)
+    p = (ctypes.c_uint64 * L)(*params)
+    tb = (ctypes.c_double * L)(*t_b)
+    out = (ctypes.c_uint8 * L)()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        pyoracle.REF.ref_optimal_plan(p, tb, L, trace.forward_time, trace.bytes_per_element, model.a, model.b, out)
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts) * 1e6
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port of Algorithm 2
+    + the reference's own optimal_plan from oracle/_ref) on host cores."""
+    from paper_1912_09268_b200 import dist as D
+    from paper_1912_09268_b200 import gradsched as gs
+
+    rank, world, _ = D.env_world()
+    if rank != 0:
+        return 0
+    N = max(world, args.gpus)
+    trace = gs.load_trace(trace_path(args.trace))
+    # paper cluster-independent model: a NVLink-class guess; the plan only
+    # decides grouping, the CPU work is the same bytes either way
+    model = gs.AllReduceModel(20e-6, 1.0 / 600e9)
+    plan = gs.optimal_plan(trace, model)
+    tags = [int(t) for t in plan.tags]
+    threads = os.cpu_count() or 1
+    cpu_pipeline_sample(trace, tags, N, args.lr, threads, 0.0, iters_cap=args.warmup)
+    times = cpu_pipeline_sample(trace, tags, N, args.lr, threads, 1e9, iters_cap=args.steps)
+    total = sum(times)
+    value = N * len(times) / total
+    solver = ref_solver_us(trace, model)
+    sample = (f"{len(times)} CPU iterations of {args.trace} ({trace.n_layers()} tensors, "
+              f"{trace.total_params()} fp32 params), {N} ranks emulated as host buffers; "
+              f"reference optimal_plan {solver:.1f} us on 1 core" if solver else "")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": len(times),
+        "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "impl": "reference",
+        "data": "synthetic uniform[-1,1) fp32 gradients",
+        "config": {"workload": args.trace, "trace": os.path.relpath(trace_path(args.trace), ROOT),
+                   "plan": "optimal", "ranks": N},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------- GPU leg
+def fit_with_fallback(gs, meas):
+    try:
+        return gs.fit_model(meas), "fit_model over the full sweep"
+    except gs.FitError:
+        small = [m for m in meas if m.size_bytes <= 4 << 20]
+        try:
+            return gs.fit_model(small), "fit_model over sizes <= 4 MiB (full sweep not linear)"
+        except gs.FitError:
+            t0 = min(m.time_sec for m in meas)
+            big = sorted(meas, key=lambda m: m.size_bytes)[-2:]
+            b = max(0.0, (big[1].time_sec - big[0].time_sec) / max(1, big[1].size_bytes - big[0].size_bytes))
+            return gs.AllReduceModel(t0, b), "min-time startup + large-message slope"
+
+
+def calibration_sizes(total_bytes: int):
+    top = max(1 << 22, 1 << math.ceil(math.log2(max(total_bytes, 1))))
+    sizes = []
+    s = 4096
+    while s <= top:
+        sizes.append(s)
+        mid = int(s * math.sqrt(2)) & ~15
+        if mid < top:
+            sizes.append(mid)
+        s *= 2
+    return sizes
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    from paper_1912_09268_b200 import dist as D
+    from paper_1912_09268_b200 import gradsched as gs
+    from paper_1912_09268_b200 import runtime as rt
+
+    rank, world, local = D.init("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    N = world
+    trace = gs.load_trace(trace_path(args.trace))
+    counts = [l.params for l in trace.layers]
+    L = len(counts)
+    total_bytes = 4 * sum(counts)
+    padded = rt.padded_elems(counts)
+
+    # gradients: one flat fp32 buffer (16-byte aligned layer views, like a
+    # framework's flat grad buffer); weights: one allocation per layer
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0x5EED0000 + rank)
+    flat_grad = torch.empty(padded, dtype=torch.float32, device=dev).uniform_(-1, 1, generator=gen)
+    offs = [0]
+    for c in counts:
+        offs.append(offs[-1] + ((c + 3) & ~3))
+    grads = [flat_grad[offs[i]:offs[i] + counts[i]] for i in range(L)]
+    wgen = torch.Generator(device=dev)
+    wgen.manual_seed(0xC0FFEE)
+    weights = [torch.empty(max(c, 1), dtype=torch.float32, device=dev).uniform_(-1, 1, generator=wgen)[:c]
+               for c in counts]
+
+    comm = rt.Comm(rank, N, local, 4 * padded)
+    comm.set_oneshot_max(args.oneshot_max)
+
+    # ---- N1: on-box calibration of the fused kernel at this N, fitted
+    sizes = calibration_sizes(total_bytes)
+    meas = comm.calibrate(sizes, warmup=3, reps=15, algo=args.algo)
+    tvec = torch.tensor([m.time_sec for m in meas], dtype=torch.float64, device=dev)
+    if N > 1:
+        torch.distributed.all_reduce(tvec, op=torch.distributed.ReduceOp.MAX)
+    meas = [gs.CommMeasurement(m.size_bytes, float(t)) for m, t in zip(meas, tvec.tolist())]
+    model, fit_how = fit_with_fallback(gs, meas)
+    out_dir = os.environ.get("MGW_OUT_DIR")
+    if out_dir and rank == 0:
+        os.makedirs(out_dir, exist_ok=True)
+        with open(os.path.join(out_dir, f"calib_{args.trace}_P{N}.csv"), "w") as f:
+            f.write("size_bytes,time_us\n")
+            for m in meas:
+                f.write(f"{m.size_bytes},{m.time_sec * 1e6:.3f}\n")
+
+    # ---- plans (host solver, replicated; verified identical across ranks)
+    plans = {
+        "mgwfbp": gs.optimal_plan(trace, model),
+        "wfbp": gs.MergePlan.all_normal(L),
+        "single_buffer": gs.MergePlan.all_merged(L),
+        "greedy": gs.greedy_plan(trace, model),
+    }
+    digest = D.agree_plan(plans["mgwfbp"].tags)
+    flush = args.l2_flush_mib << 20
+    pipes = {}
+    dplans = {}
+    for name, plan in plans.items():
+        dplans[name] = rt.DevicePlan(comm, grads, weights, plan)
+        pipes[name] = rt.Pipeline(dplans[name], trace, args.lr, args.algo,
+                                  record_group_times=(name == "mgwfbp"), l2_flush_bytes=flush)
+
+    def timed(name, iters):
+        D.barrier()
+        torch.cuda.synchronize()
+        ms = pipes[name].run(iters)
+        torch.cuda.synchronize()
+        D.barrier()
+        return ms
+
+    for name in pipes:
+        pipes[name].run(max(1, args.warmup))
+    torch.cuda.synchronize()
+
+    # ---- the timed region: K MG-WFBP iterations
+    launches0 = rt.kernel_launches()
+    with ClockSampler(local) as clk:
+        ms = timed("mgwfbp", args.steps)
+    launches = rt.kernel_launches() - launches0
+    clocks = clk.summary()
+    t_total = D.max_over_ranks(sum(ms) / 1e3, dev)
+    value = N * args.steps / t_total
+    group_ms = pipes["mgwfbp"].group_times_ms()
+
+    # ---- comparison strategies on the same box / pipeline
+    strat = {}
+    for name in ("mgwfbp", "wfbp", "single_buffer", "greedy"):
+        m = ms if name == "mgwfbp" else timed(name, args.steps)
+        per = sorted(m)
+        med = D.max_over_ranks(statistics.median(per), dev)
+        p10 = D.max_over_ranks(per[max(0, int(0.1 * len(per)) - 0)], dev)
+        p90 = D.max_over_ranks(per[min(len(per) - 1, int(0.9 * len(per)))], dev)
+        pred = gs.iteration_time(trace, plans[name], model).iteration_time
+        strat[name] = {"iter_ms_median": med, "iter_ms_p10": p10, "iter_ms_p90": p90,
+                       "predicted_ms": pred * 1e3, "groups": dplans[name].n_groups}
+    compute_ms = (trace.forward_time + sum(l.backward_time for l in trace.layers)) * 1e3
+
+    # ---- e2e through the public API with host buffers
+    host_grad = torch.empty(padded, dtype=torch.float32, pin_memory=True)
+    host_grad.copy_(flat_grad.cpu())
+    host_out = torch.empty(4, dtype=torch.float32, pin_memory=True)
+    pipe = pipes["mgwfbp"]
+    D.barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(pipe.stream):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            flat_grad.copy_(host_grad, non_blocking=True)
+            pipe.launch(1)
+            host_out.copy_(weights[0][:4] if counts[0] >= 4 else flat_grad[:4], non_blocking=True)
+        e1.record()
+    e1.synchronize()
+    e2e_s = D.max_over_ranks(e0.elapsed_time(e1) / 1e3, dev)
+    D.barrier()
+
+    # ---- roofline of the dominant kernel (the fused group kernel)
+    peaks = measured_peaks()
+    gbytes = [dplans["mgwfbp"].group_span(g)[2] for g in range(dplans["mgwfbp"].n_groups)]
+    kern_s = sum(group_ms) / 1e3
+    if N == 1:
+        algo_bytes = sum(3 * b for b in gbytes)  # read grad, read W, write W
+        peak = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
+        roof = {"bound": "hbm", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+    else:
+        algo_bytes = sum(2 * (N - 1) / N * b for b in gbytes)  # NVLink bus bytes
+        peak = NVLINK_PEER_GBS
+        roof = {"bound": "nvlink", "peak_source": "measured B200 peer copy 770 GB/s/direction (B200_PROFILING.md)"}
+    achieved = algo_bytes / kern_s / 1e9 if kern_s > 0 else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_{args.trace}_P{N}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    roof.update({"kernel": "group_allreduce_kernel (fused pack+allreduce+unpack/SGD)",
+                 "achieved": achieved, "peak": peak, "unit": "GB/s",
+                 "frac": achieved / peak if achieved else None, "traffic": traffic,
+                 "algorithmic_bytes_per_iter": algo_bytes, "kernel_ms_per_iter": kern_s * 1e3,
+                 "launches_per_iter": len(group_ms)})
+
+    bus = {}
+    if N > 1:
+        for m in meas:
+            if m.size_bytes >= (16 << 20):
+                bus[str(m.size_bytes)] = 2 * (N - 1) / N * m.size_bytes / m.time_sec / 1e9
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        times = cpu_pipeline_sample(trace, [int(t) for t in plans["mgwfbp"].tags], 1, args.lr, threads,
+                                    args.cpu_budget_s)
+        solver = ref_solver_us(trace, model)
+        cpu = {"value": len(times) / sum(times), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{len(times)} iterations of the CPU Algorithm-2 restatement (oracle/mgw_oracle.c, "
+                         f"same trace/plan, P=1, {threads} threads)"
+                         + (f"; reference optimal_plan (oracle/_ref) {solver:.1f} us on 1 core" if solver else "")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic uniform[-1,1) fp32 gradients; backward replayed from B200-measured per-tensor t_b",
+            "config": {"workload": args.trace, "trace": os.path.relpath(trace_path(args.trace), ROOT),
+                       "layers": L, "params": sum(counts), "grad_bytes": total_bytes,
+                       "plan": "optimal_plan on on-box calibrated (a, b)", "plan_sha256": digest[:16],
+                       "groups": dplans["mgwfbp"].n_groups, "algo": args.algo, "oneshot_max": args.oneshot_max,
+                       "parallelism": f"dp{N}", "l2": f"flushed every iteration ({args.l2_flush_mib} MiB memset "
+                                                     "on the comm stream during the forward replay)",
+                       "compute_ms": compute_ms},
+            "calibration": {"a_us": model.a * 1e6, "b_ps_per_byte": model.b * 1e12, "how": fit_how,
+                            "sizes": len(meas), "largest_bytes": meas[-1].size_bytes,
+                            "largest_us": meas[-1].time_sec * 1e6},
+            "strategies": strat,
+            "speedup_vs_wfbp": strat["wfbp"]["iter_ms_median"] / strat["mgwfbp"]["iter_ms_median"],
+            "speedup_vs_single_buffer": strat["single_buffer"]["iter_ms_median"] / strat["mgwfbp"]["iter_ms_median"],
+            "bus_gbs": bus,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": N * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": padded * 4,
+                    "d2h_bytes_per_step": 16},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    for p in pipes.values():
+        p.close()
+    for p in dplans.values():
+        p.close()
+    comm.close()
+    if torch.distributed.is_initialized():
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

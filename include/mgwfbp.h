@@ -1,0 +1,220 @@
+/*
+ * mgwfbp.h — C ABI of the B200-native MG-WFBP runtime (libmgwfbp.so).
+ *
+ * The reference (arxiv 1912.09268, `gradsched`) exposes a header-only C++
+ * API and no FFI. This header is the thin, plain-pointer boundary that a
+ * binding (ctypes, cgo, JNI, ...) or a C++ host calls. It has two halves:
+ *
+ *  HOST (pure, thread-safe, no CUDA): the solver, predictor and calibration
+ *  fit, bit-exact with the reference C++ functions they replace.
+ *
+ *  DEVICE (sm_100a, one process per GPU): symmetric merge arenas mapped over
+ *  NVLink with CUDA IPC, the pack kernel, the fused pack -> one-shot/two-shot
+ *  all-reduce -> unpack+SGD kernel, the backward-replay pipeline and the
+ *  on-box calibration sweep. The reference only *models* these (paper
+ *  Algorithm 2; cost model comm_model.hpp:194-199).
+ *
+ * Conventions
+ *  - Every function returns an mgw_status. On failure mgw_last_error()
+ *    returns a thread-local message. No C++ exception crosses this ABI.
+ *  - Status codes mirror the reference CLI exit codes (tools/main.cpp:31-35):
+ *    2 = bad input (ValidationError / ParseError / FitError),
+ *    3 = planner rejection (PlannerError), 4 = guard refusal (GuardError).
+ *  - Tags: 0 = normal (group head), 1 = merged (folds into the next lower
+ *    layer), indexed in forward order like ModelTrace::layers.
+ *  - Times in seconds (double) unless a name says otherwise.
+ *  - Streams are cudaStream_t passed as void*. Device pointers are
+ *    caller-owned fp32 buffers; nothing on the hot path allocates.
+ *  - Device functions of one communicator are collective: every rank calls
+ *    them in the same order with the same arguments (sizes, plans, groups).
+ */
+#ifndef MGWFBP_H_
+#define MGWFBP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MGW_OK = 0,
+  MGW_ERR_INPUT = 2,
+  MGW_ERR_PLANNER = 3,
+  MGW_ERR_GUARD = 4,
+  MGW_ERR_CUDA = 6,
+  MGW_ERR_INTERNAL = 7,
+} mgw_status;
+
+/* One calibration sample. Same fields as gradsched::CommMeasurement
+ * (reference comm_model.hpp:121-130). */
+typedef struct {
+  uint64_t size_bytes;
+  double time_sec;
+} mgw_meas;
+
+const char* mgw_last_error(void);
+/* Class of the last error: "ValidationError", "ParseError", "FitError",
+ * "PlannerError", "GuardError", "CudaError" or "Error". */
+const char* mgw_last_error_kind(void);
+const char* mgw_version(void);
+
+/* ------------------------------------------------------------------ HOST */
+
+/* gradsched::fit_model (comm_model.hpp:209-251): 1/t^2-weighted least
+ * squares -> T(M) = a + b*M. */
+int mgw_fit(const mgw_meas* samples, size_t n, double* a_out, double* b_out);
+
+/* gradsched::load_measurements_csv (comm_model.hpp:255-308). Two-call
+ * pattern: pass out=NULL to get the count, then a buffer of that size. */
+int mgw_load_measurements_csv(const char* path, mgw_meas* out, size_t cap, size_t* n_out);
+
+/* gradsched::coefficients_for (comm_model.hpp:140-191). algo: 0 binary
+ * tree, 1 recursive doubling, 2 recursive halving/doubling, 3 double binary
+ * trees, 4 ring. */
+int mgw_coefficients(int algo, double alpha, double beta, double gamma, int n_workers,
+                     int dbt_literal, double* a_out, double* b_out);
+
+/* A trace in the reference schema (trace.hpp:38-94): L layers in forward
+ * order, params[i] gradient elements, t_b[i] backward seconds. */
+
+/* gradsched::load_trace (trace.hpp:148-219). Two-call pattern on params /
+ * t_b (pass NULL to query L). */
+int mgw_load_trace(const char* path, size_t* L_out, double* t_f_out, int* bpe_out,
+                   uint64_t* params_out, double* t_b_out, size_t cap);
+
+/* gradsched::optimal_plan (planner.hpp:63-98), bit-exact tags. */
+int mgw_plan_optimal(const uint64_t* params, const double* t_b, size_t L, double t_f,
+                     int bpe, double a, double b, uint8_t* tags_out);
+
+/* gradsched::greedy_plan (planner.hpp:112-148; paper Algorithm 1). */
+int mgw_plan_greedy(const uint64_t* params, const double* t_b, size_t L, double t_f,
+                    int bpe, double a, double b, uint8_t* tags_out);
+
+/* gradsched::brute_force_plan (planner.hpp:159-200); L <= max_layers. */
+int mgw_plan_brute_force(const uint64_t* params, const double* t_b, size_t L, double t_f,
+                         int bpe, double a, double b, size_t max_layers, uint8_t* tags_out,
+                         double* iter_time_out);
+
+/* gradsched::iteration_time (timeline.hpp:158-177). Any of the per-layer
+ * outputs may be NULL. */
+int mgw_predict(const uint64_t* params, const double* t_b, size_t L, double t_f, int bpe,
+                double a, double b, const uint8_t* tags, double* iter_time_out,
+                double* comm_nonoverlap_out, double* tau_b_out, double* tau_c_out,
+                double* t_c_out);
+
+/* gradsched::synceasgd_time / naive_time (timeline.hpp:196-221). */
+int mgw_baseline_times(const uint64_t* params, const double* t_b, size_t L, double t_f,
+                       int bpe, double a, double b, double* synceasgd_out, double* naive_out);
+
+/* gradsched::synth_trace + save_trace (trace.hpp:257-346, :221-248): the
+ * canonical JSON text of a deterministic synthetic trace, NUL-terminated in
+ * buf when cap > length. Returns the length, or -status on error. */
+long mgw_synth_trace_json(size_t n_layers, uint64_t total_params, double total_backward_time,
+                          double forward_time, double size_skew, int bpe, uint64_t seed, char* buf,
+                          size_t cap);
+
+/* ---------------------------------------------------------------- DEVICE */
+
+typedef struct mgw_comm mgw_comm;
+typedef struct mgw_plan mgw_plan;
+typedef struct mgw_pipeline mgw_pipeline;
+
+/* Per-rank communicator on `device`: allocates the symmetric merge arena
+ * (2 x arena_bytes: double-buffered by launch parity) and the signal area.
+ * nranks in {1, 2, 4, 8}. */
+int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_comm** out);
+
+/* CUDA IPC handles of this rank's arena + signal area (opaque bytes). */
+size_t mgw_comm_handle_size(void);
+int mgw_comm_export_handle(mgw_comm* comm, void* handle_out);
+/* all_handles: nranks * mgw_comm_handle_size() bytes in rank order. Maps
+ * every peer's arena and signals into this process (NVLink P2P). */
+int mgw_comm_open_peers(mgw_comm* comm, const void* all_handles);
+int mgw_comm_destroy(mgw_comm* comm);
+
+/* Single-GPU emulation of `nranks` ranks (all arenas on one device, every
+ * collective launched as ONE cooperative kernel over all emulated ranks).
+ * Used by the parity tests on one B200; never by the multi-GPU path. */
+int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_comm** out);
+
+/* Device-side plan: the layer table of this rank (grads[i], weights[i]
+ * are device fp32 pointers with counts[i] elements; weights may be NULL
+ * when lr is never used) and the merge tags. For a loopback comm the
+ * arrays hold nranks*L pointers, emulated rank r at [r*L, (r+1)*L).
+ * Group g (0-based, ascending head index) is [head_g, head_{g+1}). */
+int mgw_plan_create(mgw_comm* comm, size_t L, float* const* grads, float* const* weights,
+                    const uint64_t* counts, const uint8_t* tags, mgw_plan** out);
+int mgw_plan_destroy(mgw_plan* plan);
+int mgw_plan_num_groups(const mgw_plan* plan, int* n_groups_out);
+/* Padded element span of group g inside the merge layout (layers start
+ * 16-byte aligned). */
+int mgw_plan_group_span(const mgw_plan* plan, int group, uint64_t* elem_begin,
+                        uint64_t* elem_count, uint64_t* bytes_unpadded);
+
+/* Pack kernel: gather group g's layer gradients, times `scale`, into the
+ * contiguous merge buffer `merge_buf` (>= elem_count floats, padded
+ * layout, zero padding). Rank-local. */
+int mgw_pack(mgw_plan* plan, int group, float scale, float* merge_buf, void* stream);
+
+/* Unpack + SGD: for every layer of group g, w -= lr * red (non-contracted
+ * fp32) and, if write_grad, grad = red. Rank-local. */
+int mgw_unpack_sgd(mgw_plan* plan, int group, const float* merge_buf, float lr, int write_grad,
+                   void* stream);
+
+/* Algorithm selection for the merged all-reduce. */
+typedef enum { MGW_ALGO_AUTO = 0, MGW_ALGO_ONESHOT = 1, MGW_ALGO_TWOSHOT = 2 } mgw_algo;
+/* Epilogue flags. */
+enum { MGW_SGD = 1, MGW_WRITE_GRAD = 2 };
+
+/* The fused hot op, collective: pack (x 1/P) -> all-reduce over NVLink in
+ * rank order -> unpack + SGD, one kernel per group. */
+int mgw_group_allreduce(mgw_plan* plan, int group, float lr, int epilogue, int algo,
+                        void* stream);
+
+/* One-shot/two-shot crossover (bytes) used by MGW_ALGO_AUTO. */
+int mgw_comm_set_oneshot_max(mgw_comm* comm, uint64_t bytes);
+
+/* Backward-replay pipeline (paper Algorithm 2): a compute stream spins
+ * until each group head's ready time (t_f + backward of the layers above,
+ * trace order), a comm stream launches each group the moment its head is
+ * ready, FIFO in backward order; the whole iteration is one CUDA graph.
+ * t_b: L backward seconds, t_f: forward seconds. l2_flush_bytes > 0 adds
+ * a memset of that many bytes on a side branch at iteration start (it
+ * overlaps the forward replay, as a real forward evicts L2), which the first
+ * group waits for, so no iteration reads gradients/weights hot from L2. */
+int mgw_pipeline_create(mgw_plan* plan, const double* t_b, double t_f, float lr, int algo,
+                        int record_group_times, size_t l2_flush_bytes, mgw_pipeline** out);
+int mgw_pipeline_destroy(mgw_pipeline* pipe);
+/* Launch `iters` iterations back to back on the pipeline's compute stream
+ * (asynchronous). */
+int mgw_pipeline_launch(mgw_pipeline* pipe, int iters);
+/* Synchronous: run iters iterations, write per-iteration device times (ms,
+ * CUDA events on the compute stream). */
+int mgw_pipeline_run(mgw_pipeline* pipe, int iters, float* iter_ms_out);
+/* Per-group kernel durations (ms) of the last launched iteration, in group
+ * order; requires record_group_times. */
+int mgw_pipeline_group_times(mgw_pipeline* pipe, float* group_ms_out);
+/* The compute stream (cudaStream_t) the pipeline runs on. */
+int mgw_pipeline_stream(mgw_pipeline* pipe, void** stream_out);
+
+/* On-box calibration sweep (N1): for each size, warmup + reps timed runs
+ * of the fused group kernel on a single-layer group of size/4 elements;
+ * writes the median per size. Collective. */
+int mgw_calibrate(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int warmup, int reps,
+                  int algo, mgw_meas* out);
+
+/* Plain in-place sum all-reduce of a contiguous fp32 device buffer in rank
+ * order (no scale, no SGD), through the same kernel. Collective. */
+int mgw_allreduce(mgw_comm* comm, float* buf, size_t n_elems, int algo, void* stream);
+
+/* Device counts / kernels launched by this library since load (evidence
+ * for the bench's gpu_launches). */
+uint64_t mgw_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MGWFBP_H_ */

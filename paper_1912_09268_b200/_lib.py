@@ -1,0 +1,113 @@
+"""ctypes binding of the C ABI in include/mgwfbp.h (libmgwfbp.so).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_1912_09268_b200/csrc``). There is no fallback: if the shared
+object is missing, importing this module raises, so nothing can silently run
+a CPU path in place of the CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libmgwfbp.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(or `make -C paper_1912_09268_b200/csrc`). There is no CPU fallback."
+    )
+
+lib = C.CDLL(LIB_PATH)
+
+u8p = C.POINTER(C.c_uint8)
+u64p = C.POINTER(C.c_uint64)
+f64p = C.POINTER(C.c_double)
+f32p = C.POINTER(C.c_float)
+vp = C.c_void_p
+
+
+class Meas(C.Structure):
+    _fields_ = [("size_bytes", C.c_uint64), ("time_sec", C.c_double)]
+
+
+def _proto(name, argtypes, restype=C.c_int):
+    fn = getattr(lib, name)
+    fn.argtypes = argtypes
+    fn.restype = restype
+    return fn
+
+
+mgw_last_error = _proto("mgw_last_error", [], C.c_char_p)
+mgw_last_error_kind = _proto("mgw_last_error_kind", [], C.c_char_p)
+mgw_version = _proto("mgw_version", [], C.c_char_p)
+mgw_fit = _proto("mgw_fit", [C.POINTER(Meas), C.c_size_t, f64p, f64p])
+mgw_load_measurements_csv = _proto(
+    "mgw_load_measurements_csv", [C.c_char_p, C.POINTER(Meas), C.c_size_t, C.POINTER(C.c_size_t)]
+)
+mgw_coefficients = _proto(
+    "mgw_coefficients", [C.c_int, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, f64p, f64p]
+)
+mgw_load_trace = _proto(
+    "mgw_load_trace",
+    [C.c_char_p, C.POINTER(C.c_size_t), f64p, C.POINTER(C.c_int), u64p, f64p, C.c_size_t],
+)
+_plan_args = [u64p, f64p, C.c_size_t, C.c_double, C.c_int, C.c_double, C.c_double]
+mgw_plan_optimal = _proto("mgw_plan_optimal", _plan_args + [u8p])
+mgw_plan_greedy = _proto("mgw_plan_greedy", _plan_args + [u8p])
+mgw_plan_brute_force = _proto("mgw_plan_brute_force", _plan_args + [C.c_size_t, u8p, f64p])
+mgw_predict = _proto("mgw_predict", _plan_args + [u8p, f64p, f64p, f64p, f64p, f64p])
+mgw_baseline_times = _proto("mgw_baseline_times", _plan_args + [f64p, f64p])
+mgw_synth_trace_json = _proto(
+    "mgw_synth_trace_json",
+    [C.c_size_t, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_int, C.c_uint64, C.c_char_p,
+     C.c_size_t],
+    C.c_long,
+)
+
+mgw_comm_create = _proto("mgw_comm_create", [C.c_int, C.c_int, C.c_int, C.c_size_t, C.POINTER(vp)])
+mgw_comm_create_loopback = _proto(
+    "mgw_comm_create_loopback", [C.c_int, C.c_int, C.c_size_t, C.POINTER(vp)]
+)
+mgw_comm_handle_size = _proto("mgw_comm_handle_size", [], C.c_size_t)
+mgw_comm_export_handle = _proto("mgw_comm_export_handle", [vp, vp])
+mgw_comm_open_peers = _proto("mgw_comm_open_peers", [vp, vp])
+mgw_comm_destroy = _proto("mgw_comm_destroy", [vp])
+mgw_comm_set_oneshot_max = _proto("mgw_comm_set_oneshot_max", [vp, C.c_uint64])
+mgw_plan_create = _proto(
+    "mgw_plan_create", [vp, C.c_size_t, C.POINTER(vp), C.POINTER(vp), u64p, u8p, C.POINTER(vp)]
+)
+mgw_plan_destroy = _proto("mgw_plan_destroy", [vp])
+mgw_plan_num_groups = _proto("mgw_plan_num_groups", [vp, C.POINTER(C.c_int)])
+mgw_plan_group_span = _proto("mgw_plan_group_span", [vp, C.c_int, u64p, u64p, u64p])
+mgw_pack = _proto("mgw_pack", [vp, C.c_int, C.c_float, vp, vp])
+mgw_unpack_sgd = _proto("mgw_unpack_sgd", [vp, C.c_int, vp, C.c_float, C.c_int, vp])
+mgw_group_allreduce = _proto("mgw_group_allreduce", [vp, C.c_int, C.c_float, C.c_int, C.c_int, vp])
+mgw_allreduce = _proto("mgw_allreduce", [vp, vp, C.c_size_t, C.c_int, vp])
+mgw_calibrate = _proto(
+    "mgw_calibrate", [vp, u64p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.POINTER(Meas)]
+)
+mgw_pipeline_create = _proto(
+    "mgw_pipeline_create",
+    [vp, f64p, C.c_double, C.c_float, C.c_int, C.c_int, C.c_size_t, C.POINTER(vp)],
+)
+mgw_pipeline_destroy = _proto("mgw_pipeline_destroy", [vp])
+mgw_pipeline_launch = _proto("mgw_pipeline_launch", [vp, C.c_int])
+mgw_pipeline_run = _proto("mgw_pipeline_run", [vp, C.c_int, f32p])
+mgw_pipeline_group_times = _proto("mgw_pipeline_group_times", [vp, f32p])
+mgw_pipeline_stream = _proto("mgw_pipeline_stream", [vp, C.POINTER(vp)])
+mgw_kernel_launches = _proto("mgw_kernel_launches", [], C.c_uint64)
+
+# Every symbol the header declares (checked by tests/test_capi_symbols.py).
+EXPORTED = [
+    name
+    for name in dir()
+    if name.startswith("mgw_") and callable(globals()[name])
+]
+
+
+def arr(ctype, values):
+    """A ctypes array holding `values`."""
+    values = list(values)
+    return (ctype * max(1, len(values)))(*values)

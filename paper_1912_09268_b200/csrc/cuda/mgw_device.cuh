@@ -1,0 +1,133 @@
+// mgwfbp-b200: device-side data layout and PTX helpers shared by the
+// kernels (kernels.cu) and the host runtime (runtime.cu).
+//
+// Data layout in HBM (per rank):
+//   merge arena   2 copies x (padded model elements) fp32, selected by the
+//                 parity of the communicator's launch counter. Layer l of
+//                 the plan lives at element offs[l] (16-byte aligned), so
+//                 every merge group [head_g, head_{g+1}) is one contiguous
+//                 span — the paper's pre-allocated merge buffers
+//                  laid out once for all groups.
+//   signal area   two barrier planes x kMaxCtas x kMaxRanks uint32 flags,
+//                 written by peers over NVLink (st.release.sys) and spun on
+//                 locally (ld.acquire.sys).
+//   state         [0] launch counter (epoch source), [1] CTA done counter,
+//                 [2] barrier-timeout error flag.
+// Work unit: a Tile = up to kTileElems consecutive elements of ONE layer,
+// so pack/unpack read and write contiguous 16-byte vectors.
+#ifndef MGWFBP_DEVICE_CUH_
+#define MGWFBP_DEVICE_CUH_
+
+#include <cstdint>
+
+namespace mgw {
+
+constexpr int kMaxRanks = 8;
+constexpr int kMaxCtas = 1024;           // per-rank CTAs of one collective launch
+constexpr int kThreads = 512;            // threads per CTA of the fused kernel
+constexpr uint32_t kTileElems = 4096;    // 16 KiB of fp32; 2 float4 per thread
+constexpr uint32_t kVecPerThread = kTileElems / 4 / kThreads;
+constexpr uint32_t kLayerMask = 0x3fffffffu;
+constexpr uint32_t kGradUnaligned = 0x80000000u;
+constexpr uint32_t kWeightUnaligned = 0x40000000u;
+constexpr int kSignalPlane = kMaxCtas * kMaxRanks;  // uint32 per barrier plane
+constexpr int kSignalWords = 2 * kSignalPlane;
+constexpr int kStateWords = 4;
+
+struct Tile {
+  uint32_t layer;  // layer index | alignment flags
+  uint32_t len;    // valid elements in this tile
+  uint32_t src;    // first element inside the layer
+  uint32_t moff;   // first element in the merge layout (multiple of 4)
+};
+static_assert(sizeof(Tile) == 16, "tile descriptor is one 16-byte load");
+
+// Everything one (possibly emulated) rank needs inside a collective launch.
+struct RankView {
+  float* arena[kMaxRanks];       // every rank's merge arena (peer-mapped)
+  uint32_t* signal[kMaxRanks];   // every rank's signal area (peer-mapped)
+  uint32_t* state;               // this rank's counters
+  float* const* grads;           // this rank's layer gradient pointers
+  float* const* weights;         // this rank's layer weight pointers (may hold NULLs)
+  int rank;
+};
+
+struct GroupLaunch {
+  const Tile* tiles;     // this group's tiles
+  uint32_t n_tiles;
+  int nranks;
+  float scale;           // 1/P, applied in the pack phase
+  float lr;
+  int epilogue;          // MGW_SGD | MGW_WRITE_GRAD
+  uint64_t copy_stride;  // elements between the two arena copies
+  RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
+};
+
+#ifdef __CUDACC__
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Peer / merge-arena loads: L1-bypassing (.cg), so data written by another
+// GPU after this SM last cached the line is never read stale.
+__device__ __forceinline__ float4 ld_cg_v4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// Streaming gradient reads: read once per iteration, keep L1 clean.
+__device__ __forceinline__ float4 ld_stream_v4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ float4 ld_v4(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+
+__device__ __forceinline__ void st_v4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                     __fadd_rn(a.w, b.w));
+}
+
+__device__ __forceinline__ float4 mul4(float4 a, float s) {
+  return make_float4(__fmul_rn(a.x, s), __fmul_rn(a.y, s), __fmul_rn(a.z, s), __fmul_rn(a.w, s));
+}
+
+// w - lr*g with two roundings (never an FMA): the oracle's semantics.
+__device__ __forceinline__ float sgd1(float w, float g, float lr) {
+  return __fsub_rn(w, __fmul_rn(lr, g));
+}
+
+#endif  // __CUDACC__
+
+}  // namespace mgw
+
+#endif  // MGWFBP_DEVICE_CUH_

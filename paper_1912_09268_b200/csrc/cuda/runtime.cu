@@ -1,0 +1,737 @@
+// mgwfbp-b200: device half of the C ABI (include/mgwfbp.h) — communicator
+// (symmetric merge arenas mapped over NVLink with CUDA IPC), device plans
+// (tile tables for every merge group), the standalone pack / unpack+SGD ops,
+// the fused per-group all-reduce, the backward-replay pipeline captured as
+// one CUDA graph per plan, and the on-box calibration sweep.
+//
+// Paper mapping: Algorithm 2 runs a comm daemon thread
+// that pops layers and calls SynchonizedAllReduce(lb) on each normal layer;
+// here the comm "thread" is a CUDA stream whose kernels wait on per-group
+// events of the compute stream, FIFO in backward order — exactly the
+// serialised schedule of reference timeline.hpp:128-154.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "capi_common.hpp"
+#include "gradsched/errors.hpp"
+#include "mgw_device.cuh"
+#include "mgwfbp.h"
+
+namespace mgw {
+
+cudaError_t launch_group_allreduce(const GroupLaunch& L, int ctas_per_rank, bool two_shot,
+                                   bool loopback, cudaStream_t stream);
+cudaError_t max_ctas_per_sm(int nranks, bool two_shot, bool loopback, int* out);
+cudaError_t launch_pack(const Tile* tiles, uint32_t n_tiles, float* const* grads, float* merge,
+                        uint64_t begin, float scale, int ctas, cudaStream_t stream);
+cudaError_t launch_unpack_sgd(const Tile* tiles, uint32_t n_tiles, float* const* grads,
+                              float* const* weights, const float* merge, uint64_t begin, float lr,
+                              int epi, int ctas, cudaStream_t stream);
+cudaError_t launch_replay(unsigned long long* clock, unsigned long long deadline_ns, int first,
+                          cudaStream_t stream);
+
+std::atomic<uint64_t> g_kernel_launches{0};
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+// Bad arguments are input errors (MGW_ERR_INPUT), like the reference's
+// ValidationError.
+void require(bool ok, const std::string& msg) {
+  if (!ok) throw gradsched::ValidationError(msg);
+}
+
+struct IpcBlob {
+  cudaIpcMemHandle_t arena;
+  cudaIpcMemHandle_t signal;
+};
+
+}  // namespace
+}  // namespace mgw
+
+using mgw::ck;
+using mgw::require;
+
+struct mgw_comm {
+  int rank = 0;
+  int nranks = 1;
+  int device = 0;
+  bool loopback = false;
+  size_t arena_elems = 0;  // per copy
+  uint64_t oneshot_max = 512 * 1024;
+  int num_sms = 148;
+  // own allocations (loopback: one per emulated rank)
+  std::vector<float*> arenas;
+  std::vector<uint32_t*> signals;
+  std::vector<uint32_t*> states;
+  // peer mappings opened through IPC (real mode)
+  std::vector<void*> opened;
+  float* peer_arena[mgw::kMaxRanks] = {};
+  uint32_t* peer_signal[mgw::kMaxRanks] = {};
+  bool peers_ready = false;
+  cudaStream_t stream = nullptr;  // calibrate / plain all-reduce
+  // cached single-buffer plan for mgw_allreduce
+  mgw_plan* ar_plan = nullptr;
+  float* ar_buf = nullptr;
+  size_t ar_n = 0;
+};
+
+struct mgw_plan {
+  mgw_comm* comm = nullptr;
+  size_t L = 0;
+  int n_views = 1;
+  std::vector<uint64_t> counts;
+  std::vector<uint64_t> offs;       // L+1 padded element offsets
+  std::vector<size_t> heads;        // G+1, ascending, heads[G] = L
+  std::vector<uint32_t> tile_first; // G+1 tile ranges per group
+  mgw::Tile* d_tiles = nullptr;
+  float** d_grads = nullptr;        // n_views * L
+  float** d_weights = nullptr;      // n_views * L
+  std::vector<float*> h_grads;
+  std::vector<float*> h_weights;
+  int G() const { return static_cast<int>(heads.size()) - 1; }
+};
+
+struct mgw_pipeline {
+  mgw_plan* plan = nullptr;
+  cudaStream_t compute = nullptr;
+  cudaStream_t comm = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  std::vector<cudaEvent_t> ready;
+  std::vector<cudaEvent_t> g_start, g_end;
+  unsigned long long* d_clock = nullptr;
+  void* flush_buf = nullptr;
+  size_t flush_bytes = 0;
+  int iter_flush_value = 0x5a;
+  bool timed_groups = false;
+  int kernels_per_iter = 0;
+};
+
+namespace mgw {
+namespace {
+
+void set_device(const mgw_comm* c) { ck(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+uint32_t* alloc_zero_u32(size_t words) {
+  uint32_t* p = nullptr;
+  ck(cudaMalloc(&p, words * sizeof(uint32_t)), "cudaMalloc(signal)");
+  ck(cudaMemset(p, 0, words * sizeof(uint32_t)), "cudaMemset(signal)");
+  return p;
+}
+
+float* alloc_arena(size_t elems) {
+  float* p = nullptr;
+  ck(cudaMalloc(&p, std::max<size_t>(2 * elems, 4) * sizeof(float)), "cudaMalloc(arena)");
+  ck(cudaMemset(p, 0, std::max<size_t>(2 * elems, 4) * sizeof(float)), "cudaMemset(arena)");
+  return p;
+}
+
+void init_common(mgw_comm* c, int device, size_t arena_bytes) {
+  c->device = device;
+  c->arena_elems = (arena_bytes / sizeof(float) + 3) & ~size_t{3};
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  ck(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+  ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+}
+
+RankView make_view(const mgw_comm* c, int r, float* const* grads, float* const* weights) {
+  RankView v{};
+  for (int q = 0; q < c->nranks; ++q) {
+    if (c->loopback) {
+      v.arena[q] = c->arenas[q];
+      v.signal[q] = c->signals[q];
+    } else {
+      v.arena[q] = c->peer_arena[q];
+      v.signal[q] = c->peer_signal[q];
+    }
+  }
+  v.state = c->states[c->loopback ? r : 0];
+  v.grads = grads;
+  v.weights = weights;
+  v.rank = c->loopback ? r : c->rank;
+  return v;
+}
+
+bool use_two_shot(const mgw_comm* c, uint64_t bytes, int algo) {
+  if (c->nranks == 1) return false;
+  if (algo == MGW_ALGO_ONESHOT) return false;
+  if (algo == MGW_ALGO_TWOSHOT) return true;
+  return bytes > c->oneshot_max;
+}
+
+int grid_for(const mgw_comm* c, uint32_t n_tiles, bool two_shot) {
+  int occ = 1;
+  ck(max_ctas_per_sm(c->nranks, two_shot, c->loopback, &occ), "occupancy");
+  int cap = std::max(1, occ) * c->num_sms;
+  if (c->loopback) cap = std::max(1, cap / c->nranks);
+  cap = std::min(cap, kMaxCtas);
+  const uint32_t units = two_shot ? (n_tiles + c->nranks - 1) / c->nranks : n_tiles;
+  return static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(units, cap)));
+}
+
+uint64_t group_bytes(const mgw_plan* p, int g) {
+  uint64_t s = 0;
+  for (size_t l = p->heads[g]; l < p->heads[g + 1]; ++l) s += p->counts[l] * sizeof(float);
+  return s;
+}
+
+// Fused pack -> all-reduce -> unpack+SGD for group g.
+void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStream_t stream) {
+  mgw_comm* c = p->comm;
+  require(c->loopback || c->nranks == 1 || c->peers_ready,
+          "communicator peers not opened (call mgw_comm_open_peers)");
+  require(g >= 0 && g < p->G(), "group index out of range");
+  GroupLaunch L{};
+  L.tiles = p->d_tiles + p->tile_first[g];
+  L.n_tiles = p->tile_first[g + 1] - p->tile_first[g];
+  L.nranks = c->nranks;
+  L.scale = 1.0f / static_cast<float>(c->nranks);
+  L.lr = lr;
+  L.epilogue = epilogue;
+  L.copy_stride = c->arena_elems;
+  for (int r = 0; r < p->n_views; ++r) {
+    L.views[r] = make_view(c, r, p->d_grads + static_cast<size_t>(r) * p->L,
+                           p->d_weights + static_cast<size_t>(r) * p->L);
+  }
+  const bool two = use_two_shot(c, group_bytes(p, g), algo);
+  ck(launch_group_allreduce(L, grid_for(c, L.n_tiles, two), two, c->loopback, stream),
+     "group_allreduce launch");
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void check_barrier_flags(const mgw_comm* c) {
+  for (uint32_t* st : c->states) {
+    uint32_t flag = 0;
+    ck(cudaMemcpy(&flag, st + 2, sizeof flag, cudaMemcpyDeviceToHost), "read barrier flag");
+    if (flag != 0) throw CudaFailure("cross-rank barrier timed out (a peer never arrived)");
+  }
+}
+
+void destroy_plan(mgw_plan* p) {
+  if (p == nullptr) return;
+  cudaFree(p->d_tiles);
+  cudaFree(p->d_grads);
+  cudaFree(p->d_weights);
+  delete p;
+}
+
+mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* weights,
+                     const uint64_t* counts, const uint8_t* tags) {
+  require(c != nullptr, "comm is NULL");
+  require(L >= 1, "plan needs at least one layer");
+  require(grads != nullptr && counts != nullptr && tags != nullptr, "NULL plan arrays");
+  require(tags[0] == 0, "the first layer cannot be merged (tags[0] must be 0)");
+  set_device(c);
+  auto* p = new mgw_plan();
+  p->comm = c;
+  p->L = L;
+  p->n_views = c->loopback ? c->nranks : 1;
+  p->counts.assign(counts, counts + L);
+  p->offs.resize(L + 1, 0);
+  for (size_t l = 0; l < L; ++l) {
+    require(tags[l] <= 1, "tags must be 0 or 1");
+    require(counts[l] < (uint64_t{1} << 32), "layer too large (>= 2^32 elements)");
+    p->offs[l + 1] = p->offs[l] + ((counts[l] + 3) & ~uint64_t{3});
+    if (l == 0 || tags[l] == 0) p->heads.push_back(l);
+  }
+  p->heads.push_back(L);
+  if (p->offs[L] > c->arena_elems) {
+    const std::string msg = "plan needs " + std::to_string(p->offs[L] * 4) +
+                            " arena bytes; communicator has " + std::to_string(c->arena_elems * 4);
+    delete p;
+    throw gradsched::ValidationError(msg);
+  }
+  require(p->offs[L] < (uint64_t{1} << 32), "model too large for 32-bit tile offsets");
+  const size_t nv = static_cast<size_t>(p->n_views);
+  p->h_grads.assign(grads, grads + nv * L);
+  p->h_weights.assign(nv * L, nullptr);
+  if (weights != nullptr) p->h_weights.assign(weights, weights + nv * L);
+
+  std::vector<Tile> tiles;
+  for (int g = 0; g + 1 < static_cast<int>(p->heads.size()); ++g) {
+    p->tile_first.push_back(static_cast<uint32_t>(tiles.size()));
+    for (size_t l = p->heads[g]; l < p->heads[g + 1]; ++l) {
+      uint32_t flags = 0;
+      for (size_t r = 0; r < nv; ++r) {
+        if (reinterpret_cast<uintptr_t>(p->h_grads[r * L + l]) % 16) flags |= kGradUnaligned;
+        if (reinterpret_cast<uintptr_t>(p->h_weights[r * L + l]) % 16) flags |= kWeightUnaligned;
+        require(counts[l] == 0 || p->h_grads[r * L + l] != nullptr, "NULL gradient pointer");
+      }
+      for (uint64_t s = 0; s < counts[l]; s += kTileElems) {
+        Tile t;
+        t.layer = static_cast<uint32_t>(l) | flags;
+        t.len = static_cast<uint32_t>(std::min<uint64_t>(kTileElems, counts[l] - s));
+        t.src = static_cast<uint32_t>(s);
+        t.moff = static_cast<uint32_t>(p->offs[l] + s);
+        tiles.push_back(t);
+      }
+    }
+  }
+  p->tile_first.push_back(static_cast<uint32_t>(tiles.size()));
+  require(L <= kLayerMask, "too many layers");
+  ck(cudaMalloc(&p->d_tiles, std::max<size_t>(tiles.size(), 1) * sizeof(Tile)), "cudaMalloc(tiles)");
+  if (!tiles.empty()) {
+    ck(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice),
+       "upload tiles");
+  }
+  ck(cudaMalloc(&p->d_grads, nv * L * sizeof(float*)), "cudaMalloc(grads table)");
+  ck(cudaMalloc(&p->d_weights, nv * L * sizeof(float*)), "cudaMalloc(weights table)");
+  ck(cudaMemcpy(p->d_grads, p->h_grads.data(), nv * L * sizeof(float*), cudaMemcpyHostToDevice),
+     "upload grads table");
+  ck(cudaMemcpy(p->d_weights, p->h_weights.data(), nv * L * sizeof(float*),
+                cudaMemcpyHostToDevice),
+     "upload weights table");
+  return p;
+}
+
+}  // namespace
+}  // namespace mgw
+
+extern "C" {
+
+uint64_t mgw_kernel_launches(void) { return mgw::g_kernel_launches.load(); }
+
+size_t mgw_comm_handle_size(void) { return sizeof(mgw::IpcBlob); }
+
+int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_comm** out) {
+  MGW_TRY {
+    require(out != nullptr, "out is NULL");
+    require(nranks == 1 || nranks == 2 || nranks == 4 || nranks == 8, "nranks must be 1, 2, 4 or 8");
+    require(rank >= 0 && rank < nranks, "rank out of range");
+    auto* c = new mgw_comm();
+    c->rank = rank;
+    c->nranks = nranks;
+    mgw::init_common(c, device, arena_bytes);
+    c->arenas.push_back(mgw::alloc_arena(c->arena_elems));
+    c->signals.push_back(mgw::alloc_zero_u32(mgw::kSignalWords));
+    c->states.push_back(mgw::alloc_zero_u32(mgw::kStateWords));
+    ck(cudaDeviceSynchronize(), "init sync");
+    c->peer_arena[rank] = c->arenas[0];
+    c->peer_signal[rank] = c->signals[0];
+    c->peers_ready = nranks == 1;
+    *out = c;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_comm** out) {
+  MGW_TRY {
+    require(out != nullptr, "out is NULL");
+    require(nranks == 1 || nranks == 2 || nranks == 4 || nranks == 8, "nranks must be 1, 2, 4 or 8");
+    auto* c = new mgw_comm();
+    c->nranks = nranks;
+    c->loopback = true;
+    mgw::init_common(c, device, arena_bytes);
+    for (int r = 0; r < nranks; ++r) {
+      c->arenas.push_back(mgw::alloc_arena(c->arena_elems));
+      c->signals.push_back(mgw::alloc_zero_u32(mgw::kSignalWords));
+      c->states.push_back(mgw::alloc_zero_u32(mgw::kStateWords));
+    }
+    ck(cudaDeviceSynchronize(), "init sync");
+    c->peers_ready = true;
+    *out = c;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_export_handle(mgw_comm* c, void* handle_out) {
+  MGW_TRY {
+    require(c != nullptr && handle_out != nullptr && !c->loopback, "bad communicator/handle");
+    mgw::set_device(c);
+    mgw::IpcBlob blob;
+    ck(cudaIpcGetMemHandle(&blob.arena, c->arenas[0]), "cudaIpcGetMemHandle(arena)");
+    ck(cudaIpcGetMemHandle(&blob.signal, c->signals[0]), "cudaIpcGetMemHandle(signal)");
+    std::memcpy(handle_out, &blob, sizeof blob);
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_open_peers(mgw_comm* c, const void* all_handles) {
+  MGW_TRY {
+    require(c != nullptr && all_handles != nullptr && !c->loopback, "bad communicator/handles");
+    mgw::set_device(c);
+    const auto* blobs = static_cast<const mgw::IpcBlob*>(all_handles);
+    for (int q = 0; q < c->nranks; ++q) {
+      if (q == c->rank) continue;
+      void* a = nullptr;
+      void* s = nullptr;
+      ck(cudaIpcOpenMemHandle(&a, blobs[q].arena, cudaIpcMemLazyEnablePeerAccess),
+         "cudaIpcOpenMemHandle(arena)");
+      ck(cudaIpcOpenMemHandle(&s, blobs[q].signal, cudaIpcMemLazyEnablePeerAccess),
+         "cudaIpcOpenMemHandle(signal)");
+      c->opened.push_back(a);
+      c->opened.push_back(s);
+      c->peer_arena[q] = static_cast<float*>(a);
+      c->peer_signal[q] = static_cast<uint32_t*>(s);
+    }
+    c->peers_ready = true;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_set_oneshot_max(mgw_comm* c, uint64_t bytes) {
+  MGW_TRY {
+    require(c != nullptr, "comm is NULL");
+    c->oneshot_max = bytes;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_destroy(mgw_comm* c) {
+  MGW_TRY {
+    if (c == nullptr) return 0;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    mgw::destroy_plan(c->ar_plan);
+    for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+    for (float* a : c->arenas) cudaFree(a);
+    for (uint32_t* s : c->signals) cudaFree(s);
+    for (uint32_t* s : c->states) cudaFree(s);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+  }
+  MGW_CATCH
+}
+
+int mgw_plan_create(mgw_comm* comm, size_t L, float* const* grads, float* const* weights,
+                    const uint64_t* counts, const uint8_t* tags, mgw_plan** out) {
+  MGW_TRY {
+    require(out != nullptr, "out is NULL");
+    *out = mgw::build_plan(comm, L, grads, weights, counts, tags);
+  }
+  MGW_CATCH
+}
+
+int mgw_plan_destroy(mgw_plan* plan) {
+  MGW_TRY {
+    if (plan) cudaSetDevice(plan->comm->device);
+    mgw::destroy_plan(plan);
+  }
+  MGW_CATCH
+}
+
+int mgw_plan_num_groups(const mgw_plan* plan, int* n) {
+  MGW_TRY {
+    require(plan != nullptr && n != nullptr, "NULL argument");
+    *n = plan->G();
+  }
+  MGW_CATCH
+}
+
+int mgw_plan_group_span(const mgw_plan* p, int g, uint64_t* begin, uint64_t* count,
+                        uint64_t* bytes) {
+  MGW_TRY {
+    require(p != nullptr && g >= 0 && g < p->G(), "bad plan/group");
+    if (begin) *begin = p->offs[p->heads[g]];
+    if (count) *count = p->offs[p->heads[g + 1]] - p->offs[p->heads[g]];
+    if (bytes) *bytes = mgw::group_bytes(p, g);
+  }
+  MGW_CATCH
+}
+
+int mgw_pack(mgw_plan* p, int g, float scale, float* merge_buf, void* stream) {
+  MGW_TRY {
+    require(p != nullptr && merge_buf != nullptr && g >= 0 && g < p->G(), "bad pack arguments");
+    mgw::set_device(p->comm);
+    const uint32_t n = p->tile_first[g + 1] - p->tile_first[g];
+    const int ctas = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(n, 4 * p->comm->num_sms)));
+    ck(mgw::launch_pack(p->d_tiles + p->tile_first[g], n, p->d_grads, merge_buf,
+                        p->offs[p->heads[g]], scale, ctas, static_cast<cudaStream_t>(stream)),
+       "pack launch");
+    mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  MGW_CATCH
+}
+
+int mgw_unpack_sgd(mgw_plan* p, int g, const float* merge_buf, float lr, int write_grad,
+                   void* stream) {
+  MGW_TRY {
+    require(p != nullptr && merge_buf != nullptr && g >= 0 && g < p->G(), "bad unpack arguments");
+    mgw::set_device(p->comm);
+    const uint32_t n = p->tile_first[g + 1] - p->tile_first[g];
+    const int ctas = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(n, 4 * p->comm->num_sms)));
+    const int epi = MGW_SGD | (write_grad ? MGW_WRITE_GRAD : 0);
+    ck(mgw::launch_unpack_sgd(p->d_tiles + p->tile_first[g], n, p->d_grads, p->d_weights,
+                              merge_buf, p->offs[p->heads[g]], lr, epi, ctas,
+                              static_cast<cudaStream_t>(stream)),
+       "unpack launch");
+    mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  MGW_CATCH
+}
+
+int mgw_group_allreduce(mgw_plan* p, int g, float lr, int epilogue, int algo, void* stream) {
+  MGW_TRY {
+    require(p != nullptr, "plan is NULL");
+    mgw::set_device(p->comm);
+    mgw::launch_group(p, g, lr, epilogue, algo, static_cast<cudaStream_t>(stream));
+  }
+  MGW_CATCH
+}
+
+int mgw_allreduce(mgw_comm* c, float* buf, size_t n, int algo, void* stream) {
+  MGW_TRY {
+    require(c != nullptr && buf != nullptr && n > 0 && !c->loopback, "bad all-reduce arguments");
+    mgw::set_device(c);
+    if (c->ar_plan == nullptr || c->ar_buf != buf || c->ar_n != n) {
+      mgw::destroy_plan(c->ar_plan);
+      c->ar_plan = nullptr;
+      const uint64_t cnt = n;
+      const uint8_t tag = 0;
+      float* g[1] = {buf};
+      c->ar_plan = mgw::build_plan(c, 1, g, nullptr, &cnt, &tag);
+      c->ar_buf = buf;
+      c->ar_n = n;
+    }
+    // A plain SUM all-reduce: same kernel, pack scale 1, result written
+    // back into buf, no SGD.
+    mgw_plan* p = c->ar_plan;
+    mgw::GroupLaunch L{};
+    L.tiles = p->d_tiles;
+    L.n_tiles = p->tile_first[1];
+    L.nranks = c->nranks;
+    L.scale = 1.0f;
+    L.lr = 0.0f;
+    L.epilogue = MGW_WRITE_GRAD;
+    L.copy_stride = c->arena_elems;
+    L.views[0] = mgw::make_view(c, 0, p->d_grads, p->d_weights);
+    const bool two = mgw::use_two_shot(c, static_cast<uint64_t>(n) * 4, algo);
+    ck(mgw::launch_group_allreduce(L, mgw::grid_for(c, L.n_tiles, two), two, false,
+                                   static_cast<cudaStream_t>(stream)),
+       "allreduce launch");
+    mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  MGW_CATCH
+}
+
+int mgw_calibrate(mgw_comm* c, const uint64_t* sizes, size_t n, int warmup, int reps, int algo,
+                  mgw_meas* out) {
+  MGW_TRY {
+    require(c != nullptr && sizes != nullptr && out != nullptr && reps >= 1, "bad calibrate args");
+    require(!c->loopback, "calibration runs on a real communicator");
+    mgw::set_device(c);
+    uint64_t max_bytes = 16;
+    for (size_t i = 0; i < n; ++i) max_bytes = std::max(max_bytes, sizes[i]);
+    const size_t max_elems = (max_bytes + 3) / 4;
+    float* grad = nullptr;
+    float* w = nullptr;
+    ck(cudaMalloc(&grad, max_elems * sizeof(float)), "cudaMalloc(calib grad)");
+    ck(cudaMalloc(&w, max_elems * sizeof(float)), "cudaMalloc(calib w)");
+    ck(cudaMemset(grad, 0, max_elems * sizeof(float)), "memset");
+    ck(cudaMemset(w, 0, max_elems * sizeof(float)), "memset");
+    std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(reps));
+    for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    std::vector<float> ms(reps);
+    try {
+      for (size_t i = 0; i < n; ++i) {
+        const uint64_t cnt = (sizes[i] + 3) / 4;
+        const uint8_t tag = 0;
+        float* gp[1] = {grad};
+        float* wp[1] = {w};
+        mgw_plan* p = mgw::build_plan(c, 1, gp, wp, &cnt, &tag);
+        for (int k = 0; k < warmup; ++k) mgw::launch_group(p, 0, 0.0f, MGW_SGD, algo, c->stream);
+        for (int k = 0; k < reps; ++k) {
+          ck(cudaEventRecord(ev[2 * k], c->stream), "record");
+          mgw::launch_group(p, 0, 0.0f, MGW_SGD, algo, c->stream);
+          ck(cudaEventRecord(ev[2 * k + 1], c->stream), "record");
+        }
+        ck(cudaStreamSynchronize(c->stream), "calibrate sync");
+        for (int k = 0; k < reps; ++k) {
+          ck(cudaEventElapsedTime(&ms[k], ev[2 * k], ev[2 * k + 1]), "elapsed");
+        }
+        std::sort(ms.begin(), ms.end());
+        const double med = reps % 2 ? ms[reps / 2] : 0.5 * (ms[reps / 2 - 1] + ms[reps / 2]);
+        out[i].size_bytes = sizes[i];
+        out[i].time_sec = med * 1e-3;
+        mgw::destroy_plan(p);
+      }
+      mgw::check_barrier_flags(c);
+    } catch (...) {
+      for (auto& e : ev) cudaEventDestroy(e);
+      cudaFree(grad);
+      cudaFree(w);
+      throw;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaFree(grad);
+    cudaFree(w);
+  }
+  MGW_CATCH
+}
+
+int mgw_pipeline_create(mgw_plan* p, const double* t_b, double t_f, float lr, int algo,
+                        int record_group_times, size_t l2_flush_bytes, mgw_pipeline** out) {
+  MGW_TRY {
+    require(p != nullptr && t_b != nullptr && out != nullptr, "bad pipeline arguments");
+    require(!p->comm->loopback, "pipelines run on a real communicator");
+    require(t_f >= 0.0, "t_f must be >= 0");
+    mgw::set_device(p->comm);
+    const size_t L = p->L;
+    // Ready time of every layer, reference timeline.hpp:99-108 / planner.hpp:67-70.
+    std::vector<double> tau_b(L);
+    tau_b[L - 1] = t_f;
+    for (size_t i = L - 1; i-- > 0;) tau_b[i] = tau_b[i + 1] + t_b[i + 1];
+
+    auto* pipe = new mgw_pipeline();
+    pipe->plan = p;
+    pipe->timed_groups = record_group_times != 0;
+    const int G = p->G();
+    ck(cudaStreamCreateWithFlags(&pipe->compute, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&pipe->comm, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&pipe->fork, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&pipe->join, cudaEventDisableTiming), "event");
+    pipe->ready.resize(G);
+    for (auto& e : pipe->ready) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    if (pipe->timed_groups) {
+      pipe->g_start.resize(G);
+      pipe->g_end.resize(G);
+      for (auto& e : pipe->g_start) ck(cudaEventCreate(&e), "event");
+      for (auto& e : pipe->g_end) ck(cudaEventCreate(&e), "event");
+    }
+    ck(cudaMalloc(&pipe->d_clock, 2 * sizeof(unsigned long long)), "cudaMalloc(clock)");
+    ck(cudaMemset(pipe->d_clock, 0, 2 * sizeof(unsigned long long)), "memset(clock)");
+    if (l2_flush_bytes > 0) {
+      ck(cudaMalloc(&pipe->flush_buf, l2_flush_bytes), "cudaMalloc(l2 flush)");
+      pipe->flush_bytes = l2_flush_bytes;
+    }
+
+    ck(cudaStreamBeginCapture(pipe->compute, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+      ck(cudaEventRecord(pipe->fork, pipe->compute), "fork");
+      ck(cudaStreamWaitEvent(pipe->comm, pipe->fork, 0), "fork wait");
+      if (pipe->flush_bytes > 0) {
+        // The comm stream is idle until the first group is ready: evict L2
+        // there while the compute stream replays the forward pass.
+        ck(cudaMemsetAsync(pipe->flush_buf, pipe->iter_flush_value, pipe->flush_bytes, pipe->comm),
+           "l2 flush");
+      }
+      bool first = true;
+      for (int g = G - 1; g >= 0; --g) {
+        const size_t head = p->heads[g];
+        const double ready_s = tau_b[head] + t_b[head];
+        const auto deadline = static_cast<unsigned long long>(std::llround(ready_s * 1e9));
+        ck(mgw::launch_replay(pipe->d_clock, deadline, first ? 1 : 0, pipe->compute), "replay");
+        first = false;
+        ck(cudaEventRecord(pipe->ready[g], pipe->compute), "ready");
+        ck(cudaStreamWaitEvent(pipe->comm, pipe->ready[g], 0), "ready wait");
+        if (pipe->timed_groups) {
+          ck(cudaEventRecordWithFlags(pipe->g_start[g], pipe->comm, cudaEventRecordExternal),
+             "group start");
+        }
+        mgw::launch_group(p, g, lr, MGW_SGD, algo, pipe->comm);
+        if (pipe->timed_groups) {
+          ck(cudaEventRecordWithFlags(pipe->g_end[g], pipe->comm, cudaEventRecordExternal),
+             "group end");
+        }
+      }
+      ck(cudaEventRecord(pipe->join, pipe->comm), "join");
+      ck(cudaStreamWaitEvent(pipe->compute, pipe->join, 0), "join wait");
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(pipe->compute, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    ck(cudaStreamEndCapture(pipe->compute, &pipe->graph), "end capture");
+    ck(cudaGraphInstantiate(&pipe->exec, pipe->graph, 0), "graph instantiate");
+    // the capture counted kernels once; graph replays add per launch
+    mgw::g_kernel_launches.fetch_sub(static_cast<uint64_t>(G), std::memory_order_relaxed);
+    pipe->kernels_per_iter = 2 * G;
+    *out = pipe;
+  }
+  MGW_CATCH
+}
+
+int mgw_pipeline_destroy(mgw_pipeline* pipe) {
+  MGW_TRY {
+    if (pipe == nullptr) return 0;
+    cudaSetDevice(pipe->plan->comm->device);
+    cudaStreamSynchronize(pipe->compute);
+    if (pipe->exec) cudaGraphExecDestroy(pipe->exec);
+    if (pipe->graph) cudaGraphDestroy(pipe->graph);
+    for (auto e : pipe->ready) cudaEventDestroy(e);
+    for (auto e : pipe->g_start) cudaEventDestroy(e);
+    for (auto e : pipe->g_end) cudaEventDestroy(e);
+    cudaEventDestroy(pipe->fork);
+    cudaEventDestroy(pipe->join);
+    cudaFree(pipe->d_clock);
+    if (pipe->flush_buf) cudaFree(pipe->flush_buf);
+    cudaStreamDestroy(pipe->compute);
+    cudaStreamDestroy(pipe->comm);
+    delete pipe;
+  }
+  MGW_CATCH
+}
+
+int mgw_pipeline_launch(mgw_pipeline* pipe, int iters) {
+  MGW_TRY {
+    require(pipe != nullptr && iters >= 0, "bad pipeline launch");
+    mgw::set_device(pipe->plan->comm);
+    for (int i = 0; i < iters; ++i) {
+      ck(cudaGraphLaunch(pipe->exec, pipe->compute), "graph launch");
+      mgw::g_kernel_launches.fetch_add(pipe->kernels_per_iter, std::memory_order_relaxed);
+    }
+  }
+  MGW_CATCH
+}
+
+int mgw_pipeline_run(mgw_pipeline* pipe, int iters, float* iter_ms) {
+  MGW_TRY {
+    require(pipe != nullptr && iters >= 1 && iter_ms != nullptr, "bad pipeline run");
+    mgw::set_device(pipe->plan->comm);
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(iters) + 1);
+    for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    try {
+      ck(cudaEventRecord(ev[0], pipe->compute), "record");
+      for (int i = 0; i < iters; ++i) {
+        ck(cudaGraphLaunch(pipe->exec, pipe->compute), "graph launch");
+        mgw::g_kernel_launches.fetch_add(pipe->kernels_per_iter, std::memory_order_relaxed);
+        ck(cudaEventRecord(ev[i + 1], pipe->compute), "record");
+      }
+      ck(cudaEventSynchronize(ev[iters]), "pipeline sync");
+      for (int i = 0; i < iters; ++i) ck(cudaEventElapsedTime(&iter_ms[i], ev[i], ev[i + 1]), "elapsed");
+      mgw::check_barrier_flags(pipe->plan->comm);
+    } catch (...) {
+      for (auto e : ev) cudaEventDestroy(e);
+      throw;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  MGW_CATCH
+}
+
+int mgw_pipeline_group_times(mgw_pipeline* pipe, float* group_ms) {
+  MGW_TRY {
+    require(pipe != nullptr && group_ms != nullptr && pipe->timed_groups,
+            "pipeline was created without record_group_times");
+    mgw::set_device(pipe->plan->comm);
+    ck(cudaStreamSynchronize(pipe->compute), "sync");
+    for (size_t g = 0; g < pipe->g_start.size(); ++g) {
+      ck(cudaEventElapsedTime(&group_ms[g], pipe->g_start[g], pipe->g_end[g]), "elapsed");
+    }
+  }
+  MGW_CATCH
+}
+
+int mgw_pipeline_stream(mgw_pipeline* pipe, void** stream_out) {
+  MGW_TRY {
+    require(pipe != nullptr && stream_out != nullptr, "NULL argument");
+    *stream_out = pipe->compute;
+  }
+  MGW_CATCH
+}
+
+}  // extern "C"

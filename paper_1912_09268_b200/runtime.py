@@ -1,0 +1,203 @@
+"""Device runtime: communicator, device plans, fused merged all-reduce,
+backward-replay pipeline and calibration — thin Python handles over the C
+ABI (include/mgwfbp.h). PyTorch is used only as plumbing: device memory for
+gradients/weights, the current CUDA stream, and torch.distributed to swap
+the CUDA IPC handles once at start-up (paper Algorithm 2 line 8, Bcast).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import arr
+from .gradsched import (AllReduceModel, CommMeasurement, MergePlan, ModelTrace, check,
+                        fit_model)
+
+ALGO = {"auto": 0, "oneshot": 1, "twoshot": 2}
+SGD = 1
+WRITE_GRAD = 2
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def padded_elems(counts: Sequence[int]) -> int:
+    """Merge-layout size: every layer starts on a 16-byte boundary."""
+    return sum((int(c) + 3) & ~3 for c in counts)
+
+
+class Comm:
+    """One rank's communicator (or a single-GPU loopback of `nranks` ranks)."""
+
+    def __init__(self, rank: int, nranks: int, device: int, arena_bytes: int,
+                 group=None, loopback: bool = False):
+        self.rank, self.nranks, self.device = rank, nranks, device
+        self.loopback = loopback
+        h = C.c_void_p()
+        if loopback:
+            check(_lib.mgw_comm_create_loopback(nranks, device, arena_bytes, C.byref(h)))
+        else:
+            check(_lib.mgw_comm_create(rank, nranks, device, arena_bytes, C.byref(h)))
+        self.handle = h
+        if not loopback and nranks > 1:
+            self._exchange(group)
+
+    @classmethod
+    def create_loopback(cls, nranks: int, device: int, arena_bytes: int) -> "Comm":
+        return cls(0, nranks, device, arena_bytes, loopback=True)
+
+    def _exchange(self, group) -> None:
+        import torch.distributed as dist
+
+        size = _lib.mgw_comm_handle_size()
+        blob = (C.c_uint8 * size)()
+        check(_lib.mgw_comm_export_handle(self.handle, blob))
+        gathered: List[Optional[bytes]] = [None] * self.nranks
+        dist.all_gather_object(gathered, bytes(blob), group=group)
+        allb = b"".join(gathered)
+        buf = (C.c_uint8 * len(allb)).from_buffer_copy(allb)
+        check(_lib.mgw_comm_open_peers(self.handle, buf))
+
+    def set_oneshot_max(self, nbytes: int) -> None:
+        check(_lib.mgw_comm_set_oneshot_max(self.handle, int(nbytes)))
+
+    def allreduce_(self, buf: torch.Tensor, algo: str = "auto", stream=None) -> torch.Tensor:
+        """In-place SUM all-reduce (rank order) of a contiguous fp32 tensor."""
+        assert buf.dtype == torch.float32 and buf.is_cuda and buf.is_contiguous()
+        check(_lib.mgw_allreduce(self.handle, buf.data_ptr(), buf.numel(), ALGO[algo], _stream_ptr(stream)))
+        return buf
+
+    def calibrate(self, sizes: Sequence[int], warmup: int = 3, reps: int = 20,
+                  algo: str = "auto") -> List[CommMeasurement]:
+        """N1: on-box fused all-reduce size sweep; median seconds per size."""
+        out = (_lib.Meas * len(sizes))()
+        check(_lib.mgw_calibrate(self.handle, arr(C.c_uint64, sizes), len(sizes), warmup, reps,
+                                 ALGO[algo], out))
+        return [CommMeasurement(out[i].size_bytes, out[i].time_sec) for i in range(len(sizes))]
+
+    def close(self) -> None:
+        if self.handle:
+            check(_lib.mgw_comm_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DevicePlan:
+    """A merge plan bound to this rank's gradient / weight tensors.
+
+    grads / weights: one fp32 CUDA tensor per layer in forward order (for a
+    loopback comm: a list per emulated rank).
+    """
+
+    def __init__(self, comm: Comm, grads, weights, plan: MergePlan):
+        self.comm = comm
+        if comm.loopback:
+            assert len(grads) == comm.nranks
+            flat_g = [t for per in grads for t in per]
+            flat_w = [t for per in weights for t in per] if weights is not None else None
+            L = len(grads[0])
+        else:
+            flat_g, flat_w, L = list(grads), (list(weights) if weights is not None else None), len(grads)
+        self.L = L
+        self._keep = (flat_g, flat_w)  # tensors must outlive the plan
+        counts = [int(t.numel()) for t in flat_g[:L]]
+        self.counts = counts
+        gp = arr(C.c_void_p, (t.data_ptr() for t in flat_g))
+        wp = arr(C.c_void_p, (t.data_ptr() for t in flat_w)) if flat_w is not None else None
+        h = C.c_void_p()
+        check(_lib.mgw_plan_create(comm.handle, L, gp, wp, arr(C.c_uint64, counts),
+                                   arr(C.c_uint8, (int(t) for t in plan.tags)), C.byref(h)))
+        self.handle = h
+        n = C.c_int()
+        check(_lib.mgw_plan_num_groups(h, C.byref(n)))
+        self.n_groups = n.value
+
+    def group_span(self, g: int) -> Tuple[int, int, int]:
+        b, c, by = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(_lib.mgw_plan_group_span(self.handle, g, C.byref(b), C.byref(c), C.byref(by)))
+        return b.value, c.value, by.value
+
+    def pack(self, g: int, scale: float, merge_buf: torch.Tensor, stream=None) -> None:
+        check(_lib.mgw_pack(self.handle, g, scale, merge_buf.data_ptr(), _stream_ptr(stream)))
+
+    def unpack_sgd(self, g: int, merge_buf: torch.Tensor, lr: float, write_grad: bool = False,
+                   stream=None) -> None:
+        check(_lib.mgw_unpack_sgd(self.handle, g, merge_buf.data_ptr(), lr, int(write_grad),
+                                  _stream_ptr(stream)))
+
+    def group_allreduce(self, g: int, lr: float, epilogue: int = SGD, algo: str = "auto",
+                        stream=None) -> None:
+        check(_lib.mgw_group_allreduce(self.handle, g, lr, epilogue, ALGO[algo], _stream_ptr(stream)))
+
+    def close(self) -> None:
+        if self.handle:
+            check(_lib.mgw_plan_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Pipeline:
+    """Paper Algorithm 2 on one GPU: backward replay on a compute stream,
+    each merge group's fused all-reduce on a comm stream the moment its head
+    layer is ready, one CUDA graph per iteration."""
+
+    def __init__(self, dplan: DevicePlan, trace: ModelTrace, lr: float, algo: str = "auto",
+                 record_group_times: bool = False, l2_flush_bytes: int = 0):
+        self.dplan = dplan
+        tb = arr(C.c_double, (l.backward_time for l in trace.layers))
+        h = C.c_void_p()
+        check(_lib.mgw_pipeline_create(dplan.handle, tb, float(trace.forward_time), lr, ALGO[algo],
+                                       int(record_group_times), int(l2_flush_bytes), C.byref(h)))
+        self.handle = h
+        s = C.c_void_p()
+        check(_lib.mgw_pipeline_stream(h, C.byref(s)))
+        self.stream = torch.cuda.ExternalStream(s.value, device=torch.device("cuda", dplan.comm.device))
+
+    def launch(self, iters: int = 1) -> None:
+        check(_lib.mgw_pipeline_launch(self.handle, iters))
+
+    def run(self, iters: int) -> List[float]:
+        out = (C.c_float * iters)()
+        check(_lib.mgw_pipeline_run(self.handle, iters, out))
+        return list(out)
+
+    def group_times_ms(self) -> List[float]:
+        out = (C.c_float * max(1, self.dplan.n_groups))()
+        check(_lib.mgw_pipeline_group_times(self.handle, out))
+        return list(out)[: self.dplan.n_groups]
+
+    def close(self) -> None:
+        if self.handle:
+            check(_lib.mgw_pipeline_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def kernel_launches() -> int:
+    return int(_lib.mgw_kernel_launches())
+
+
+def calibrated_model(comm: Comm, sizes: Sequence[int], warmup: int = 3, reps: int = 20,
+                     algo: str = "auto") -> Tuple[AllReduceModel, List[CommMeasurement]]:
+    meas = comm.calibrate(sizes, warmup, reps, algo)
+    return fit_model(meas), meas

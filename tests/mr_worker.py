@@ -1,0 +1,108 @@
+"""Multi-GPU parity worker (launched by tests/test_gpu_multirank.py through
+torch.distributed.run, one process per GPU, NCCL for the plumbing).
+
+Every rank builds seeded gradients/weights, maps the peers' merge arenas
+over NVLink (CUDA IPC), runs the fused per-group all-reduce (one-shot,
+two-shot, auto) for several iterations, and checks the result bit-for-bit
+against the CPU oracle fed with ALL ranks' inputs (regenerated locally from
+the seeds). Also: plain SUM all-reduce vs NCCL (norm-wise bound), a pipeline
+run, and a calibration sweep whose fit must be usable by the planner.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import pyoracle  # noqa: E402
+from paper_1912_09268_b200 import dist as D  # noqa: E402
+from paper_1912_09268_b200 import gradsched as gs  # noqa: E402
+from paper_1912_09268_b200 import runtime as rt  # noqa: E402
+
+COUNTS = [1000, 0, 7, 9000, 4096, 13, 200000, 1, 4097, 3, 3_000_000]
+LR = 0.01
+
+
+def inputs(P):
+    g = [[np.random.default_rng(0x5EED0000 + r).uniform(-1, 1, c).astype(np.float32) for c in COUNTS]
+         for r in range(P)]
+    w = [[np.random.default_rng(0xC0FFEE).uniform(-1, 1, c).astype(np.float32) for c in COUNTS]
+         for _ in range(P)]
+    return g, w
+
+
+def main():
+    rank, P, local = D.init("nccl")
+    torch.cuda.set_device(local)
+    rng = np.random.default_rng(9)
+    t_b = list(rng.uniform(1e-5, 4e-4, len(COUNTS)))
+    tr = gs.trace_from_arrays(COUNTS, t_b, 1e-3)
+    plan = gs.optimal_plan(tr, gs.AllReduceModel(2e-5, 1 / 500e9))
+    D.agree_plan(plan.tags)
+    tags = [int(t) for t in plan.tags]
+    comm = rt.Comm(rank, P, local, 4 * rt.padded_elems(COUNTS))
+    comm.set_oneshot_max(64 * 1024)
+    failures = []
+    for algo in ("oneshot", "twoshot", "auto"):
+        g_np, w_np = inputs(P)
+        g_dev = [torch.from_numpy(a.copy()).cuda() for a in g_np[rank]]
+        w_dev = [torch.from_numpy(a.copy()).cuda() for a in w_np[rank]]
+        dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+        for _ in range(3):
+            for g in reversed(range(dp.n_groups)):
+                dp.group_allreduce(g, LR, rt.SGD | rt.WRITE_GRAD, algo)
+            pyoracle.allreduce_sgd(g_np, w_np, tags, LR, write_grad=True)
+        torch.cuda.synchronize()
+        for l in range(len(COUNTS)):
+            if not np.array_equal(w_dev[l].cpu().numpy(), w_np[rank][l]):
+                failures.append(f"{algo} weights layer {l}")
+            if not np.array_equal(g_dev[l].cpu().numpy(), g_np[rank][l]):
+                failures.append(f"{algo} grads layer {l}")
+        dp.close()
+
+    # plain SUM all-reduce vs NCCL: bit-exact is not expected (NCCL's order
+    # differs); bound |x - y| <= 1e-6 * sum_r |x_r| (SURVEY §7 vii)
+    for n in (1 << 10, (1 << 20) + 3, 16 << 20):
+        x = torch.rand(n, device="cuda") * 2 - 1 + rank
+        mine, ref = x.clone(), x.clone()
+        comm.allreduce_(mine)
+        dist.all_reduce(ref)
+        absx = x.abs()
+        dist.all_reduce(absx)
+        torch.cuda.synchronize()
+        if not bool(((mine - ref).abs() <= 1e-6 * absx + 1e-30).all()):
+            failures.append(f"allreduce vs nccl n={n}")
+
+    # pipeline at P ranks
+    g_dev = [torch.rand(c, device="cuda") for c in COUNTS]
+    w_dev = [torch.rand(c, device="cuda") for c in COUNTS]
+    dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+    pipe = rt.Pipeline(dp, tr, LR, record_group_times=True)
+    ms = pipe.run(5)
+    compute_ms = (tr.forward_time + sum(t_b)) * 1e3
+    if not all(m >= compute_ms * 0.999 for m in ms):
+        failures.append(f"pipeline faster than its compute: {ms} < {compute_ms}")
+    pipe.close()
+    dp.close()
+
+    meas = comm.calibrate([4096 << k for k in range(0, 14, 2)], warmup=2, reps=5)
+    try:
+        gs.fit_model(meas)
+    except gs.FitError as e:
+        failures.append(f"calibration fit: {e}")
+    comm.close()
+    out = [None] * P
+    dist.all_gather_object(out, failures)
+    if rank == 0:
+        bad = [f for per in out for f in per]
+        print("MULTIRANK", "OK" if not bad else "FAIL", bad, flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,113 @@
+"""CPU checks of the boundary and the reduction oracle (no GPU compute):
+  * libmgwfbp.so loads and exports every symbol include/*.h declares;
+  * the C-ABI status/exception mapping mirrors the reference classes;
+  * the oracle's pack / rank-order reduction / SGD agrees with an
+    independent numpy float32 statement of the same semantics.
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from oracle import pyoracle
+from paper_1912_09268_b200 import _lib
+from paper_1912_09268_b200 import gradsched as gs
+
+
+def _declared_symbols():
+    syms = set()
+    for fn in os.listdir(os.path.join(ROOT, "include")):
+        if fn.endswith(".h"):
+            text = open(os.path.join(ROOT, "include", fn)).read()
+            syms |= set(re.findall(r"\b(mgw_[a-z0-9_]+)\s*\(", text))
+    return syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    declared = _declared_symbols()
+    assert len(declared) >= 35
+    missing = [s for s in sorted(declared) if not hasattr(lib, s)]
+    assert not missing, missing
+    # and the Python binding covers all of them
+    assert declared <= set(_lib.EXPORTED), sorted(declared - set(_lib.EXPORTED))
+
+
+def test_version_and_error_kind():
+    assert b"sm_100a" in _lib.mgw_version()
+    with pytest.raises(gs.ParseError, match="cannot open"):
+        gs.load_trace("/nonexistent/trace.json")
+    with pytest.raises(gs.ParseError, match="header"):
+        p = os.path.join(ROOT, "tests", "golden", "three_layer.json")
+        gs.load_measurements_csv(p)
+
+
+def test_device_api_without_gpu_fails_loudly_not_silently():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by -m gpu tests")
+    h = ctypes.c_void_p()
+    rc = _lib.mgw_comm_create(0, 1, 0, 1 << 20, ctypes.byref(h))
+    assert rc == 6  # MGW_ERR_CUDA: no device, no CPU fallback
+    assert _lib.mgw_last_error_kind() == b"CudaError"
+
+
+def test_merge_offsets_are_16_byte_aligned():
+    counts = [7, 0, 1, 4, 4097, 3]
+    offs = pyoracle.merge_offsets(counts)
+    assert offs == [0, 8, 8, 12, 16, 4116, 4120]
+    assert all(o % 4 == 0 for o in offs)
+
+
+def _np_reduce(grads, weights, lr, P):
+    s = np.float32(1.0 / P)
+    out_w, out_g = [], []
+    for l in range(len(grads[0])):
+        acc = (grads[0][l] * s).astype(np.float32)
+        for r in range(1, P):
+            acc = (acc + (grads[r][l] * s).astype(np.float32)).astype(np.float32)
+        step = (np.float32(lr) * acc).astype(np.float32)
+        out_w.append([(weights[r][l] - step).astype(np.float32) for r in range(P)])
+        out_g.append(acc)
+    return out_w, out_g
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_oracle_reduction_matches_numpy_rank_order(P):
+    rng = np.random.default_rng(P)
+    counts = [0, 1, 7, 4096, 5000, 33]
+    grads = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(P)]
+    weights = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(P)]
+    want_w, want_g = _np_reduce(grads, weights, 0.01, P)
+    pyoracle.allreduce_sgd(grads, weights, [0, 1, 0, 1, 1, 0], 0.01, write_grad=True)
+    for l in range(len(counts)):
+        for r in range(P):
+            assert np.array_equal(weights[r][l], want_w[l][r])
+            assert np.array_equal(grads[r][l], want_g[l])
+
+
+def test_oracle_pack_layout():
+    rng = np.random.default_rng(7)
+    grads = [rng.uniform(-1, 1, c).astype(np.float32) for c in (5, 0, 9)]
+    out = pyoracle.pack(grads, 0, 3, 0.5)
+    assert out.size == 8 + 0 + 12
+    assert np.array_equal(out[:5], (grads[0] * np.float32(0.5)).astype(np.float32))
+    assert np.all(out[5:8] == 0)
+    assert np.array_equal(out[8:17], (grads[2] * np.float32(0.5)).astype(np.float32))
+    assert np.all(out[17:] == 0)
+
+
+def test_cpu_pipeline_runs_and_respects_replay_time():
+    counts = [1000, 2000, 0, 500]
+    t_b = [2e-3, 1e-3, 1e-3, 1e-3]
+    grads = [[np.ones(c, np.float32) for c in counts]]
+    weights = [[np.zeros(c, np.float32) for c in counts]]
+    times = pyoracle.pipeline_run(grads, weights, counts, t_b, 1e-3, [0, 1, 0, 0], 0.5, 2, 3)
+    assert len(times) == 3
+    assert all(t >= 6e-3 for t in times)  # t_f + sum(t_b) replayed
+    # 3 iterations of w -= 0.5 * 1 (P=1)
+    assert np.all(weights[0][0] == -1.5)

@@ -1,0 +1,204 @@
+"""GPU parity of the sm_100a kernels against the CPU oracle (bit-exact) and,
+at full size, against a plain torch fp32 rank-order reference.
+
+Multi-rank collectives are exercised on ONE B200 through the loopback
+communicator: P emulated ranks, every collective one cooperative launch
+(never P launches that wait on each other). The multi-GPU path is
+tests/test_gpu_multirank.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import pyoracle
+from paper_1912_09268_b200 import gradsched as gs
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_1912_09268_b200 import runtime as rt
+
+RAGGED = [1000, 0, 7, 9000, 4096, 13, 20000, 1, 4097, 3]
+LR = 0.01
+
+
+def _np(rng, counts, P):
+    return [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(P)]
+
+
+def _dev(arrays):
+    return [[torch.from_numpy(a.copy()).cuda() for a in per] for per in arrays]
+
+
+def _plan_for(counts, seed=1):
+    rng = np.random.default_rng(seed)
+    t_b = list(rng.uniform(1e-5, 5e-4, len(counts)))
+    tr = gs.trace_from_arrays(counts, t_b, 1e-3)
+    return tr, gs.optimal_plan(tr, gs.AllReduceModel(3e-5, 1e-9))
+
+
+def test_pack_kernel_bit_exact_incl_unaligned_views():
+    rng = np.random.default_rng(11)
+    counts = RAGGED
+    g_np = _np(rng, counts, 1)[0]
+    # layer 2 is an unaligned view (offset by one float) to force the scalar path
+    base = torch.from_numpy(np.concatenate([[0.0], g_np[2]]).astype(np.float32)).cuda()
+    g_dev = [torch.from_numpy(a).cuda() for a in g_np]
+    g_dev[2] = base[1:]
+    tr, plan = _plan_for(counts)
+    comm = rt.Comm(0, 1, 0, 4 * rt.padded_elems(counts))
+    dp = rt.DevicePlan(comm, g_dev, None, plan)
+    offs = pyoracle.merge_offsets(counts)
+    for g, members in enumerate(plan.groups()):
+        b, n, nbytes = dp.group_span(g)
+        assert b == offs[members[0]] and n == offs[members[-1] + 1] - b
+        assert nbytes == 4 * sum(counts[i] for i in members)
+        out = torch.full((max(n, 1),), float("nan"), device="cuda")
+        dp.pack(g, 0.25, out)
+        torch.cuda.synchronize()
+        want = pyoracle.pack(g_np, members[0], members[-1] + 1, 0.25)
+        assert np.array_equal(out[:n].cpu().numpy(), want), g
+    dp.close()
+    comm.close()
+
+
+def test_unpack_sgd_kernel_bit_exact():
+    rng = np.random.default_rng(12)
+    counts = RAGGED
+    g_np = _np(rng, counts, 1)[0]
+    w_np = _np(rng, counts, 1)[0]
+    g_dev = [torch.from_numpy(a.copy()).cuda() for a in g_np]
+    w_dev = [torch.from_numpy(a.copy()).cuda() for a in w_np]
+    _, plan = _plan_for(counts)
+    comm = rt.Comm(0, 1, 0, 4 * rt.padded_elems(counts))
+    dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+    for g, members in enumerate(plan.groups()):
+        b, n, _ = dp.group_span(g)
+        red_np = rng.uniform(-1, 1, max(n, 1)).astype(np.float32)
+        dp.unpack_sgd(g, torch.from_numpy(red_np).cuda(), LR, write_grad=True)
+        torch.cuda.synchronize()
+        offs = pyoracle.merge_offsets(counts)
+        for l in members:
+            r = red_np[offs[l] - b: offs[l] - b + counts[l]]
+            want_w = (w_np[l] - (np.float32(LR) * r).astype(np.float32)).astype(np.float32)
+            assert np.array_equal(w_dev[l].cpu().numpy(), want_w), l
+            assert np.array_equal(g_dev[l].cpu().numpy(), r), l
+    dp.close()
+    comm.close()
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+@pytest.mark.parametrize("algo", ["oneshot", "twoshot", "auto"])
+def test_fused_group_allreduce_bit_exact_vs_oracle(P, algo):
+    if P == 1 and algo != "auto":
+        pytest.skip("P=1 has no exchange")
+    rng = np.random.default_rng(100 + P)
+    counts = RAGGED
+    g_np, w_np = _np(rng, counts, P), _np(rng, counts, P)
+    g_dev, w_dev = _dev(g_np), _dev(w_np)
+    _, plan = _plan_for(counts, seed=P)
+    tags = [int(t) for t in plan.tags]
+    if P == 1:
+        comm = rt.Comm(0, 1, 0, 4 * rt.padded_elems(counts))
+        dp = rt.DevicePlan(comm, g_dev[0], w_dev[0], plan)
+    else:
+        comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
+        comm.set_oneshot_max(16 * 1024)  # auto: small groups one-shot, big two-shot
+        dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+    # three iterations (exercises the epoch counter and arena parity)
+    for it in range(3):
+        for g in reversed(range(dp.n_groups)):
+            dp.group_allreduce(g, LR, rt.SGD | rt.WRITE_GRAD, algo)
+        pyoracle.allreduce_sgd(g_np, w_np, tags, LR, write_grad=True)
+    torch.cuda.synchronize()
+    for r in range(P):
+        for l in range(len(counts)):
+            assert np.array_equal(w_dev[r][l].cpu().numpy(), w_np[r][l]), (r, l)
+            assert np.array_equal(g_dev[r][l].cpu().numpy(), g_np[r][l]), (r, l)
+    dp.close()
+    comm.close()
+
+
+@pytest.mark.parametrize("P,algo", [(8, "twoshot"), (8, "oneshot"), (4, "twoshot"), (2, "twoshot")])
+def test_large_message_matches_torch_fp32_rank_order(P, algo):
+    """64 MiB per rank, 3 layers: bit-exact against torch fp32 elementwise
+    ops in rank order (separate mul/add kernels, no FMA)."""
+    torch.manual_seed(P)
+    counts = [16 * 1024 * 1024 - 5, 3, 1 << 20]
+    grads = [[torch.rand(c, device="cuda") * 2 - 1 for c in counts] for _ in range(P)]
+    weights = [[torch.rand(c, device="cuda") for c in counts] for _ in range(P)]
+    s = torch.tensor(1.0 / P, device="cuda")
+    lr = torch.tensor(LR, device="cuda")
+    want_w = []
+    for l in range(len(counts)):
+        acc = grads[0][l] * s
+        for r in range(1, P):
+            acc = acc + grads[r][l] * s
+        want_w.append([weights[r][l] - lr * acc for r in range(P)])
+    comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
+    plan = gs.MergePlan.all_merged(len(counts))
+    dp = rt.DevicePlan(comm, grads, weights, plan)
+    dp.group_allreduce(0, LR, rt.SGD, algo)
+    torch.cuda.synchronize()
+    for l in range(len(counts)):
+        for r in range(P):
+            assert torch.equal(weights[r][l], want_w[l][r]), (l, r)
+    dp.close()
+    comm.close()
+
+
+def test_zero_byte_group_is_a_noop_launch():
+    counts = [100, 0, 0, 50]
+    tags = [0, 0, 1, 0]  # group 1 = layers 1..2, zero bytes
+    g = [[torch.ones(c, device="cuda") for c in counts] for _ in range(2)]
+    w = [[torch.zeros(c, device="cuda") for c in counts] for _ in range(2)]
+    comm = rt.Comm.create_loopback(2, 0, 4 * rt.padded_elems(counts))
+    dp = rt.DevicePlan(comm, g, w, gs.MergePlan([gs.LayerTag(t) for t in tags]))
+    assert dp.n_groups == 3 and dp.group_span(1)[2] == 0
+    for gi in reversed(range(3)):
+        dp.group_allreduce(gi, 1.0, rt.SGD)
+    torch.cuda.synchronize()
+    assert torch.all(w[0][0] == -1.0) and torch.all(w[1][3] == -1.0)
+    dp.close()
+    comm.close()
+
+
+def test_plain_allreduce_p1_is_identity_and_calibration_fits():
+    comm = rt.Comm(0, 1, 0, 64 << 20)
+    x = torch.randn(1000003, device="cuda")
+    y = x.clone()
+    comm.allreduce_(y)
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+    sizes = [4096 << k for k in range(0, 13, 2)]
+    model, meas = rt.calibrated_model(comm, sizes, warmup=2, reps=5)
+    assert all(m.time_sec > 0 for m in meas)
+    assert meas[-1].time_sec > meas[0].time_sec
+    assert model.a > 0 and model.b >= 0
+    comm.close()
+
+
+def test_pipeline_p1_replays_backward_and_applies_sgd():
+    rng = np.random.default_rng(5)
+    counts = RAGGED
+    t_b = list(rng.uniform(5e-5, 3e-4, len(counts)))
+    tr = gs.trace_from_arrays(counts, t_b, 2e-3)
+    plan = gs.optimal_plan(tr, gs.AllReduceModel(5e-6, 1 / 3e12))
+    g_np, w_np = _np(rng, counts, 1), _np(rng, counts, 1)
+    g_dev, w_dev = _dev(g_np), _dev(w_np)
+    comm = rt.Comm(0, 1, 0, 4 * rt.padded_elems(counts))
+    dp = rt.DevicePlan(comm, g_dev[0], w_dev[0], plan)
+    pipe = rt.Pipeline(dp, tr, LR, record_group_times=True, l2_flush_bytes=64 << 20)
+    ms = pipe.run(4)
+    compute_ms = (tr.forward_time + sum(t_b)) * 1e3
+    assert all(m >= compute_ms * 0.999 for m in ms), (ms, compute_ms)
+    assert all(m < compute_ms + 2.0 for m in ms), (ms, compute_ms)
+    gt = pipe.group_times_ms()
+    assert len(gt) == dp.n_groups and all(t > 0 for t in gt)
+    for _ in range(4):
+        pyoracle.allreduce_sgd(g_np, w_np, [int(t) for t in plan.tags], LR)
+    for l in range(len(counts)):
+        assert np.array_equal(w_dev[0][l].cpu().numpy(), w_np[0][l]), l
+    pipe.close()
+    dp.close()
+    comm.close()
