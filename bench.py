@@ -214,8 +214,8 @@ def fit_with_fallback(gs, meas):
             return gs.AllReduceModel(t0, b), "min-time startup + large-message slope"
 
 
-def calibration_sizes(total_bytes: int):
-    top = max(1 << 22, 1 << math.ceil(math.log2(max(total_bytes, 1))))
+def calibration_sizes(total_bytes: int, arena_bytes: int):
+    top = min(arena_bytes, max(1 << 22, 1 << math.ceil(math.log2(max(total_bytes, 1)))))
     sizes = []
     s = 4096
     while s <= top:
@@ -262,11 +262,11 @@ def main():
     weights = [torch.empty(max(c, 1), dtype=torch.float32, device=dev).uniform_(-1, 1, generator=wgen)[:c]
                for c in counts]
 
-    comm = rt.Comm(rank, N, local, 4 * padded)
+    comm = rt.Comm(rank, N, local, 4 * max(padded, 1 << 20))
     comm.set_oneshot_max(args.oneshot_max)
 
     # ---- N1: on-box calibration of the fused kernel at this N, fitted
-    sizes = calibration_sizes(total_bytes)
+    sizes = calibration_sizes(total_bytes, 4 * padded)
     meas = comm.calibrate(sizes, warmup=3, reps=15, algo=args.algo)
     tvec = torch.tensor([m.time_sec for m in meas], dtype=torch.float64, device=dev)
     if N > 1:

@@ -102,7 +102,7 @@ def main() -> None:
     # named-model traces (shapes from torchvision/transformers; see tools/extract_traces.py)
     tdir = os.path.join(ROOT, "traces")
     for fn in sorted(os.listdir(tdir)) if os.path.isdir(tdir) else []:
-        if not fn.endswith(".json"):
+        if not fn.endswith(".json") or fn == "META.json":
             continue
         with open(os.path.join(tdir, fn)) as f:
             tr = json.load(f)
