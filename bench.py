@@ -421,6 +421,14 @@ def main():
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+    # Teardown order matters: pinned host blocks used on the pipeline's
+    # stream must be released while that stream still exists.
+    torch.cuda.synchronize()
+    del host_grad, host_out
+    import gc
+
+    gc.collect()
+    torch._C._host_emptyCache()
     for p in pipes.values():
         p.close()
     for p in dplans.values():

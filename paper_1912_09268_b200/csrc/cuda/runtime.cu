@@ -81,6 +81,8 @@ struct mgw_comm {
   uint32_t* peer_signal[mgw::kMaxRanks] = {};
   bool peers_ready = false;
   cudaStream_t stream = nullptr;  // calibrate / plain all-reduce
+  unsigned long long* d_clock = nullptr;  // calibration spin clock
+  int occ_cache[2] = {0, 0};           // CTAs/SM of the one-shot / two-shot kernel
   // cached single-buffer plan for mgw_allreduce
   mgw_plan* ar_plan = nullptr;
   float* ar_buf = nullptr;
@@ -145,6 +147,8 @@ void init_common(mgw_comm* c, int device, size_t arena_bytes) {
   ck(cudaSetDevice(device), "cudaSetDevice");
   ck(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+  ck(cudaMalloc(&c->d_clock, 2 * sizeof(unsigned long long)), "cudaMalloc(clock)");
+  ck(cudaMemset(c->d_clock, 0, 2 * sizeof(unsigned long long)), "memset(clock)");
 }
 
 RankView make_view(const mgw_comm* c, int r, float* const* grads, float* const* weights) {
@@ -172,9 +176,9 @@ bool use_two_shot(const mgw_comm* c, uint64_t bytes, int algo) {
   return bytes > c->oneshot_max;
 }
 
-int grid_for(const mgw_comm* c, uint32_t n_tiles, bool two_shot) {
-  int occ = 1;
-  ck(max_ctas_per_sm(c->nranks, two_shot, c->loopback, &occ), "occupancy");
+int grid_for(mgw_comm* c, uint32_t n_tiles, bool two_shot) {
+  int& occ = c->occ_cache[two_shot ? 1 : 0];
+  if (occ == 0) ck(max_ctas_per_sm(c->nranks, two_shot, c->loopback, &occ), "occupancy");
   int cap = std::max(1, occ) * c->num_sms;
   if (c->loopback) cap = std::max(1, cap / c->nranks);
   cap = std::min(cap, kMaxCtas);
@@ -401,6 +405,7 @@ int mgw_comm_destroy(mgw_comm* c) {
     for (uint32_t* s : c->signals) cudaFree(s);
     for (uint32_t* s : c->states) cudaFree(s);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->d_clock) cudaFree(c->d_clock);
     delete c;
   }
   MGW_CATCH
@@ -542,6 +547,11 @@ int mgw_calibrate(mgw_comm* c, const uint64_t* sizes, size_t n, int warmup, int 
         float* gp[1] = {grad};
         float* wp[1] = {w};
         mgw_plan* p = mgw::build_plan(c, 1, gp, wp, &cnt, &tag);
+        // Hold the stream with a spin so every rep below is already queued
+        // when the GPU reaches it: the event-to-event times then measure
+        // the device-side cost (kernel + stream gap), not host launch latency.
+        const unsigned long long spin_ns = 100000ull + 30000ull * (warmup + reps);
+        ck(mgw::launch_replay(c->d_clock, spin_ns, 1, c->stream), "calibration spin");
         for (int k = 0; k < warmup; ++k) mgw::launch_group(p, 0, 0.0f, MGW_SGD, algo, c->stream);
         for (int k = 0; k < reps; ++k) {
           ck(cudaEventRecord(ev[2 * k], c->stream), "record");
