@@ -376,11 +376,29 @@ def main():
                  "algorithmic_bytes_per_iter": algo_bytes, "kernel_ms_per_iter": kern_s * 1e3,
                  "launches_per_iter": len(group_ms)})
 
+    # merged all-reduce bus GB/s = 2(P-1)/P * S / t: ours (fused kernel, from
+    # the calibration sweep) next to NCCL (torch.distributed.all_reduce, same
+    # sizes, comparison baseline only)
     bus = {}
     if N > 1:
-        for m in meas:
-            if m.size_bytes >= (16 << 20):
-                bus[str(m.size_bytes)] = 2 * (N - 1) / N * m.size_bytes / m.time_sec / 1e9
+        big = [m for m in meas if m.size_bytes >= (1 << 20)]
+        ncclt = []
+        for m in big:
+            x = torch.ones(m.size_bytes // 4, dtype=torch.float32, device=dev)
+            for _ in range(3):
+                torch.distributed.all_reduce(x)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            torch.cuda.synchronize()
+            ev[0].record()
+            for _ in range(10):
+                torch.distributed.all_reduce(x)
+            ev[1].record()
+            ev[1].synchronize()
+            ncclt.append(D.max_over_ranks(ev[0].elapsed_time(ev[1]) / 10 / 1e3, dev))
+            del x
+        for m, tn in zip(big, ncclt):
+            f = 2 * (N - 1) / N * m.size_bytes / 1e9
+            bus[str(m.size_bytes)] = {"mgwfbp": f / m.time_sec, "nccl": f / tn}
 
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:

@@ -89,7 +89,7 @@ def main():
     pipe.close()
     dp.close()
 
-    meas = comm.calibrate([4096 << k for k in range(0, 14, 2)], warmup=2, reps=5)
+    meas = comm.calibrate([4096 << k for k in range(0, 12, 2)], warmup=2, reps=5)  # <= arena
     try:
         gs.fit_model(meas)
     except gs.FitError as e:
