@@ -51,6 +51,9 @@ def parse_args():
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot"])
     ap.add_argument("--oneshot-max", type=int, default=512 * 1024)
+    ap.add_argument("--engine-ctas", type=int, default=-1,
+                    help="-1: persistent comm engine, one CTA per SM; >0: that many CTAs; "
+                         "0: one fused kernel launch per group")
     ap.add_argument("--l2-flush-mib", type=int, default=256)
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -267,7 +270,10 @@ def main():
 
     # ---- N1: on-box calibration of the fused kernel at this N, fitted
     sizes = calibration_sizes(total_bytes, 4 * padded)
-    meas = comm.calibrate(sizes, warmup=3, reps=15, algo=args.algo)
+    if args.engine_ctas != 0:
+        meas = comm.calibrate_engine(sizes, warmup=2, reps=5, algo=args.algo, engine_ctas=args.engine_ctas)
+    else:
+        meas = comm.calibrate(sizes, warmup=3, reps=15, algo=args.algo)
     tvec = torch.tensor([m.time_sec for m in meas], dtype=torch.float64, device=dev)
     if N > 1:
         torch.distributed.all_reduce(tvec, op=torch.distributed.ReduceOp.MAX)
@@ -295,7 +301,8 @@ def main():
     for name, plan in plans.items():
         dplans[name] = rt.DevicePlan(comm, grads, weights, plan)
         pipes[name] = rt.Pipeline(dplans[name], trace, args.lr, args.algo,
-                                  record_group_times=(name == "mgwfbp"), l2_flush_bytes=flush)
+                                  record_group_times=True, l2_flush_bytes=flush,
+                                  engine_ctas=args.engine_ctas)
 
     def timed(name, iters):
         D.barrier()
@@ -421,6 +428,8 @@ def main():
                        "layers": L, "params": sum(counts), "grad_bytes": total_bytes,
                        "plan": "optimal_plan on on-box calibrated (a, b)", "plan_sha256": digest[:16],
                        "groups": dplans["mgwfbp"].n_groups, "algo": args.algo, "oneshot_max": args.oneshot_max,
+                       "comm": ("persistent engine, %s CTAs" % ("1/SM" if args.engine_ctas < 0 else args.engine_ctas))
+                               if args.engine_ctas else "one fused kernel launch per group",
                        "parallelism": f"dp{N}", "l2": f"flushed every iteration ({args.l2_flush_mib} MiB memset "
                                                      "on the comm stream during the forward replay)",
                        "compute_ms": compute_ms},

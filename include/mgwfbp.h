@@ -183,9 +183,15 @@ int mgw_comm_set_oneshot_max(mgw_comm* comm, uint64_t bytes);
  * t_b: L backward seconds, t_f: forward seconds. l2_flush_bytes > 0 adds
  * a memset of that many bytes on a side branch at iteration start (it
  * overlaps the forward replay, as a real forward evicts L2), which the first
- * group waits for, so no iteration reads gradients/weights hot from L2. */
+ * group waits for, so no iteration reads gradients/weights hot from L2.
+ * engine_ctas selects the comm side: 0 = one fused kernel launch per group,
+ * each gated by its head's ready event; != 0 = the persistent comm engine,
+ * ONE kernel per iteration with engine_ctas CTAs (< 0: one per SM) that
+ * runs the groups in backward order as the replay marks them ready (no
+ * per-group launch cost; the paper's comm daemon thread, on the GPU). */
 int mgw_pipeline_create(mgw_plan* plan, const double* t_b, double t_f, float lr, int algo,
-                        int record_group_times, size_t l2_flush_bytes, mgw_pipeline** out);
+                        int record_group_times, size_t l2_flush_bytes, int engine_ctas,
+                        mgw_pipeline** out);
 int mgw_pipeline_destroy(mgw_pipeline* pipe);
 /* Launch `iters` iterations back to back on the pipeline's compute stream
  * (asynchronous). */
@@ -204,6 +210,13 @@ int mgw_pipeline_stream(mgw_pipeline* pipe, void** stream_out);
  * writes the median per size. Collective. */
 int mgw_calibrate(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int warmup, int reps,
                   int algo, mgw_meas* out);
+
+/* Calibration of the persistent comm engine: per size, iterations of an
+ * engine over 8 equal groups that are all ready at once; the median
+ * per-group device duration (%globaltimer, first CTA start -> last CTA end)
+ * is the sample. This is the T(M) the planner sees in engine pipelines. */
+int mgw_calibrate_engine(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int warmup,
+                         int reps, int algo, int engine_ctas, mgw_meas* out);
 
 /* Plain in-place sum all-reduce of a contiguous fp32 device buffer in rank
  * order (no scale, no SGD), through the same kernel. Collective. */

@@ -90,7 +90,11 @@ mgw_calibrate = _proto(
 )
 mgw_pipeline_create = _proto(
     "mgw_pipeline_create",
-    [vp, f64p, C.c_double, C.c_float, C.c_int, C.c_int, C.c_size_t, C.POINTER(vp)],
+    [vp, f64p, C.c_double, C.c_float, C.c_int, C.c_int, C.c_size_t, C.c_int, C.POINTER(vp)],
+)
+mgw_calibrate_engine = _proto(
+    "mgw_calibrate_engine",
+    [vp, u64p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Meas)],
 )
 mgw_pipeline_destroy = _proto("mgw_pipeline_destroy", [vp])
 mgw_pipeline_launch = _proto("mgw_pipeline_launch", [vp, C.c_int])

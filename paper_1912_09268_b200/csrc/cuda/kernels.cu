@@ -1,23 +1,33 @@
 // mgwfbp-b200 sm_100a kernels.
 //
-//  group_allreduce_kernel<P, TWO_SHOT, LOOPBACK>  — THE hot op: for one merge
+//  run_group<P>  — THE hot op, shared by both launch styles: for one merge
 //      group, pack (gather layer grads x 1/P into the merge arena) ->
 //      all-reduce over NVLink peer memory, summed in rank order ->
-//      unpack + SGD into the layer weights. One launch per group.
+//      unpack + SGD into the layer weights.
 //        one-shot: every rank reads every peer's packed tiles; 1 barrier.
 //        two-shot: tile t is owned by rank t % P; owners reduce their tiles
 //          in place (reduce-scatter), then every rank pulls the other
 //          owners' reduced tiles (all-gather) fused with SGD; 2 barriers.
+//  engine_kernel<P> — the persistent comm engine: one launch per iteration
+//      runs every group in backward order as soon as the compute side marks
+//      its head ready (paper Algorithm 2's daemon thread, on the GPU; no
+//      per-group launch latency).
+//  group_allreduce_kernel<P, TWO_SHOT, LOOPBACK> — one launch per group
+//      (standalone C-ABI op, calibration of that op, and the single-GPU
+//      loopback emulation of P ranks in one cooperative launch).
 //  pack_kernel / unpack_sgd_kernel — the standalone pack and unpack+SGD
 //      ops of the C ABI (rank-local, HBM-bound).
 //  replay_kernel — backward-pass replay: one thread spins on %globaltimer
-//      until a group head's ready time (pipeline.cu).
+//      until a group head's ready time, then marks the group ready.
 //
 // Cross-rank synchronisation is per CTA index: CTA b of every rank handles
 // the same tiles, so CTA b only waits for CTA b of the peers (flag plane
-// [b][src_rank], epoch = launch counter + 1, monotone, never reset).
-// Reductions use __fadd_rn / __fmul_rn / __fsub_rn only: no FMA contraction,
-// bit-exact with the CPU oracle's fl(fl(x0*s) + x1*s)... rank order.
+// [b][src_rank], epochs from a per-rank launch counter, monotone, never
+// reset). Every collective launch starts with an entry barrier over all its
+// CTAs, so no rank overwrites its merge arena while a peer may still read it
+// from an earlier launch. Reductions use __fadd_rn / __fmul_rn / __fsub_rn
+// only: no FMA contraction, bit-exact with the CPU oracle's
+// fl(fl(x0*s) + x1*s)... rank order.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -65,9 +75,11 @@ __device__ __forceinline__ void epilogue(const Tile& t, uint32_t e, float4 g, fl
       wv.z = sgd1(wv.z, g.z, lr);
       wv.w = sgd1(wv.w, g.w, lr);
       st_v4(w, wv);
-    } else {
-      const float gs[4] = {g.x, g.y, g.z, g.w};
-      for (uint32_t j = 0; j < n; ++j) w[j] = sgd1(w[j], gs[j], lr);
+    } else {  // ragged tail or unaligned layer: scalar, no local-memory array
+      if (n > 0) w[0] = sgd1(w[0], g.x, lr);
+      if (n > 1) w[1] = sgd1(w[1], g.y, lr);
+      if (n > 2) w[2] = sgd1(w[2], g.z, lr);
+      if (n > 3) w[3] = sgd1(w[3], g.w, lr);
     }
   }
   if (epi & MGW_WRITE_GRAD) {
@@ -75,18 +87,24 @@ __device__ __forceinline__ void epilogue(const Tile& t, uint32_t e, float4 g, fl
     if (n == 4 && !(t.layer & kGradUnaligned)) {
       st_v4(d, g);
     } else {
-      const float gs[4] = {g.x, g.y, g.z, g.w};
-      for (uint32_t j = 0; j < n; ++j) d[j] = gs[j];
+      if (n > 0) d[0] = g.x;
+      if (n > 1) d[1] = g.y;
+      if (n > 2) d[2] = g.z;
+      if (n > 3) d[3] = g.w;
     }
   }
 }
 
-// CTA-index barrier across ranks on barrier plane `plane`.
-__device__ __forceinline__ void rank_barrier(const RankView& v, int P, int plane, uint32_t epoch) {
+// Barrier of CTA index `cta` with the same CTA index of every rank, on
+// barrier plane `plane`: signal every peer (st.release.sys over NVLink),
+// then wait for every peer's signal (ld.acquire.sys), bounded by a timeout
+// that records an error instead of hanging the GPU.
+__device__ __forceinline__ void rank_barrier(const RankView& v, int P, int plane, uint32_t epoch,
+                                             uint32_t cta) {
   __syncthreads();
   if (threadIdx.x < P) {
     const int q = threadIdx.x;
-    const uint32_t slot = plane * kSignalPlane + blockIdx.x * kMaxRanks;
+    const uint32_t slot = plane * kSignalPlane + cta * kMaxRanks;
     st_release_sys(v.signal[q] + slot + v.rank, epoch);
     const uint32_t* mine = v.signal[v.rank] + slot + q;
     if (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
@@ -102,8 +120,9 @@ __device__ __forceinline__ void rank_barrier(const RankView& v, int P, int plane
   __syncthreads();
 }
 
-// Last CTA of this rank bumps the launch counter (epoch + parity source).
-__device__ __forceinline__ void finish_launch(const RankView& v, uint32_t seq) {
+// The last CTA of this rank to leave advances the launch counter by `used`
+// epochs (the epoch source of the next launch).
+__device__ __forceinline__ void finish_launch(const RankView& v, uint32_t seq, uint32_t used) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -111,122 +130,104 @@ __device__ __forceinline__ void finish_launch(const RankView& v, uint32_t seq) {
     if (prev == gridDim.x - 1) {
       atomicExch(v.state + 1, 0u);
       __threadfence();
-      atomicExch(v.state, seq + 1);
+      atomicExch(v.state, seq + used);
     }
   }
 }
 
+// Vectors per batch of peer loads: all of a thread's vectors for small P
+// (2P loads in flight), one at a time for P = 8 (8 in flight, ~64 KiB per
+// CTA) so the persistent engine stays within 128 registers without spills.
 template <int P>
-__device__ __forceinline__ void reduce_tile_rank_order(const RankView& v, const Tile& t,
-                                                       uint64_t copy_off, float4 (&acc)[kVecPerThread],
-                                                       bool (&live)[kVecPerThread]) {
-  float4 x[kVecPerThread][P];
+struct Batch {
+  static constexpr uint32_t kVec = P >= 8 ? 1 : kVecPerThread;
+  static constexpr int kPeers = P >= 8 ? 4 : P;  // all-gather: peers per load batch
+};
+
+// Reduce tile t over all ranks in rank order (x0 + x1 + ... + x_{P-1}, each
+// already scaled by 1/P in the pack), optionally store the sum in place in
+// this rank's arena (two-shot owner), then unpack + SGD.
+template <int P>
+__device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, uint64_t copy_off,
+                                            float* inplace, float lr, int epi) {
+  constexpr uint32_t B = Batch<P>::kVec;
   const uint32_t nvec = (t.len + 3) >> 2;
+  const uint32_t layer = t.layer & kLayerMask;
+  float* w = v.weights[layer];
+  float* g = v.grads[layer];
 #pragma unroll
-  for (uint32_t k = 0; k < kVecPerThread; ++k) {
-    const uint32_t i = threadIdx.x + k * kThreads;
-    live[k] = i < nvec;
-    if (live[k]) {
+  for (uint32_t k0 = 0; k0 < kVecPerThread; k0 += B) {
+    float4 x[B][P];
 #pragma unroll
-      for (int q = 0; q < P; ++q) x[k][q] = ld_cg_v4(v.arena[q] + copy_off + t.moff + i * 4);
+    for (uint32_t j = 0; j < B; ++j) {
+      const uint32_t i = threadIdx.x + (k0 + j) * kThreads;
+      if (i < nvec) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) x[j][q] = ld_cg_v4(v.arena[q] + copy_off + t.moff + i * 4);
+      }
     }
-  }
 #pragma unroll
-  for (uint32_t k = 0; k < kVecPerThread; ++k) {
-    if (live[k]) {
-      float4 s = x[k][0];
+    for (uint32_t j = 0; j < B; ++j) {
+      const uint32_t i = threadIdx.x + (k0 + j) * kThreads;
+      if (i < nvec) {
+        float4 s = x[j][0];
 #pragma unroll
-      for (int q = 1; q < P; ++q) s = add4(s, x[k][q]);
-      acc[k] = s;
+        for (int q = 1; q < P; ++q) s = add4(s, x[j][q]);
+        if (inplace != nullptr) st_v4(inplace + t.moff + i * 4, s);
+        epilogue(t, i * 4, s, w, g, lr, epi);
+      }
     }
   }
 }
 
-template <int P, bool TWO_SHOT, bool LOOPBACK>
-__global__ void __launch_bounds__(kThreads) group_allreduce_kernel(const GroupLaunch L) {
-  const RankView& v = L.views[LOOPBACK ? blockIdx.y : 0];
-  __shared__ uint32_t s_seq;
-  if (threadIdx.x == 0) s_seq = ld_volatile_u32(v.state);
-  __syncthreads();
-  const uint32_t seq = s_seq;
-  const uint32_t epoch = seq + 1;
-  const uint64_t copy_off = static_cast<uint64_t>(seq & 1u) * L.copy_stride;
-  const Tile* tiles = L.tiles;
-  const uint32_t n_tiles = L.n_tiles;
+// One-shot body: pack my tiles, barrier, pull every rank's copy of my tiles
+// and reduce them in rank order, unpack + SGD.
+template <int P>
+__device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* tiles,
+                                               uint32_t n_tiles, uint32_t epoch, uint64_t copy_off,
+                                               float scale, float lr, int epi, uint32_t cta,
+                                               uint32_t ncta) {
+  float* mine = v.arena[v.rank] + copy_off;
+  for (uint32_t ti = cta; ti < n_tiles; ti += ncta) pack_tile(tiles[ti], v.grads, mine, scale);
+  rank_barrier(v, P, 0, epoch, cta);
+  for (uint32_t ti = cta; ti < n_tiles; ti += ncta) {
+    reduce_tile<P>(v, tiles[ti], copy_off, nullptr, lr, epi);
+  }
+}
 
-  if constexpr (P == 1) {
-    // Single rank: no exchange. grad x 1/P (= 1) straight into the epilogue.
-    for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
-      const Tile t = tiles[ti];
-      const uint32_t layer = t.layer & kLayerMask;
-      const float* src = v.grads[layer] + t.src;
-      float* w = v.weights[layer];
-      float* g = v.grads[layer];
-      const bool aligned = !(t.layer & kGradUnaligned);
-      const uint32_t nvec = (t.len + 3) >> 2;
-      for (uint32_t i = threadIdx.x; i < nvec; i += blockDim.x) {
-        const uint32_t e = i * 4;
-        const float4 x = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
-        epilogue(t, e, mul4(x, L.scale), w, g, L.lr, L.epilogue);
-      }
-    }
-  } else if constexpr (!TWO_SHOT) {
-    float* mine = v.arena[v.rank] + copy_off;
-    for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
-      pack_tile(tiles[ti], v.grads, mine, L.scale);
-    }
-    rank_barrier(v, P, 0, epoch);
-    for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
-      const Tile t = tiles[ti];
-      float4 acc[kVecPerThread];
-      bool live[kVecPerThread];
-      reduce_tile_rank_order<P>(v, t, copy_off, acc, live);
-      const uint32_t layer = t.layer & kLayerMask;
-      float* w = v.weights[layer];
-      float* g = v.grads[layer];
+// Two-shot body: reduce-scatter to tile owners (in place), then all-gather
+// fused with unpack + SGD.
+template <int P>
+__device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* tiles,
+                                               uint32_t n_tiles, uint32_t epoch, uint64_t copy_off,
+                                               float scale, float lr, int epi, uint32_t cta,
+                                               uint32_t ncta) {
+  float* mine = v.arena[v.rank] + copy_off;
+  // Tiles are dealt to owners round-robin: super-tile s = tiles [s*P, s*P+P).
+  const uint32_t n_super = (n_tiles + P - 1) / P;
+  for (uint32_t s = cta; s < n_super; s += ncta) {
 #pragma unroll
-      for (uint32_t k = 0; k < kVecPerThread; ++k) {
-        if (live[k]) epilogue(t, (threadIdx.x + k * kThreads) * 4, acc[k], w, g, L.lr, L.epilogue);
-      }
+    for (int q = 0; q < P; ++q) {
+      const uint32_t ti = s * P + q;
+      if (ti < n_tiles) pack_tile(tiles[ti], v.grads, mine, scale);
     }
-  } else {
-    // Tiles are dealt to owners round-robin: super-tile s = tiles [s*P, s*P+P).
-    const uint32_t n_super = (n_tiles + P - 1) / P;
-    float* mine = v.arena[v.rank] + copy_off;
-    for (uint32_t s = blockIdx.x; s < n_super; s += gridDim.x) {
+  }
+  rank_barrier(v, P, 0, epoch, cta);
+  for (uint32_t s = cta; s < n_super; s += ncta) {
+    const uint32_t ti = s * P + v.rank;
+    if (ti < n_tiles) reduce_tile<P>(v, tiles[ti], copy_off, mine, lr, epi);
+  }
+  rank_barrier(v, P, 1, epoch, cta);
+  // All-gather fused with unpack + SGD: pull the other owners' tiles,
+  // kPeers tiles x kVecPerThread vectors of loads in flight per batch.
+  constexpr int QC = Batch<P>::kPeers;
+  for (uint32_t s = cta; s < n_super; s += ncta) {
 #pragma unroll
-      for (int q = 0; q < P; ++q) {
-        const uint32_t ti = s * P + q;
-        if (ti < n_tiles) pack_tile(tiles[ti], v.grads, mine, L.scale);
-      }
-    }
-    rank_barrier(v, P, 0, epoch);
-    // Reduce-scatter: this rank's tile of every super-tile, reduced in place.
-    for (uint32_t s = blockIdx.x; s < n_super; s += gridDim.x) {
-      const uint32_t ti = s * P + v.rank;
-      if (ti >= n_tiles) continue;
-      const Tile t = tiles[ti];
-      float4 acc[kVecPerThread];
-      bool live[kVecPerThread];
-      reduce_tile_rank_order<P>(v, t, copy_off, acc, live);
-      const uint32_t layer = t.layer & kLayerMask;
-      float* w = v.weights[layer];
-      float* g = v.grads[layer];
+    for (int q0 = 0; q0 < P; q0 += QC) {
+      float4 x[QC][kVecPerThread];
 #pragma unroll
-      for (uint32_t k = 0; k < kVecPerThread; ++k) {
-        if (live[k]) {
-          const uint32_t e = (threadIdx.x + k * kThreads) * 4;
-          st_v4(mine + t.moff + e, acc[k]);
-          epilogue(t, e, acc[k], w, g, L.lr, L.epilogue);
-        }
-      }
-    }
-    rank_barrier(v, P, 1, epoch);
-    // All-gather fused with unpack + SGD: pull every other owner's tile.
-    for (uint32_t s = blockIdx.x; s < n_super; s += gridDim.x) {
-      float4 x[P][kVecPerThread];
-#pragma unroll
-      for (int q = 0; q < P; ++q) {
+      for (int j = 0; j < QC; ++j) {
+        const int q = q0 + j;
         const uint32_t ti = s * P + q;
         if (q == v.rank || ti >= n_tiles) continue;
         const Tile t = tiles[ti];
@@ -234,11 +235,12 @@ __global__ void __launch_bounds__(kThreads) group_allreduce_kernel(const GroupLa
 #pragma unroll
         for (uint32_t k = 0; k < kVecPerThread; ++k) {
           const uint32_t i = threadIdx.x + k * kThreads;
-          if (i < nvec) x[q][k] = ld_cg_v4(v.arena[q] + copy_off + t.moff + i * 4);
+          if (i < nvec) x[j][k] = ld_cg_v4(v.arena[q] + copy_off + t.moff + i * 4);
         }
       }
 #pragma unroll
-      for (int q = 0; q < P; ++q) {
+      for (int j = 0; j < QC; ++j) {
+        const int q = q0 + j;
         const uint32_t ti = s * P + q;
         if (q == v.rank || ti >= n_tiles) continue;
         const Tile t = tiles[ti];
@@ -249,12 +251,118 @@ __global__ void __launch_bounds__(kThreads) group_allreduce_kernel(const GroupLa
 #pragma unroll
         for (uint32_t k = 0; k < kVecPerThread; ++k) {
           const uint32_t i = threadIdx.x + k * kThreads;
-          if (i < nvec) epilogue(t, i * 4, x[q][k], w, g, L.lr, L.epilogue);
+          if (i < nvec) epilogue(t, i * 4, x[j][k], w, g, lr, epi);
         }
       }
     }
   }
-  finish_launch(v, seq);
+}
+
+// One merge group, executed by CTA `cta` of `ncta`. `epoch` numbers this
+// group's barriers; `copy_off` selects the merge-arena copy.
+template <int P>
+__device__ __forceinline__ void run_group(bool two_shot, const RankView& v, const Tile* tiles,
+                                          uint32_t n_tiles, uint32_t epoch, uint64_t copy_off,
+                                          float scale, float lr, int epi, uint32_t cta,
+                                          uint32_t ncta) {
+  if constexpr (P == 1) {
+    // Single rank: no exchange. grad x 1/P (= 1) straight into the epilogue.
+    for (uint32_t ti = cta; ti < n_tiles; ti += ncta) {
+      const Tile t = tiles[ti];
+      const uint32_t layer = t.layer & kLayerMask;
+      const float* src = v.grads[layer] + t.src;
+      float* w = v.weights[layer];
+      float* g = v.grads[layer];
+      const bool aligned = !(t.layer & kGradUnaligned);
+      const uint32_t nvec = (t.len + 3) >> 2;
+      for (uint32_t i = threadIdx.x; i < nvec; i += blockDim.x) {
+        const uint32_t e = i * 4;
+        const float4 x = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
+        epilogue(t, e, mul4(x, scale), w, g, lr, epi);
+      }
+    }
+  } else {
+    if (two_shot) {
+      two_shot_group<P>(v, tiles, n_tiles, epoch, copy_off, scale, lr, epi, cta, ncta);
+    } else {
+      one_shot_group<P>(v, tiles, n_tiles, epoch, copy_off, scale, lr, epi, cta, ncta);
+    }
+  }
+}
+
+template <int P, bool TWO_SHOT, bool LOOPBACK>
+__global__ void __launch_bounds__(kThreads, 1) group_allreduce_kernel(const __grid_constant__ GroupLaunch L) {
+  const RankView& v = L.views[LOOPBACK ? blockIdx.y : 0];
+  if constexpr (P == 1) {
+    run_group<1>(false, v, L.tiles, L.n_tiles, 0, 0, L.scale, L.lr, L.epilogue, blockIdx.x,
+                 gridDim.x);
+  } else {
+    __shared__ uint32_t s_seq;
+    if (threadIdx.x == 0) s_seq = ld_volatile_u32(v.state);
+    __syncthreads();
+    const uint32_t seq = s_seq;
+    rank_barrier(v, P, 1, seq + 1, blockIdx.x);  // entry: peers have left every older launch
+    const uint32_t epoch = seq + 2;
+    const uint64_t copy_off = static_cast<uint64_t>(epoch & 1u) * L.copy_stride;
+    run_group<P>(TWO_SHOT, v, L.tiles, L.n_tiles, epoch, copy_off, L.scale, L.lr, L.epilogue,
+                 blockIdx.x, gridDim.x);
+    finish_launch(v, seq, 2);
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineLaunch E) {
+  const RankView& v = E.v;
+  __shared__ uint32_t s_seq, s_iter;
+  if (threadIdx.x == 0) {
+    s_seq = P > 1 ? ld_volatile_u32(v.state) : 0u;
+    s_iter = ld_volatile_u32(E.pipe + 1);
+  }
+  __syncthreads();
+  const uint32_t seq = s_seq;
+  const uint32_t iter = s_iter;
+  // Entry barrier (runs while the compute stream replays the forward pass):
+  // every peer has finished every older launch before anything is packed.
+  if constexpr (P > 1) rank_barrier(v, P, 1, seq + 1, blockIdx.x);
+  for (uint32_t k = 0; k < E.G; ++k) {
+    const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
+    const EngineGroup grp = E.groups[gi];
+    const bool two = P > 1 && grp.two_shot != 0;
+    const uint32_t units = two ? (grp.n_tiles + P - 1) / P : grp.n_tiles;
+    if (blockIdx.x >= units) continue;  // same on every rank: no barrier to skip
+    if (threadIdx.x == 0) {
+      const uint32_t target = iter * E.G + k + 1;
+      while (static_cast<int32_t>(ld_acquire_gpu(E.pipe) - target) < 0) {
+      }
+      if (E.stamps != nullptr && blockIdx.x == 0) E.stamps[2 * gi] = globaltimer_ns();
+    }
+    __syncthreads();
+    const uint32_t epoch = seq + 2 + k;
+    const uint64_t copy_off = static_cast<uint64_t>(epoch & 1u) * E.copy_stride;
+    run_group<P>(two, v, E.tiles + grp.tile_first, grp.n_tiles, epoch, copy_off, E.scale, E.lr,
+                 E.epilogue, blockIdx.x, gridDim.x);
+    if (E.stamps != nullptr) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t active = units < gridDim.x ? units : gridDim.x;
+        if (atomicAdd(E.group_done + gi, 1u) == active - 1) {
+          E.group_done[gi] = 0;
+          E.stamps[2 * gi + 1] = globaltimer_ns();
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(E.pipe + 2, 1u) == gridDim.x - 1) {
+      atomicExch(E.pipe + 2, 0u);
+      __threadfence();
+      atomicExch(E.pipe + 1, iter + 1);
+      if (P > 1) atomicExch(v.state, seq + 1 + E.G);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) pack_kernel(const Tile* tiles, uint32_t n_tiles,
@@ -286,9 +394,10 @@ __global__ void __launch_bounds__(kThreads) unpack_sgd_kernel(const Tile* tiles,
 }
 
 // clock[0]: iteration start (written by the first replay kernel of an
-// iteration), clock[1]: completion time of the latest replay kernel.
-__global__ void replay_kernel(unsigned long long* clock, unsigned long long deadline_ns,
-                              int first) {
+// iteration), clock[1]: completion time of the latest replay kernel. When
+// `ready` is given, the group is marked ready for the comm engine.
+__global__ void replay_kernel(unsigned long long* clock, unsigned long long deadline_ns, int first,
+                              uint32_t* ready) {
   if (threadIdx.x != 0) return;
   unsigned long long t0;
   if (first) {
@@ -301,6 +410,10 @@ __global__ void replay_kernel(unsigned long long* clock, unsigned long long dead
   unsigned long long now = globaltimer_ns();
   while (now < due) now = globaltimer_ns();
   clock[1] = now;
+  if (ready != nullptr) {
+    __threadfence();
+    atomicAdd(ready, 1u);
+  }
 }
 
 template <int P, bool TWO, bool LB>
@@ -327,6 +440,16 @@ cudaError_t launch_lb(const GroupLaunch& L, dim3 grid, bool two, cudaStream_t s)
   }
 }
 
+const void* engine_fn(int nranks) {
+  switch (nranks) {
+    case 1: return reinterpret_cast<const void*>(engine_kernel<1>);
+    case 2: return reinterpret_cast<const void*>(engine_kernel<2>);
+    case 4: return reinterpret_cast<const void*>(engine_kernel<4>);
+    case 8: return reinterpret_cast<const void*>(engine_kernel<8>);
+    default: return nullptr;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_group_allreduce(const GroupLaunch& L, int ctas_per_rank, bool two_shot,
@@ -334,6 +457,19 @@ cudaError_t launch_group_allreduce(const GroupLaunch& L, int ctas_per_rank, bool
   const dim3 grid(ctas_per_rank, loopback ? L.nranks : 1);
   return loopback ? launch_lb<true>(L, grid, two_shot, stream)
                   : launch_lb<false>(L, grid, two_shot, stream);
+}
+
+cudaError_t launch_engine(const EngineLaunch& E, int ctas, cudaStream_t stream) {
+  const void* fn = engine_fn(E.nranks);
+  if (fn == nullptr) return cudaErrorInvalidValue;
+  void* args[] = {const_cast<EngineLaunch*>(&E)};
+  return cudaLaunchKernel(fn, dim3(ctas), dim3(kThreads), args, 0, stream);
+}
+
+cudaError_t engine_ctas_per_sm(int nranks, int* out) {
+  const void* fn = engine_fn(nranks);
+  if (fn == nullptr) return cudaErrorInvalidValue;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kThreads, 0);
 }
 
 cudaError_t max_ctas_per_sm(int nranks, bool two_shot, bool loopback, int* out) {
@@ -369,8 +505,8 @@ cudaError_t launch_unpack_sgd(const Tile* tiles, uint32_t n_tiles, float* const*
 }
 
 cudaError_t launch_replay(unsigned long long* clock, unsigned long long deadline_ns, int first,
-                          cudaStream_t stream) {
-  replay_kernel<<<1, 32, 0, stream>>>(clock, deadline_ns, first);
+                          uint32_t* ready, cudaStream_t stream) {
+  replay_kernel<<<1, 32, 0, stream>>>(clock, deadline_ns, first, ready);
   return cudaGetLastError();
 }
 

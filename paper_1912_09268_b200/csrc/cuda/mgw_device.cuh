@@ -63,7 +63,39 @@ struct GroupLaunch {
   RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
 };
 
+// One merge group as the persistent comm engine sees it.
+struct EngineGroup {
+  uint32_t tile_first;
+  uint32_t n_tiles;
+  uint32_t two_shot;
+  uint32_t pad;
+};
+
+// The persistent comm engine (paper Algorithm 2's communication daemon, on
+// the GPU): ONE kernel per iteration walks the groups in backward order,
+// each one the moment the compute side marks its head layer ready.
+struct EngineLaunch {
+  RankView v;
+  const Tile* tiles;
+  const EngineGroup* groups;     // ascending group index
+  uint32_t G;
+  int nranks;
+  float scale;
+  float lr;
+  int epilogue;
+  uint64_t copy_stride;
+  uint32_t* pipe;                // [0] groups made ready (monotone), [1] iteration, [2] CTA exit count
+  uint32_t* group_done;          // G counters for end stamps (NULL: no timing)
+  unsigned long long* stamps;    // 2*G: (start, end) %globaltimer of each group (NULL: no timing)
+};
+
 #ifdef __CUDACC__
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;

@@ -34,7 +34,9 @@ cudaError_t launch_unpack_sgd(const Tile* tiles, uint32_t n_tiles, float* const*
                               float* const* weights, const float* merge, uint64_t begin, float lr,
                               int epi, int ctas, cudaStream_t stream);
 cudaError_t launch_replay(unsigned long long* clock, unsigned long long deadline_ns, int first,
-                          cudaStream_t stream);
+                          uint32_t* ready, cudaStream_t stream);
+cudaError_t launch_engine(const EngineLaunch& E, int ctas, cudaStream_t stream);
+cudaError_t engine_ctas_per_sm(int nranks, int* out);
 
 std::atomic<uint64_t> g_kernel_launches{0};
 
@@ -120,6 +122,13 @@ struct mgw_pipeline {
   int iter_flush_value = 0x5a;
   bool timed_groups = false;
   int kernels_per_iter = 0;
+  // persistent comm engine mode
+  bool engine = false;
+  int engine_ctas = 0;
+  uint32_t* d_pipe = nullptr;             // ready count, iteration, exit count
+  uint32_t* d_group_done = nullptr;       // G
+  unsigned long long* d_stamps = nullptr; // 2G
+  mgw::EngineGroup* d_groups = nullptr;   // G
 };
 
 namespace mgw {
@@ -300,6 +309,9 @@ mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* w
      "upload weights table");
   return p;
 }
+
+mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float lr, int algo,
+                             bool timed, size_t l2_flush_bytes, int engine_ctas);
 
 }  // namespace
 }  // namespace mgw
@@ -551,7 +563,7 @@ int mgw_calibrate(mgw_comm* c, const uint64_t* sizes, size_t n, int warmup, int 
         // when the GPU reaches it: the event-to-event times then measure
         // the device-side cost (kernel + stream gap), not host launch latency.
         const unsigned long long spin_ns = 100000ull + 30000ull * (warmup + reps);
-        ck(mgw::launch_replay(c->d_clock, spin_ns, 1, c->stream), "calibration spin");
+        ck(mgw::launch_replay(c->d_clock, spin_ns, 1, nullptr, c->stream), "calibration spin");
         for (int k = 0; k < warmup; ++k) mgw::launch_group(p, 0, 0.0f, MGW_SGD, algo, c->stream);
         for (int k = 0; k < reps; ++k) {
           ck(cudaEventRecord(ev[2 * k], c->stream), "record");
@@ -583,12 +595,31 @@ int mgw_calibrate(mgw_comm* c, const uint64_t* sizes, size_t n, int warmup, int 
 }
 
 int mgw_pipeline_create(mgw_plan* p, const double* t_b, double t_f, float lr, int algo,
-                        int record_group_times, size_t l2_flush_bytes, mgw_pipeline** out) {
+                        int record_group_times, size_t l2_flush_bytes, int engine_ctas,
+                        mgw_pipeline** out) {
   MGW_TRY {
     require(p != nullptr && t_b != nullptr && out != nullptr, "bad pipeline arguments");
+    *out = mgw::build_pipeline(p, t_b, t_f, lr, algo, record_group_times != 0, l2_flush_bytes,
+                               engine_ctas);
+  }
+  MGW_CATCH
+}
+
+}  // extern "C"
+
+namespace mgw {
+namespace {
+
+// Backward-replay pipeline as one CUDA graph per iteration. engine_ctas == 0:
+// one fused kernel launch per group, each waiting on its head's ready event;
+// engine_ctas != 0: ONE persistent engine kernel (engine_ctas CTAs, < 0 =
+// one per SM) that the replay kernels feed through a device ready counter.
+mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float lr, int algo,
+                             bool timed, size_t l2_flush_bytes, int engine_ctas) {
+  {
     require(!p->comm->loopback, "pipelines run on a real communicator");
     require(t_f >= 0.0, "t_f must be >= 0");
-    mgw::set_device(p->comm);
+    set_device(p->comm);
     const size_t L = p->L;
     // Ready time of every layer, reference timeline.hpp:99-108 / planner.hpp:67-70.
     std::vector<double> tau_b(L);
@@ -597,15 +628,40 @@ int mgw_pipeline_create(mgw_plan* p, const double* t_b, double t_f, float lr, in
 
     auto* pipe = new mgw_pipeline();
     pipe->plan = p;
-    pipe->timed_groups = record_group_times != 0;
+    pipe->timed_groups = timed;
+    pipe->engine = engine_ctas != 0;
     const int G = p->G();
+    mgw_comm* c = p->comm;
+    if (pipe->engine) {
+      int occ = 1;
+      ck(engine_ctas_per_sm(c->nranks, &occ), "engine occupancy");
+      // the engine runs concurrently with the replay kernel: leave room
+      const int cap = std::min(kMaxCtas, std::max(1, occ) * c->num_sms - 1);
+      pipe->engine_ctas = std::min(cap, engine_ctas < 0 ? c->num_sms : engine_ctas);
+      ck(cudaMalloc(&pipe->d_pipe, 4 * sizeof(uint32_t)), "cudaMalloc(pipe)");
+      ck(cudaMemset(pipe->d_pipe, 0, 4 * sizeof(uint32_t)), "memset(pipe)");
+      ck(cudaMalloc(&pipe->d_group_done, std::max(G, 1) * sizeof(uint32_t)), "cudaMalloc");
+      ck(cudaMemset(pipe->d_group_done, 0, std::max(G, 1) * sizeof(uint32_t)), "memset");
+      ck(cudaMalloc(&pipe->d_stamps, 2 * std::max(G, 1) * sizeof(unsigned long long)), "cudaMalloc");
+      ck(cudaMemset(pipe->d_stamps, 0, 2 * std::max(G, 1) * sizeof(unsigned long long)), "memset");
+      std::vector<EngineGroup> groups(G);
+      for (int g = 0; g < G; ++g) {
+        groups[g].tile_first = p->tile_first[g];
+        groups[g].n_tiles = p->tile_first[g + 1] - p->tile_first[g];
+        groups[g].two_shot = use_two_shot(c, group_bytes(p, g), algo) ? 1u : 0u;
+        groups[g].pad = 0;
+      }
+      ck(cudaMalloc(&pipe->d_groups, std::max(G, 1) * sizeof(EngineGroup)), "cudaMalloc(groups)");
+      ck(cudaMemcpy(pipe->d_groups, groups.data(), G * sizeof(EngineGroup), cudaMemcpyHostToDevice),
+         "upload groups");
+    }
     ck(cudaStreamCreateWithFlags(&pipe->compute, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&pipe->comm, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&pipe->fork, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&pipe->join, cudaEventDisableTiming), "event");
-    pipe->ready.resize(G);
+    pipe->ready.resize(pipe->engine ? 0 : G);
     for (auto& e : pipe->ready) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    if (pipe->timed_groups) {
+    if (pipe->timed_groups && !pipe->engine) {
       pipe->g_start.resize(G);
       pipe->g_end.resize(G);
       for (auto& e : pipe->g_start) ck(cudaEventCreate(&e), "event");
@@ -628,20 +684,39 @@ int mgw_pipeline_create(mgw_plan* p, const double* t_b, double t_f, float lr, in
         ck(cudaMemsetAsync(pipe->flush_buf, pipe->iter_flush_value, pipe->flush_bytes, pipe->comm),
            "l2 flush");
       }
+      if (pipe->engine) {
+        EngineLaunch E{};
+        E.v = make_view(c, 0, p->d_grads, p->d_weights);
+        E.tiles = p->d_tiles;
+        E.groups = pipe->d_groups;
+        E.G = static_cast<uint32_t>(G);
+        E.nranks = c->nranks;
+        E.scale = 1.0f / static_cast<float>(c->nranks);
+        E.lr = lr;
+        E.epilogue = MGW_SGD;
+        E.copy_stride = c->arena_elems;
+        E.pipe = pipe->d_pipe;
+        E.group_done = timed ? pipe->d_group_done : nullptr;
+        E.stamps = timed ? pipe->d_stamps : nullptr;
+        ck(launch_engine(E, pipe->engine_ctas, pipe->comm), "engine launch");
+      }
       bool first = true;
       for (int g = G - 1; g >= 0; --g) {
         const size_t head = p->heads[g];
         const double ready_s = tau_b[head] + t_b[head];
         const auto deadline = static_cast<unsigned long long>(std::llround(ready_s * 1e9));
-        ck(mgw::launch_replay(pipe->d_clock, deadline, first ? 1 : 0, pipe->compute), "replay");
+        ck(launch_replay(pipe->d_clock, deadline, first ? 1 : 0,
+                         pipe->engine ? pipe->d_pipe : nullptr, pipe->compute),
+           "replay");
         first = false;
+        if (pipe->engine) continue;
         ck(cudaEventRecord(pipe->ready[g], pipe->compute), "ready");
         ck(cudaStreamWaitEvent(pipe->comm, pipe->ready[g], 0), "ready wait");
         if (pipe->timed_groups) {
           ck(cudaEventRecordWithFlags(pipe->g_start[g], pipe->comm, cudaEventRecordExternal),
              "group start");
         }
-        mgw::launch_group(p, g, lr, MGW_SGD, algo, pipe->comm);
+        launch_group(p, g, lr, MGW_SGD, algo, pipe->comm);
         if (pipe->timed_groups) {
           ck(cudaEventRecordWithFlags(pipe->g_end[g], pipe->comm, cudaEventRecordExternal),
              "group end");
@@ -657,13 +732,19 @@ int mgw_pipeline_create(mgw_plan* p, const double* t_b, double t_f, float lr, in
     }
     ck(cudaStreamEndCapture(pipe->compute, &pipe->graph), "end capture");
     ck(cudaGraphInstantiate(&pipe->exec, pipe->graph, 0), "graph instantiate");
-    // the capture counted kernels once; graph replays add per launch
-    mgw::g_kernel_launches.fetch_sub(static_cast<uint64_t>(G), std::memory_order_relaxed);
-    pipe->kernels_per_iter = 2 * G;
-    *out = pipe;
+    if (!pipe->engine) {
+      // the capture counted kernels once; graph replays add per launch
+      g_kernel_launches.fetch_sub(static_cast<uint64_t>(G), std::memory_order_relaxed);
+    }
+    pipe->kernels_per_iter = pipe->engine ? G + 1 : 2 * G;
+    return pipe;
   }
-  MGW_CATCH
 }
+
+}  // namespace
+}  // namespace mgw
+
+extern "C" {
 
 int mgw_pipeline_destroy(mgw_pipeline* pipe) {
   MGW_TRY {
@@ -679,6 +760,10 @@ int mgw_pipeline_destroy(mgw_pipeline* pipe) {
     cudaEventDestroy(pipe->join);
     cudaFree(pipe->d_clock);
     if (pipe->flush_buf) cudaFree(pipe->flush_buf);
+    if (pipe->d_pipe) cudaFree(pipe->d_pipe);
+    if (pipe->d_group_done) cudaFree(pipe->d_group_done);
+    if (pipe->d_stamps) cudaFree(pipe->d_stamps);
+    if (pipe->d_groups) cudaFree(pipe->d_groups);
     cudaStreamDestroy(pipe->compute);
     cudaStreamDestroy(pipe->comm);
     delete pipe;
@@ -729,9 +814,85 @@ int mgw_pipeline_group_times(mgw_pipeline* pipe, float* group_ms) {
             "pipeline was created without record_group_times");
     mgw::set_device(pipe->plan->comm);
     ck(cudaStreamSynchronize(pipe->compute), "sync");
+    if (pipe->engine) {
+      const int G = pipe->plan->G();
+      std::vector<unsigned long long> st(2 * static_cast<size_t>(G));
+      ck(cudaMemcpy(st.data(), pipe->d_stamps, st.size() * sizeof(unsigned long long),
+                    cudaMemcpyDeviceToHost),
+         "read stamps");
+      for (int g = 0; g < G; ++g) {
+        // zero-tile groups are no-ops in the engine (no CTA active)
+        group_ms[g] = st[2 * g + 1] > st[2 * g] ? static_cast<float>(st[2 * g + 1] - st[2 * g]) * 1e-6f
+                                                : 0.0f;
+      }
+      return 0;
+    }
     for (size_t g = 0; g < pipe->g_start.size(); ++g) {
       ck(cudaEventElapsedTime(&group_ms[g], pipe->g_start[g], pipe->g_end[g]), "elapsed");
     }
+  }
+  MGW_CATCH
+}
+
+int mgw_calibrate_engine(mgw_comm* c, const uint64_t* sizes, size_t n, int warmup, int reps,
+                         int algo, int engine_ctas, mgw_meas* out) {
+  MGW_TRY {
+    require(c != nullptr && sizes != nullptr && out != nullptr && reps >= 1, "bad calibrate args");
+    require(!c->loopback, "calibration runs on a real communicator");
+    mgw::set_device(c);
+    uint64_t max_bytes = 16;
+    for (size_t i = 0; i < n; ++i) max_bytes = std::max(max_bytes, sizes[i]);
+    const size_t max_elems = (max_bytes + 3) / 4;
+    constexpr int kGroups = 8;  // groups per calibration iteration (all ready at t = 0)
+    float* grad = nullptr;
+    float* w = nullptr;
+    ck(cudaMalloc(&grad, max_elems * sizeof(float)), "cudaMalloc(calib grad)");
+    ck(cudaMalloc(&w, max_elems * sizeof(float)), "cudaMalloc(calib w)");
+    ck(cudaMemset(grad, 0, max_elems * sizeof(float)), "memset");
+    ck(cudaMemset(w, 0, max_elems * sizeof(float)), "memset");
+    try {
+      for (size_t i = 0; i < n; ++i) {
+        // R layers of `cnt` elements that all alias the same buffers (the
+        // kernel reads grads / updates weights; aliasing is harmless for
+        // timing), one group each, every group ready at iteration start.
+        const uint64_t cnt = std::max<uint64_t>(1, (sizes[i] + 3) / 4);
+        const uint64_t padded = (cnt + 3) & ~uint64_t{3};
+        const int R = static_cast<int>(std::max<uint64_t>(
+            1, std::min<uint64_t>(kGroups, c->arena_elems / std::max<uint64_t>(padded, 1))));
+        std::vector<float*> gp(R, grad), wp(R, w);
+        std::vector<uint64_t> counts(R, cnt);
+        std::vector<uint8_t> tags(R, 0);
+        std::vector<double> tb(R, 0.0);
+        mgw_plan* p = mgw::build_plan(c, R, gp.data(), wp.data(), counts.data(), tags.data());
+        mgw_pipeline* pipe = nullptr;
+        try {
+          pipe = mgw::build_pipeline(p, tb.data(), 0.0, 0.0f, algo, true, 0, engine_ctas);
+          std::vector<float> ms;
+          std::vector<float> gm(R);
+          for (int k = 0; k < warmup + reps; ++k) {
+            ck(cudaGraphLaunch(pipe->exec, pipe->compute), "graph launch");
+            if (mgw_pipeline_group_times(pipe, gm.data()) != 0) throw mgw::CudaFailure("stamps");
+            if (k >= warmup) ms.insert(ms.end(), gm.begin(), gm.end());
+          }
+          std::sort(ms.begin(), ms.end());
+          out[i].size_bytes = sizes[i];
+          out[i].time_sec = 1e-3 * ms[ms.size() / 2];
+        } catch (...) {
+          mgw_pipeline_destroy(pipe);
+          mgw::destroy_plan(p);
+          throw;
+        }
+        mgw_pipeline_destroy(pipe);
+        mgw::destroy_plan(p);
+      }
+      mgw::check_barrier_flags(c);
+    } catch (...) {
+      cudaFree(grad);
+      cudaFree(w);
+      throw;
+    }
+    cudaFree(grad);
+    cudaFree(w);
   }
   MGW_CATCH
 }

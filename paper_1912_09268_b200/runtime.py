@@ -80,6 +80,15 @@ class Comm:
                                  ALGO[algo], out))
         return [CommMeasurement(out[i].size_bytes, out[i].time_sec) for i in range(len(sizes))]
 
+    def calibrate_engine(self, sizes: Sequence[int], warmup: int = 2, reps: int = 5,
+                         algo: str = "auto", engine_ctas: int = -1) -> List[CommMeasurement]:
+        """N1 for engine pipelines: median per-group device time in the
+        persistent comm engine (8 equal groups, all ready at once)."""
+        out = (_lib.Meas * len(sizes))()
+        check(_lib.mgw_calibrate_engine(self.handle, arr(C.c_uint64, sizes), len(sizes), warmup, reps,
+                                        ALGO[algo], engine_ctas, out))
+        return [CommMeasurement(out[i].size_bytes, out[i].time_sec) for i in range(len(sizes))]
+
     def close(self) -> None:
         if self.handle:
             check(_lib.mgw_comm_destroy(self.handle))
@@ -157,12 +166,16 @@ class Pipeline:
     layer is ready, one CUDA graph per iteration."""
 
     def __init__(self, dplan: DevicePlan, trace: ModelTrace, lr: float, algo: str = "auto",
-                 record_group_times: bool = False, l2_flush_bytes: int = 0):
+                 record_group_times: bool = False, l2_flush_bytes: int = 0, engine_ctas: int = -1):
+        """engine_ctas: -1 persistent comm engine with one CTA per SM, > 0 that
+        many CTAs, 0 = one fused kernel launch per group."""
         self.dplan = dplan
+        self.engine_ctas = engine_ctas
         tb = arr(C.c_double, (l.backward_time for l in trace.layers))
         h = C.c_void_p()
         check(_lib.mgw_pipeline_create(dplan.handle, tb, float(trace.forward_time), lr, ALGO[algo],
-                                       int(record_group_times), int(l2_flush_bytes), C.byref(h)))
+                                       int(record_group_times), int(l2_flush_bytes), int(engine_ctas),
+                                       C.byref(h)))
         self.handle = h
         s = C.c_void_p()
         check(_lib.mgw_pipeline_stream(h, C.byref(s)))

@@ -44,7 +44,7 @@ def main():
     plan = gs.optimal_plan(tr, gs.AllReduceModel(2e-5, 1 / 500e9))
     D.agree_plan(plan.tags)
     tags = [int(t) for t in plan.tags]
-    comm = rt.Comm(rank, P, local, 4 * rt.padded_elems(COUNTS))
+    comm = rt.Comm(rank, P, local, max(4 * rt.padded_elems(COUNTS), 80 << 20))
     comm.set_oneshot_max(64 * 1024)
     failures = []
     for algo in ("oneshot", "twoshot", "auto"):
@@ -77,23 +77,36 @@ def main():
         if not bool(((mine - ref).abs() <= 1e-6 * absx + 1e-30).all()):
             failures.append(f"allreduce vs nccl n={n}")
 
-    # pipeline at P ranks
-    g_dev = [torch.rand(c, device="cuda") for c in COUNTS]
-    w_dev = [torch.rand(c, device="cuda") for c in COUNTS]
-    dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
-    pipe = rt.Pipeline(dp, tr, LR, record_group_times=True)
-    ms = pipe.run(5)
-    compute_ms = (tr.forward_time + sum(t_b)) * 1e3
-    if not all(m >= compute_ms * 0.999 for m in ms):
-        failures.append(f"pipeline faster than its compute: {ms} < {compute_ms}")
-    pipe.close()
-    dp.close()
+    # pipelines at P ranks (per-group launches and the persistent engine):
+    # 5 iterations of SGD with the static gradients, bit-exact vs the oracle
+    for engine in (0, -1, 16):
+        g_np, w_np = inputs(P)
+        g_dev = [torch.from_numpy(a.copy()).cuda() for a in g_np[rank]]
+        w_dev = [torch.from_numpy(a.copy()).cuda() for a in w_np[rank]]
+        dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+        pipe = rt.Pipeline(dp, tr, LR, record_group_times=True, l2_flush_bytes=64 << 20, engine_ctas=engine)
+        ms = pipe.run(5)
+        gt = pipe.group_times_ms()
+        compute_ms = (tr.forward_time + sum(t_b)) * 1e3
+        if not all(m >= compute_ms * 0.999 for m in ms):
+            failures.append(f"engine={engine}: pipeline faster than its compute: {ms} < {compute_ms}")
+        if not all(t >= 0 for t in gt) or sum(gt) <= 0:
+            failures.append(f"engine={engine}: bad group times {gt}")
+        for _ in range(5):
+            pyoracle.allreduce_sgd(g_np, w_np, tags, LR)
+        for l in range(len(COUNTS)):
+            if not np.array_equal(w_dev[l].cpu().numpy(), w_np[rank][l]):
+                failures.append(f"engine={engine}: pipeline weights layer {l}")
+        pipe.close()
+        dp.close()
 
     meas = comm.calibrate([4096 << k for k in range(0, 12, 2)], warmup=2, reps=5)  # <= arena
-    try:
-        gs.fit_model(meas)
-    except gs.FitError as e:
-        failures.append(f"calibration fit: {e}")
+    meas_e = comm.calibrate_engine([4096 << k for k in range(0, 12, 2)], warmup=1, reps=3)
+    for mm in (meas, meas_e):
+        try:
+            gs.fit_model(mm)
+        except gs.FitError as e:
+            failures.append(f"calibration fit: {e}")
     comm.close()
     out = [None] * P
     dist.all_gather_object(out, failures)

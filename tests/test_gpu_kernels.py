@@ -175,10 +175,16 @@ def test_plain_allreduce_p1_is_identity_and_calibration_fits():
     assert all(m.time_sec > 0 for m in meas)
     assert meas[-1].time_sec > meas[0].time_sec
     assert model.a > 0 and model.b >= 0
+    meas_e = comm.calibrate_engine(sizes, warmup=1, reps=3)
+    assert all(m.time_sec > 0 for m in meas_e)
+    assert meas_e[-1].time_sec > meas_e[0].time_sec
+    em = gs.fit_model(meas_e)
+    assert em.a > 0 and em.b >= 0
     comm.close()
 
 
-def test_pipeline_p1_replays_backward_and_applies_sgd():
+@pytest.mark.parametrize("engine_ctas", [0, -1, 8])
+def test_pipeline_p1_replays_backward_and_applies_sgd(engine_ctas):
     rng = np.random.default_rng(5)
     counts = RAGGED
     t_b = list(rng.uniform(5e-5, 3e-4, len(counts)))
@@ -188,7 +194,8 @@ def test_pipeline_p1_replays_backward_and_applies_sgd():
     g_dev, w_dev = _dev(g_np), _dev(w_np)
     comm = rt.Comm(0, 1, 0, 4 * rt.padded_elems(counts))
     dp = rt.DevicePlan(comm, g_dev[0], w_dev[0], plan)
-    pipe = rt.Pipeline(dp, tr, LR, record_group_times=True, l2_flush_bytes=64 << 20)
+    pipe = rt.Pipeline(dp, tr, LR, record_group_times=True, l2_flush_bytes=64 << 20,
+                       engine_ctas=engine_ctas)
     ms = pipe.run(4)
     compute_ms = (tr.forward_time + sum(t_b)) * 1e3
     assert all(m >= compute_ms * 0.999 for m in ms), (ms, compute_ms)
