@@ -204,6 +204,10 @@ int mgw_pipeline_run(mgw_pipeline* pipe, int iters, float* iter_ms_out);
 int mgw_pipeline_group_times(mgw_pipeline* pipe, float* group_ms_out);
 /* The compute stream (cudaStream_t) the pipeline runs on. */
 int mgw_pipeline_stream(mgw_pipeline* pipe, void** stream_out);
+/* Diagnostics, readable while the pipeline runs: engine state {groups made
+ * ready, iteration, CTA exit count, ready-timeout flag} and the replay clock
+ * {iteration start, last replay completion} (%globaltimer ns). */
+int mgw_pipeline_debug(mgw_pipeline* pipe, uint32_t* engine_state4, uint64_t* clock2);
 
 /* On-box calibration sweep (N1): for each size, warmup + reps timed runs
  * of the fused group kernel on a single-layer group of size/4 elements;

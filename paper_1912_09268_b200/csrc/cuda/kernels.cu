@@ -332,7 +332,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     if (blockIdx.x >= units) continue;  // same on every rank: no barrier to skip
     if (threadIdx.x == 0) {
       const uint32_t target = iter * E.G + k + 1;
-      while (static_cast<int32_t>(ld_acquire_gpu(E.pipe) - target) < 0) {
+      if (static_cast<int32_t>(ld_acquire_gpu(E.pipe) - target) < 0) {
+        const uint64_t t0 = globaltimer_ns();
+        while (static_cast<int32_t>(ld_acquire_gpu(E.pipe) - target) < 0) {
+          if (globaltimer_ns() - t0 > kBarrierTimeoutNs) {  // compute side never signalled
+            atomicExch(E.pipe + 3, 1u);
+            break;
+          }
+        }
       }
       if (E.stamps != nullptr && blockIdx.x == 0) E.stamps[2 * gi] = globaltimer_ns();
     }

@@ -799,6 +799,14 @@ int mgw_pipeline_run(mgw_pipeline* pipe, int iters, float* iter_ms) {
       ck(cudaEventSynchronize(ev[iters]), "pipeline sync");
       for (int i = 0; i < iters; ++i) ck(cudaEventElapsedTime(&iter_ms[i], ev[i], ev[i + 1]), "elapsed");
       mgw::check_barrier_flags(pipe->plan->comm);
+      if (pipe->d_pipe != nullptr) {
+        uint32_t st[4];
+        ck(cudaMemcpy(st, pipe->d_pipe, sizeof st, cudaMemcpyDeviceToHost), "read pipe state");
+        if (st[3] != 0) {
+          throw mgw::CudaFailure("comm engine timed out waiting for a ready group "
+                                 "(compute stream did not run concurrently?)");
+        }
+      }
     } catch (...) {
       for (auto e : ev) cudaEventDestroy(e);
       throw;
@@ -901,6 +909,31 @@ int mgw_pipeline_stream(mgw_pipeline* pipe, void** stream_out) {
   MGW_TRY {
     require(pipe != nullptr && stream_out != nullptr, "NULL argument");
     *stream_out = pipe->compute;
+  }
+  MGW_CATCH
+}
+
+int mgw_pipeline_debug(mgw_pipeline* pipe, uint32_t* engine_state4, uint64_t* clock2) {
+  MGW_TRY {
+    require(pipe != nullptr, "NULL pipeline");
+    mgw::set_device(pipe->plan->comm);
+    // Read on a private stream: must not wait behind a stuck pipeline.
+    cudaStream_t s = nullptr;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    if (engine_state4 != nullptr) {
+      if (pipe->d_pipe) {
+        ck(cudaMemcpyAsync(engine_state4, pipe->d_pipe, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s),
+           "read pipe");
+      } else {
+        std::memset(engine_state4, 0, 4 * sizeof(uint32_t));
+      }
+    }
+    if (clock2 != nullptr) {
+      ck(cudaMemcpyAsync(clock2, pipe->d_clock, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s),
+         "read clock");
+    }
+    ck(cudaStreamSynchronize(s), "debug sync");
+    cudaStreamDestroy(s);
   }
   MGW_CATCH
 }
