@@ -635,9 +635,15 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
     if (pipe->engine) {
       int occ = 1;
       ck(engine_ctas_per_sm(c->nranks, &occ), "engine occupancy");
-      // the engine runs concurrently with the replay kernel: leave room
-      const int cap = std::min(kMaxCtas, std::max(1, occ) * c->num_sms - 1);
-      pipe->engine_ctas = std::min(cap, engine_ctas < 0 ? c->num_sms : engine_ctas);
+      // The engine runs concurrently with the compute stream, whose kernels
+      // must still find SMs: measured on B200, a 1-thread replay kernel is
+      // NOT scheduled next to engine CTAs when every SM holds one (the
+      // engine then waits forever for a ready signal), so kFreeSms SMs are
+      // always left without an engine CTA. A real backward needs them too.
+      constexpr int kFreeSms = 8;
+      const int cap = std::max(1, std::min({kMaxCtas, std::max(1, occ) * c->num_sms - 1,
+                                            c->num_sms - kFreeSms}));
+      pipe->engine_ctas = std::min(cap, engine_ctas < 0 ? cap : engine_ctas);
       ck(cudaMalloc(&pipe->d_pipe, 4 * sizeof(uint32_t)), "cudaMalloc(pipe)");
       ck(cudaMemset(pipe->d_pipe, 0, 4 * sizeof(uint32_t)), "memset(pipe)");
       ck(cudaMalloc(&pipe->d_group_done, std::max(G, 1) * sizeof(uint32_t)), "cudaMalloc");
