@@ -337,6 +337,11 @@ def main():
         pred = gs.iteration_time(trace, plans[name], model).iteration_time
         strat[name] = {"iter_ms_median": med, "iter_ms_p10": p10, "iter_ms_p90": p90,
                        "predicted_ms": pred * 1e3, "groups": dplans[name].n_groups}
+        if args.engine_ctas != 0:
+            # device clock of the last iteration: exposed comm after the replay
+            tl = pipes[name].device_timeline()
+            strat[name]["device_tail_us"] = D.max_over_ranks(tl["tail_us"], dev)
+            strat[name]["device_replay_ms"] = tl["replay_us"] / 1e3
     compute_ms = (trace.forward_time + sum(l.backward_time for l in trace.layers)) * 1e3
 
     # ---- e2e through the public API with host buffers

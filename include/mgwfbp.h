@@ -208,6 +208,10 @@ int mgw_pipeline_stream(mgw_pipeline* pipe, void** stream_out);
  * ready, iteration, CTA exit count, ready-timeout flag} and the replay clock
  * {iteration start, last replay completion} (%globaltimer ns). */
 int mgw_pipeline_debug(mgw_pipeline* pipe, uint32_t* engine_state4, uint64_t* clock2);
+/* Engine pipelines with record_group_times: the last iteration's raw
+ * (start, end) %globaltimer stamps of every group, 2*G values in group
+ * order (zero for groups without tiles). */
+int mgw_pipeline_stamps(mgw_pipeline* pipe, uint64_t* stamps_2g);
 
 /* On-box calibration sweep (N1): for each size, warmup + reps timed runs
  * of the fused group kernel on a single-layer group of size/4 elements;

@@ -102,6 +102,7 @@ mgw_pipeline_run = _proto("mgw_pipeline_run", [vp, C.c_int, f32p])
 mgw_pipeline_group_times = _proto("mgw_pipeline_group_times", [vp, f32p])
 mgw_pipeline_stream = _proto("mgw_pipeline_stream", [vp, C.POINTER(vp)])
 mgw_pipeline_debug = _proto("mgw_pipeline_debug", [vp, C.POINTER(C.c_uint32), u64p])
+mgw_pipeline_stamps = _proto("mgw_pipeline_stamps", [vp, u64p])
 mgw_kernel_launches = _proto("mgw_kernel_launches", [], C.c_uint64)
 
 # Every symbol the header declares (checked by tests/test_capi_symbols.py).

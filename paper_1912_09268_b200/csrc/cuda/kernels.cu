@@ -400,6 +400,25 @@ __global__ void __launch_bounds__(kThreads) unpack_sgd_kernel(const Tile* tiles,
   }
 }
 
+// The whole backward replay of one iteration in ONE thread (engine
+// pipelines): spin to each group head's ready time in backward order and
+// mark the group ready for the comm engine. No per-group kernel launches, so
+// the emulated compute stream is continuously busy and its timing exact.
+__global__ void replay_all_kernel(unsigned long long* clock, const unsigned long long* deadlines,
+                                  uint32_t n, uint32_t* ready) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long t0 = globaltimer_ns();
+  clock[0] = t0;
+  unsigned long long now = t0;
+  for (uint32_t k = 0; k < n; ++k) {
+    const unsigned long long due = t0 + deadlines[k];
+    while (now < due) now = globaltimer_ns();
+    __threadfence();
+    atomicAdd(ready, 1u);
+  }
+  clock[1] = now;
+}
+
 // clock[0]: iteration start (written by the first replay kernel of an
 // iteration), clock[1]: completion time of the latest replay kernel. When
 // `ready` is given, the group is marked ready for the comm engine.
@@ -514,6 +533,12 @@ cudaError_t launch_unpack_sgd(const Tile* tiles, uint32_t n_tiles, float* const*
 cudaError_t launch_replay(unsigned long long* clock, unsigned long long deadline_ns, int first,
                           uint32_t* ready, cudaStream_t stream) {
   replay_kernel<<<1, 32, 0, stream>>>(clock, deadline_ns, first, ready);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long long* deadlines_ns,
+                              uint32_t n, uint32_t* ready, cudaStream_t stream) {
+  replay_all_kernel<<<1, 32, 0, stream>>>(clock, deadlines_ns, n, ready);
   return cudaGetLastError();
 }
 

@@ -36,6 +36,8 @@ cudaError_t launch_unpack_sgd(const Tile* tiles, uint32_t n_tiles, float* const*
 cudaError_t launch_replay(unsigned long long* clock, unsigned long long deadline_ns, int first,
                           uint32_t* ready, cudaStream_t stream);
 cudaError_t launch_engine(const EngineLaunch& E, int ctas, cudaStream_t stream);
+cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long long* deadlines_ns,
+                              uint32_t n, uint32_t* ready, cudaStream_t stream);
 cudaError_t engine_ctas_per_sm(int nranks, int* out);
 
 std::atomic<uint64_t> g_kernel_launches{0};
@@ -129,6 +131,7 @@ struct mgw_pipeline {
   uint32_t* d_group_done = nullptr;       // G
   unsigned long long* d_stamps = nullptr; // 2G
   mgw::EngineGroup* d_groups = nullptr;   // G
+  unsigned long long* d_deadlines = nullptr;  // G group-head ready times (ns), backward order
 };
 
 namespace mgw {
@@ -660,6 +663,17 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
       ck(cudaMalloc(&pipe->d_groups, std::max(G, 1) * sizeof(EngineGroup)), "cudaMalloc(groups)");
       ck(cudaMemcpy(pipe->d_groups, groups.data(), G * sizeof(EngineGroup), cudaMemcpyHostToDevice),
          "upload groups");
+      // ready time of every group head, in backward (comm) order
+      std::vector<unsigned long long> dl;
+      for (int g = G - 1; g >= 0; --g) {
+        const size_t head = p->heads[g];
+        dl.push_back(static_cast<unsigned long long>(std::llround((tau_b[head] + t_b[head]) * 1e9)));
+      }
+      ck(cudaMalloc(&pipe->d_deadlines, std::max<size_t>(dl.size(), 1) * sizeof(unsigned long long)),
+         "cudaMalloc(deadlines)");
+      ck(cudaMemcpy(pipe->d_deadlines, dl.data(), dl.size() * sizeof(unsigned long long),
+                    cudaMemcpyHostToDevice),
+         "upload deadlines");
     }
     ck(cudaStreamCreateWithFlags(&pipe->compute, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&pipe->comm, cudaStreamNonBlocking), "stream");
@@ -706,16 +720,19 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
         E.stamps = timed ? pipe->d_stamps : nullptr;
         ck(launch_engine(E, pipe->engine_ctas, pipe->comm), "engine launch");
       }
+      if (pipe->engine) {
+        // one replay kernel walks every group head's ready time
+        ck(launch_replay_all(pipe->d_clock, pipe->d_deadlines, static_cast<uint32_t>(G), pipe->d_pipe,
+                             pipe->compute),
+           "replay");
+      }
       bool first = true;
-      for (int g = G - 1; g >= 0; --g) {
+      for (int g = G - 1; g >= 0 && !pipe->engine; --g) {
         const size_t head = p->heads[g];
         const double ready_s = tau_b[head] + t_b[head];
         const auto deadline = static_cast<unsigned long long>(std::llround(ready_s * 1e9));
-        ck(launch_replay(pipe->d_clock, deadline, first ? 1 : 0,
-                         pipe->engine ? pipe->d_pipe : nullptr, pipe->compute),
-           "replay");
+        ck(launch_replay(pipe->d_clock, deadline, first ? 1 : 0, nullptr, pipe->compute), "replay");
         first = false;
-        if (pipe->engine) continue;
         ck(cudaEventRecord(pipe->ready[g], pipe->compute), "ready");
         ck(cudaStreamWaitEvent(pipe->comm, pipe->ready[g], 0), "ready wait");
         if (pipe->timed_groups) {
@@ -742,7 +759,7 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
       // the capture counted kernels once; graph replays add per launch
       g_kernel_launches.fetch_sub(static_cast<uint64_t>(G), std::memory_order_relaxed);
     }
-    pipe->kernels_per_iter = pipe->engine ? G + 1 : 2 * G;
+    pipe->kernels_per_iter = pipe->engine ? 2 : 2 * G;  // engine + replay, or replay + group each
     return pipe;
   }
 }
@@ -770,6 +787,7 @@ int mgw_pipeline_destroy(mgw_pipeline* pipe) {
     if (pipe->d_group_done) cudaFree(pipe->d_group_done);
     if (pipe->d_stamps) cudaFree(pipe->d_stamps);
     if (pipe->d_groups) cudaFree(pipe->d_groups);
+    if (pipe->d_deadlines) cudaFree(pipe->d_deadlines);
     cudaStreamDestroy(pipe->compute);
     cudaStreamDestroy(pipe->comm);
     delete pipe;
@@ -915,6 +933,19 @@ int mgw_pipeline_stream(mgw_pipeline* pipe, void** stream_out) {
   MGW_TRY {
     require(pipe != nullptr && stream_out != nullptr, "NULL argument");
     *stream_out = pipe->compute;
+  }
+  MGW_CATCH
+}
+
+int mgw_pipeline_stamps(mgw_pipeline* pipe, uint64_t* stamps_2g) {
+  MGW_TRY {
+    require(pipe != nullptr && stamps_2g != nullptr && pipe->engine && pipe->timed_groups,
+            "stamps need an engine pipeline created with record_group_times");
+    mgw::set_device(pipe->plan->comm);
+    ck(cudaStreamSynchronize(pipe->compute), "sync");
+    ck(cudaMemcpy(stamps_2g, pipe->d_stamps, 2 * pipe->plan->G() * sizeof(uint64_t),
+                  cudaMemcpyDeviceToHost),
+       "read stamps");
   }
   MGW_CATCH
 }

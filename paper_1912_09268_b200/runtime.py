@@ -189,6 +189,22 @@ class Pipeline:
         check(_lib.mgw_pipeline_run(self.handle, iters, out))
         return list(out)
 
+    def device_timeline(self) -> dict:
+        """Last iteration on the device clock (engine pipelines with
+        record_group_times): replay span, end of the last group's comm, and
+        the exposed tail between them, in microseconds."""
+        G = self.dplan.n_groups
+        st = (C.c_uint64 * max(1, 2 * G))()
+        check(_lib.mgw_pipeline_stamps(self.handle, st))
+        eng = (C.c_uint32 * 4)()
+        clk = (C.c_uint64 * 2)()
+        check(_lib.mgw_pipeline_debug(self.handle, eng, clk))
+        t0, rend = clk[0], clk[1]
+        ends = [st[2 * g + 1] for g in range(G) if st[2 * g + 1]]
+        end = max(ends) if ends else rend
+        return {"replay_us": (rend - t0) / 1e3, "comm_end_us": (end - t0) / 1e3,
+                "tail_us": (end - rend) / 1e3}
+
     def group_times_ms(self) -> List[float]:
         out = (C.c_float * max(1, self.dplan.n_groups))()
         check(_lib.mgw_pipeline_group_times(self.handle, out))
