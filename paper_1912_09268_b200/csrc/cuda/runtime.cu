@@ -39,6 +39,7 @@ cudaError_t launch_engine(const EngineLaunch& E, int ctas, cudaStream_t stream);
 cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long long* deadlines_ns,
                               uint32_t n, uint32_t* ready, cudaStream_t stream);
 cudaError_t engine_ctas_per_sm(int nranks, int* out);
+cudaError_t launch_l2_flush(void* buf, size_t bytes, int ctas, cudaStream_t stream);
 
 std::atomic<uint64_t> g_kernel_launches{0};
 
@@ -701,8 +702,7 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
       if (pipe->flush_bytes > 0) {
         // The comm stream is idle until the first group is ready: evict L2
         // there while the compute stream replays the forward pass.
-        ck(cudaMemsetAsync(pipe->flush_buf, pipe->iter_flush_value, pipe->flush_bytes, pipe->comm),
-           "l2 flush");
+        ck(launch_l2_flush(pipe->flush_buf, pipe->flush_bytes, 16, pipe->comm), "l2 flush");
       }
       if (pipe->engine) {
         EngineLaunch E{};
@@ -759,7 +759,8 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
       // the capture counted kernels once; graph replays add per launch
       g_kernel_launches.fetch_sub(static_cast<uint64_t>(G), std::memory_order_relaxed);
     }
-    pipe->kernels_per_iter = pipe->engine ? 2 : 2 * G;  // engine + replay, or replay + group each
+    // engine + replay, or replay + group kernel per group; plus the L2 flush
+    pipe->kernels_per_iter = (pipe->engine ? 2 : 2 * G) + (pipe->flush_bytes > 0 ? 1 : 0);
     return pipe;
   }
 }

@@ -1,0 +1,47 @@
+"""Merged all-reduce bus bandwidth probe at P ranks (torchrun, tools only):
+fused engine kernel (one-shot / two-shot, CTA counts) vs NCCL, large sizes."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_1912_09268_b200 import dist as D  # noqa: E402
+from paper_1912_09268_b200 import runtime as rt  # noqa: E402
+
+rank, P, local = D.init("nccl")
+dev = torch.device("cuda", local)
+sizes = [int(s) << 20 for s in os.environ.get("SIZES_MB", "1,4,16,64,256").split(",")]
+comm = rt.Comm(rank, P, local, max(sizes) + (1 << 20))
+f = 2 * (P - 1) / P
+out = []
+for algo in os.environ.get("ALGOS", "oneshot,twoshot").split(","):
+    for ctas in [int(c) for c in os.environ.get("CTAS", "64,140").split(",")]:
+        m = comm.calibrate_engine(sizes, warmup=1, reps=3, algo=algo, engine_ctas=ctas)
+        t = torch.tensor([x.time_sec for x in m], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out.append((f"engine {algo} ctas={ctas}", [f * s / tt / 1e9 for s, tt in zip(sizes, t.tolist())],
+                    [tt * 1e6 for tt in t.tolist()]))
+nccl = []
+for s in sizes:
+    x = torch.ones(s // 4, device=dev)
+    for _ in range(3):
+        dist.all_reduce(x)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(10):
+        dist.all_reduce(x)
+    e1.record()
+    e1.synchronize()
+    tt = torch.tensor([e0.elapsed_time(e1) / 10 / 1e3], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    nccl.append(tt.item())
+out.append(("nccl", [f * s / tt / 1e9 for s, tt in zip(sizes, nccl)], [tt * 1e6 for tt in nccl]))
+if rank == 0:
+    print(f"P={P} sizes(MiB)={[s >> 20 for s in sizes]}  bus GB/s (time us)")
+    for name, bw, us in out:
+        print(f"  {name:28s}", "  ".join(f"{b:7.1f} ({u:8.1f})" for b, u in zip(bw, us)), flush=True)
+comm.close()
+dist.destroy_process_group()
