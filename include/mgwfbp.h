@@ -122,8 +122,9 @@ typedef struct mgw_plan mgw_plan;
 typedef struct mgw_pipeline mgw_pipeline;
 
 /* Per-rank communicator on `device`: allocates the symmetric merge arena
- * (2 x arena_bytes: double-buffered by launch parity) and the signal area.
- * nranks in {1, 2, 4, 8}. */
+ * (nranks slots of arena_bytes: slot r receives rank r's scaled gradients
+ * as posted NVLink stores) and the signal area. arena_bytes must hold the
+ * padded merge layout of every plan used with it. nranks in {1, 2, 4, 8}. */
 int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_comm** out);
 
 /* CUDA IPC handles of this rank's arena + signal area (opaque bytes). */

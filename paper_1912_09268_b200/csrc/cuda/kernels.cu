@@ -1,13 +1,13 @@
 // mgwfbp-b200 sm_100a kernels.
 //
 //  run_group<P>  — THE hot op, shared by both launch styles: for one merge
-//      group, pack (gather layer grads x 1/P into the merge arena) ->
-//      all-reduce over NVLink peer memory, summed in rank order ->
+//      group, pack (gather layer grads x 1/P) fused with a push over NVLink
+//      into the peers' merge arenas -> rank-order reduction from local HBM ->
 //      unpack + SGD into the layer weights.
-//        one-shot: every rank reads every peer's packed tiles; 1 barrier.
-//        two-shot: tile t is owned by rank t % P; owners reduce their tiles
-//          in place (reduce-scatter), then every rank pulls the other
-//          owners' reduced tiles (all-gather) fused with SGD; 2 barriers.
+//        one-shot: every rank pushes its tiles to every rank; 1 barrier.
+//        two-shot: tile t is owned by rank t % P; ranks push each tile to its
+//          owner (reduce-scatter), owners reduce + push the result to every
+//          peer (all-gather) fused with SGD; 2 barriers.
 //  engine_kernel<P> — the persistent comm engine: one launch per iteration
 //      runs every group in backward order as soon as the compute side marks
 //      its head ready (paper Algorithm 2's daemon thread, on the GPU; no
@@ -100,7 +100,10 @@ __device__ __forceinline__ void epilogue(const Tile& t, uint32_t e, float4 g, fl
 // then wait for every peer's signal (ld.acquire.sys), bounded by a timeout
 // that records an error instead of hanging the GPU.
 __device__ __forceinline__ void rank_barrier(const RankView& v, int P, int plane, uint32_t epoch,
-                                             uint32_t cta) {
+                                             uint32_t cta, bool after_remote_stores = true) {
+  // Every warp's posted NVLink stores must be visible system-wide before
+  // this CTA's flag is: each warp fences its own stores, then bar.sync.
+  if (after_remote_stores) __threadfence_system();
   __syncthreads();
   if (threadIdx.x < P) {
     const int q = threadIdx.x;
@@ -135,26 +138,52 @@ __device__ __forceinline__ void finish_launch(const RankView& v, uint32_t seq, u
   }
 }
 
-// Vectors per batch of peer loads: all of a thread's vectors for small P
-// (2P loads in flight), one at a time for P = 8 (8 in flight, ~64 KiB per
-// CTA) so the persistent engine stays within 128 registers without spills.
-template <int P>
-struct Batch {
-  static constexpr uint32_t kVec = P >= 8 ? 1 : kVecPerThread;
-  static constexpr int kPeers = P >= 8 ? 4 : P;  // all-gather: peers per load batch
-};
+// ---- push data path -------------------------------------------------------
+// Every rank's merge arena holds one SLOT per source rank (slot r at element
+// r * slot_stride, laid out like the merge buffer). Transfers are posted
+// NVLink stores into the peers' slots (no remote-load latency on the
+// critical path); every reduction reads local HBM only.
 
-// Reduce tile t over all ranks in rank order (x0 + x1 + ... + x_{P-1}, each
-// already scaled by 1/P in the pack), optionally store the sum in place in
-// this rank's arena (two-shot owner), then unpack + SGD.
+// Gather + scale tile t of this rank's gradients and store it into slot
+// `me` of the arenas of ranks [q_begin, q_end) — the pack kernel fused with
+// the scatter. kVecPerThread loads are issued before any store.
 template <int P>
-__device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, uint64_t copy_off,
-                                            float* inplace, float lr, int epi) {
-  constexpr uint32_t B = Batch<P>::kVec;
+__device__ __forceinline__ void scatter_tile(const RankView& v, const Tile& t, int q_begin, int q_end,
+                                             uint64_t my_slot, float scale) {
+  const float* src = v.grads[t.layer & kLayerMask] + t.src;
+  const bool aligned = !(t.layer & kGradUnaligned);
   const uint32_t nvec = (t.len + 3) >> 2;
-  const uint32_t layer = t.layer & kLayerMask;
-  float* w = v.weights[layer];
-  float* g = v.grads[layer];
+  float4 x[kVecPerThread];
+#pragma unroll
+  for (uint32_t k = 0; k < kVecPerThread; ++k) {
+    const uint32_t e = (threadIdx.x + k * kThreads) * 4;
+    if (e < nvec * 4) {
+      x[k] = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
+      x[k] = mul4(x[k], scale);
+    }
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < kVecPerThread; ++k) {
+    const uint32_t e = (threadIdx.x + k * kThreads) * 4;
+    if (e < nvec * 4) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        if (q >= q_begin && q < q_end) st_v4(v.arena[q] + my_slot + t.moff + e, x[k]);
+      }
+    }
+  }
+}
+
+// Rank-order sum of tile t over the P local slots (x0 + x1 + ... + x_{P-1},
+// each already scaled by 1/P); all loads are local (.cg: peers wrote them).
+template <int P>
+__device__ __forceinline__ void reduce_slots(const RankView& v, const Tile& t, uint64_t slot_stride,
+                                             float4 (&acc)[kVecPerThread]) {
+  const float* base = v.arena[v.rank] + t.moff;
+  const uint32_t nvec = (t.len + 3) >> 2;
+  // all kVecPerThread x P loads in flight for P <= 4; one vector's P loads
+  // at a time for P = 8 (keeps the engine at <= 128 registers, no spills)
+  constexpr uint32_t B = P >= 8 ? 1 : kVecPerThread;
 #pragma unroll
   for (uint32_t k0 = 0; k0 < kVecPerThread; k0 += B) {
     float4 x[B][P];
@@ -163,96 +192,110 @@ __device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, ui
       const uint32_t i = threadIdx.x + (k0 + j) * kThreads;
       if (i < nvec) {
 #pragma unroll
-        for (int q = 0; q < P; ++q) x[j][q] = ld_cg_v4(v.arena[q] + copy_off + t.moff + i * 4);
+        for (int r = 0; r < P; ++r) x[j][r] = ld_cg_v4(base + r * slot_stride + i * 4);
       }
     }
 #pragma unroll
     for (uint32_t j = 0; j < B; ++j) {
-      const uint32_t i = threadIdx.x + (k0 + j) * kThreads;
-      if (i < nvec) {
-        float4 s = x[j][0];
+      float4 s = x[j][0];
 #pragma unroll
-        for (int q = 1; q < P; ++q) s = add4(s, x[j][q]);
-        if (inplace != nullptr) st_v4(inplace + t.moff + i * 4, s);
-        epilogue(t, i * 4, s, w, g, lr, epi);
-      }
+      for (int r = 1; r < P; ++r) s = add4(s, x[j][r]);
+      acc[k0 + j] = s;
     }
   }
 }
 
-// One-shot body: pack my tiles, barrier, pull every rank's copy of my tiles
-// and reduce them in rank order, unpack + SGD.
+// One-shot: scatter my tiles to every rank, barrier, reduce the P slots of
+// my tiles locally, unpack + SGD. NVLink: (P-1) * S posted writes per rank.
 template <int P>
 __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* tiles,
-                                               uint32_t n_tiles, uint32_t epoch, uint64_t copy_off,
+                                               uint32_t n_tiles, uint32_t epoch, uint64_t slot_stride,
                                                float scale, float lr, int epi, uint32_t cta,
                                                uint32_t ncta) {
-  float* mine = v.arena[v.rank] + copy_off;
-  for (uint32_t ti = cta; ti < n_tiles; ti += ncta) pack_tile(tiles[ti], v.grads, mine, scale);
+  const uint64_t my_slot = static_cast<uint64_t>(v.rank) * slot_stride;
+  for (uint32_t ti = cta; ti < n_tiles; ti += ncta) scatter_tile<P>(v, tiles[ti], 0, P, my_slot, scale);
   rank_barrier(v, P, 0, epoch, cta);
   for (uint32_t ti = cta; ti < n_tiles; ti += ncta) {
-    reduce_tile<P>(v, tiles[ti], copy_off, nullptr, lr, epi);
+    const Tile t = tiles[ti];
+    float4 acc[kVecPerThread];
+    reduce_slots<P>(v, t, slot_stride, acc);
+    const uint32_t layer = t.layer & kLayerMask;
+    float* w = v.weights[layer];
+    float* g = v.grads[layer];
+    const uint32_t nvec = (t.len + 3) >> 2;
+#pragma unroll
+    for (uint32_t k = 0; k < kVecPerThread; ++k) {
+      const uint32_t i = threadIdx.x + k * kThreads;
+      if (i < nvec) epilogue(t, i * 4, acc[k], w, g, lr, epi);
+    }
   }
 }
 
-// Two-shot body: reduce-scatter to tile owners (in place), then all-gather
-// fused with unpack + SGD.
+// Two-shot: tile t of super-tile s = tiles [s*P, s*P+P) is owned by rank
+// t % P. Reduce-scatter: scatter each tile to its owner's slot `me`;
+// owners reduce their tiles locally in rank order, apply SGD, and push the
+// reduced tile into slot `owner` of every peer (all-gather); barrier; every
+// rank applies the other owners' reduced tiles from its local slots.
+// NVLink: 2 (P-1)/P * S posted writes per rank.
 template <int P>
 __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* tiles,
-                                               uint32_t n_tiles, uint32_t epoch, uint64_t copy_off,
+                                               uint32_t n_tiles, uint32_t epoch, uint64_t slot_stride,
                                                float scale, float lr, int epi, uint32_t cta,
                                                uint32_t ncta) {
-  float* mine = v.arena[v.rank] + copy_off;
-  // Tiles are dealt to owners round-robin: super-tile s = tiles [s*P, s*P+P).
+  const uint64_t my_slot = static_cast<uint64_t>(v.rank) * slot_stride;
   const uint32_t n_super = (n_tiles + P - 1) / P;
   for (uint32_t s = cta; s < n_super; s += ncta) {
 #pragma unroll
     for (int q = 0; q < P; ++q) {
       const uint32_t ti = s * P + q;
-      if (ti < n_tiles) pack_tile(tiles[ti], v.grads, mine, scale);
+      if (ti < n_tiles) scatter_tile<P>(v, tiles[ti], q, q + 1, my_slot, scale);
     }
   }
   rank_barrier(v, P, 0, epoch, cta);
   for (uint32_t s = cta; s < n_super; s += ncta) {
     const uint32_t ti = s * P + v.rank;
-    if (ti < n_tiles) reduce_tile<P>(v, tiles[ti], copy_off, mine, lr, epi);
+    if (ti >= n_tiles) continue;
+    const Tile t = tiles[ti];
+    float4 acc[kVecPerThread];
+    reduce_slots<P>(v, t, slot_stride, acc);
+    const uint32_t layer = t.layer & kLayerMask;
+    float* w = v.weights[layer];
+    float* g = v.grads[layer];
+    const uint32_t nvec = (t.len + 3) >> 2;
+#pragma unroll
+    for (uint32_t k = 0; k < kVecPerThread; ++k) {
+      const uint32_t i = threadIdx.x + k * kThreads;
+      if (i < nvec) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          if (q != v.rank) st_v4(v.arena[q] + my_slot + t.moff + i * 4, acc[k]);
+        }
+        epilogue(t, i * 4, acc[k], w, g, lr, epi);
+      }
+    }
   }
   rank_barrier(v, P, 1, epoch, cta);
-  // All-gather fused with unpack + SGD: pull the other owners' tiles,
-  // kPeers tiles x kVecPerThread vectors of loads in flight per batch.
-  constexpr int QC = Batch<P>::kPeers;
   for (uint32_t s = cta; s < n_super; s += ncta) {
 #pragma unroll
-    for (int q0 = 0; q0 < P; q0 += QC) {
-      float4 x[QC][kVecPerThread];
+    for (int q = 0; q < P; ++q) {
+      const uint32_t ti = s * P + q;
+      if (q == v.rank || ti >= n_tiles) continue;
+      const Tile t = tiles[ti];
+      const float* red = v.arena[v.rank] + static_cast<uint64_t>(q) * slot_stride + t.moff;
+      const uint32_t layer = t.layer & kLayerMask;
+      float* w = v.weights[layer];
+      float* g = v.grads[layer];
+      const uint32_t nvec = (t.len + 3) >> 2;
+      float4 x[kVecPerThread];
 #pragma unroll
-      for (int j = 0; j < QC; ++j) {
-        const int q = q0 + j;
-        const uint32_t ti = s * P + q;
-        if (q == v.rank || ti >= n_tiles) continue;
-        const Tile t = tiles[ti];
-        const uint32_t nvec = (t.len + 3) >> 2;
-#pragma unroll
-        for (uint32_t k = 0; k < kVecPerThread; ++k) {
-          const uint32_t i = threadIdx.x + k * kThreads;
-          if (i < nvec) x[j][k] = ld_cg_v4(v.arena[q] + copy_off + t.moff + i * 4);
-        }
+      for (uint32_t k = 0; k < kVecPerThread; ++k) {
+        const uint32_t i = threadIdx.x + k * kThreads;
+        if (i < nvec) x[k] = ld_cg_v4(red + i * 4);
       }
 #pragma unroll
-      for (int j = 0; j < QC; ++j) {
-        const int q = q0 + j;
-        const uint32_t ti = s * P + q;
-        if (q == v.rank || ti >= n_tiles) continue;
-        const Tile t = tiles[ti];
-        const uint32_t layer = t.layer & kLayerMask;
-        const uint32_t nvec = (t.len + 3) >> 2;
-        float* w = v.weights[layer];
-        float* g = v.grads[layer];
-#pragma unroll
-        for (uint32_t k = 0; k < kVecPerThread; ++k) {
-          const uint32_t i = threadIdx.x + k * kThreads;
-          if (i < nvec) epilogue(t, i * 4, x[j][k], w, g, lr, epi);
-        }
+      for (uint32_t k = 0; k < kVecPerThread; ++k) {
+        const uint32_t i = threadIdx.x + k * kThreads;
+        if (i < nvec) epilogue(t, i * 4, x[k], w, g, lr, epi);
       }
     }
   }
@@ -262,7 +305,7 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
 // group's barriers; `copy_off` selects the merge-arena copy.
 template <int P>
 __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, const Tile* tiles,
-                                          uint32_t n_tiles, uint32_t epoch, uint64_t copy_off,
+                                          uint32_t n_tiles, uint32_t epoch, uint64_t slot_stride,
                                           float scale, float lr, int epi, uint32_t cta,
                                           uint32_t ncta) {
   if constexpr (P == 1) {
@@ -283,9 +326,9 @@ __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, cons
     }
   } else {
     if (two_shot) {
-      two_shot_group<P>(v, tiles, n_tiles, epoch, copy_off, scale, lr, epi, cta, ncta);
+      two_shot_group<P>(v, tiles, n_tiles, epoch, slot_stride, scale, lr, epi, cta, ncta);
     } else {
-      one_shot_group<P>(v, tiles, n_tiles, epoch, copy_off, scale, lr, epi, cta, ncta);
+      one_shot_group<P>(v, tiles, n_tiles, epoch, slot_stride, scale, lr, epi, cta, ncta);
     }
   }
 }
@@ -301,11 +344,9 @@ __global__ void __launch_bounds__(kThreads, 1) group_allreduce_kernel(const __gr
     if (threadIdx.x == 0) s_seq = ld_volatile_u32(v.state);
     __syncthreads();
     const uint32_t seq = s_seq;
-    rank_barrier(v, P, 1, seq + 1, blockIdx.x);  // entry: peers have left every older launch
-    const uint32_t epoch = seq + 2;
-    const uint64_t copy_off = static_cast<uint64_t>(epoch & 1u) * L.copy_stride;
-    run_group<P>(TWO_SHOT, v, L.tiles, L.n_tiles, epoch, copy_off, L.scale, L.lr, L.epilogue,
-                 blockIdx.x, gridDim.x);
+    rank_barrier(v, P, 1, seq + 1, blockIdx.x, false);  // entry: peers have left every older launch
+    run_group<P>(TWO_SHOT, v, L.tiles, L.n_tiles, seq + 2, L.slot_stride, L.scale, L.lr,
+                 L.epilogue, blockIdx.x, gridDim.x);
     finish_launch(v, seq, 2);
   }
 }
@@ -323,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
   const uint32_t iter = s_iter;
   // Entry barrier (runs while the compute stream replays the forward pass):
   // every peer has finished every older launch before anything is packed.
-  if constexpr (P > 1) rank_barrier(v, P, 1, seq + 1, blockIdx.x);
+  if constexpr (P > 1) rank_barrier(v, P, 1, seq + 1, blockIdx.x, false);
   for (uint32_t k = 0; k < E.G; ++k) {
     const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
     const EngineGroup grp = E.groups[gi];
@@ -344,10 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       if (E.stamps != nullptr && blockIdx.x == 0) E.stamps[2 * gi] = globaltimer_ns();
     }
     __syncthreads();
-    const uint32_t epoch = seq + 2 + k;
-    const uint64_t copy_off = static_cast<uint64_t>(epoch & 1u) * E.copy_stride;
-    run_group<P>(two, v, E.tiles + grp.tile_first, grp.n_tiles, epoch, copy_off, E.scale, E.lr,
-                 E.epilogue, blockIdx.x, gridDim.x);
+    run_group<P>(two, v, E.tiles + grp.tile_first, grp.n_tiles, seq + 2 + k, E.slot_stride,
+                 E.scale, E.lr, E.epilogue, blockIdx.x, gridDim.x);
     if (E.stamps != nullptr) {
       __syncthreads();
       if (threadIdx.x == 0) {

@@ -2,12 +2,14 @@
 // kernels (kernels.cu) and the host runtime (runtime.cu).
 //
 // Data layout in HBM (per rank):
-//   merge arena   2 copies x (padded model elements) fp32, selected by the
-//                 parity of the communicator's launch counter. Layer l of
-//                 the plan lives at element offs[l] (16-byte aligned), so
-//                 every merge group [head_g, head_{g+1}) is one contiguous
-//                 span — the paper's pre-allocated merge buffers
-//                  laid out once for all groups.
+//   merge arena   P slots x (padded model elements) fp32; slot r receives
+//                 rank r's scaled gradients (posted NVLink stores — the push
+//                 data path). Layer l of the plan lives at element offs[l]
+//                 of a slot (16-byte aligned), so every merge group
+//                 [head_g, head_{g+1}) is one contiguous span — the paper's
+//                 pre-allocated merge buffers laid out
+//                 once for all groups. Reuse across launches is made safe by
+//                 an entry barrier, not by double buffering.
 //   signal area   two barrier planes x kMaxCtas x kMaxRanks uint32 flags,
 //                 written by peers over NVLink (st.release.sys) and spun on
 //                 locally (ld.acquire.sys).
@@ -59,7 +61,7 @@ struct GroupLaunch {
   float scale;           // 1/P, applied in the pack phase
   float lr;
   int epilogue;          // MGW_SGD | MGW_WRITE_GRAD
-  uint64_t copy_stride;  // elements between the two arena copies
+  uint64_t slot_stride;  // elements between the per-source-rank slots of an arena
   RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
 };
 
@@ -83,7 +85,7 @@ struct EngineLaunch {
   float scale;
   float lr;
   int epilogue;
-  uint64_t copy_stride;
+  uint64_t slot_stride;
   uint32_t* pipe;                // [0] groups made ready (monotone), [1] iteration, [2] CTA exit count
   uint32_t* group_done;          // G counters for end stamps (NULL: no timing)
   unsigned long long* stamps;    // 2*G: (start, end) %globaltimer of each group (NULL: no timing)

@@ -147,10 +147,12 @@ uint32_t* alloc_zero_u32(size_t words) {
   return p;
 }
 
-float* alloc_arena(size_t elems) {
+// One slot of `elems` floats per source rank (push data path).
+float* alloc_arena(size_t elems, int nranks) {
   float* p = nullptr;
-  ck(cudaMalloc(&p, std::max<size_t>(2 * elems, 4) * sizeof(float)), "cudaMalloc(arena)");
-  ck(cudaMemset(p, 0, std::max<size_t>(2 * elems, 4) * sizeof(float)), "cudaMemset(arena)");
+  const size_t n = std::max<size_t>(static_cast<size_t>(nranks) * elems, 4);
+  ck(cudaMalloc(&p, n * sizeof(float)), "cudaMalloc(arena)");
+  ck(cudaMemset(p, 0, n * sizeof(float)), "cudaMemset(arena)");
   return p;
 }
 
@@ -218,7 +220,7 @@ void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStre
   L.scale = 1.0f / static_cast<float>(c->nranks);
   L.lr = lr;
   L.epilogue = epilogue;
-  L.copy_stride = c->arena_elems;
+  L.slot_stride = c->arena_elems;
   for (int r = 0; r < p->n_views; ++r) {
     L.views[r] = make_view(c, r, p->d_grads + static_cast<size_t>(r) * p->L,
                            p->d_weights + static_cast<size_t>(r) * p->L);
@@ -335,7 +337,7 @@ int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_co
     c->rank = rank;
     c->nranks = nranks;
     mgw::init_common(c, device, arena_bytes);
-    c->arenas.push_back(mgw::alloc_arena(c->arena_elems));
+    c->arenas.push_back(mgw::alloc_arena(c->arena_elems, nranks));
     c->signals.push_back(mgw::alloc_zero_u32(mgw::kSignalWords));
     c->states.push_back(mgw::alloc_zero_u32(mgw::kStateWords));
     ck(cudaDeviceSynchronize(), "init sync");
@@ -356,7 +358,7 @@ int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_com
     c->loopback = true;
     mgw::init_common(c, device, arena_bytes);
     for (int r = 0; r < nranks; ++r) {
-      c->arenas.push_back(mgw::alloc_arena(c->arena_elems));
+      c->arenas.push_back(mgw::alloc_arena(c->arena_elems, nranks));
       c->signals.push_back(mgw::alloc_zero_u32(mgw::kSignalWords));
       c->states.push_back(mgw::alloc_zero_u32(mgw::kStateWords));
     }
@@ -527,7 +529,7 @@ int mgw_allreduce(mgw_comm* c, float* buf, size_t n, int algo, void* stream) {
     L.scale = 1.0f;
     L.lr = 0.0f;
     L.epilogue = MGW_WRITE_GRAD;
-    L.copy_stride = c->arena_elems;
+    L.slot_stride = c->arena_elems;
     L.views[0] = mgw::make_view(c, 0, p->d_grads, p->d_weights);
     const bool two = mgw::use_two_shot(c, static_cast<uint64_t>(n) * 4, algo);
     ck(mgw::launch_group_allreduce(L, mgw::grid_for(c, L.n_tiles, two), two, false,
@@ -714,7 +716,7 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
         E.scale = 1.0f / static_cast<float>(c->nranks);
         E.lr = lr;
         E.epilogue = MGW_SGD;
-        E.copy_stride = c->arena_elems;
+        E.slot_stride = c->arena_elems;
         E.pipe = pipe->d_pipe;
         E.group_done = timed ? pipe->d_group_done : nullptr;
         E.stamps = timed ? pipe->d_stamps : nullptr;
