@@ -4,10 +4,13 @@
 //      group, pack (gather layer grads x 1/P) fused with a push over NVLink
 //      into the peers' merge arenas -> rank-order reduction from local HBM ->
 //      unpack + SGD into the layer weights.
-//        one-shot: every rank pushes its tiles to every rank; 1 barrier.
+//        one-shot: every rank pushes its tiles to every rank; 1 barrier per
+//          chunk.
 //        two-shot: tile t is owned by rank t % P; ranks push each tile to its
 //          owner (reduce-scatter), owners reduce + push the result to every
-//          peer (all-gather) fused with SGD; 2 barriers.
+//          peer (all-gather) fused with SGD; 2 barriers per chunk.
+//      A CTA walks its tiles in CHUNKS (push -> barrier -> reduce per chunk),
+//      so different CTAs overlap NVLink transfer with local HBM work.
 //  engine_kernel<P> — the persistent comm engine: one launch per iteration
 //      runs every group in backward order as soon as the compute side marks
 //      its head ready (paper Algorithm 2's daemon thread, on the GPU; no
@@ -17,17 +20,19 @@
 //      loopback emulation of P ranks in one cooperative launch).
 //  pack_kernel / unpack_sgd_kernel — the standalone pack and unpack+SGD
 //      ops of the C ABI (rank-local, HBM-bound).
-//  replay_kernel — backward-pass replay: one thread spins on %globaltimer
-//      until a group head's ready time, then marks the group ready.
+//  replay_all_kernel / replay_kernel — backward-pass replay on %globaltimer.
 //
 // Cross-rank synchronisation is per CTA index: CTA b of every rank handles
-// the same tiles, so CTA b only waits for CTA b of the peers (flag plane
-// [b][src_rank], epochs from a per-rank launch counter, monotone, never
-// reset). Every collective launch starts with an entry barrier over all its
-// CTAs, so no rank overwrites its merge arena while a peer may still read it
-// from an earlier launch. Reductions use __fadd_rn / __fmul_rn / __fsub_rn
-// only: no FMA contraction, bit-exact with the CPU oracle's
-// fl(fl(x0*s) + x1*s)... rank order.
+// the same tiles, so CTA b only waits for CTA b of the peers. Each CTA index
+// counts its barriers (state counters, persisted across launches; identical
+// on every rank because every rank runs the same launches); a barrier
+// publishes the count to the peers' flag [b][me] (st.release.sys over
+// NVLink) and waits until every peer's flag [b][q] reached it. Every
+// collective launch starts with an entry barrier, so no rank overwrites a
+// peer's merge arena while that peer may still read it from an earlier
+// launch. Reductions use __fadd_rn / __fmul_rn / __fsub_rn only: no FMA
+// contraction, bit-exact with the CPU oracle's fl(fl(x0*s) + x1*s)... in
+// rank order.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -38,7 +43,14 @@ namespace mgw {
 
 namespace {
 
-constexpr uint64_t kBarrierTimeoutNs = 10ull * 1000 * 1000 * 1000;  // 10 s
+constexpr uint64_t kTimeoutNs = 10ull * 1000 * 1000 * 1000;  // 10 s: error, never a hang
+constexpr uint32_t kOneShotChunk = 4;  // tiles per barrier in one-shot (64 KiB per CTA)
+
+// super-tiles (P tiles each) per barrier pair in two-shot
+template <int P>
+struct TwoShotChunk {
+  static constexpr uint32_t value = P >= 4 ? 1 : 2;
+};
 
 __device__ __forceinline__ float4 load_tail(const float* p, uint32_t n) {
   float4 v;
@@ -95,26 +107,24 @@ __device__ __forceinline__ void epilogue(const Tile& t, uint32_t e, float4 g, fl
   }
 }
 
-// Barrier of CTA index `cta` with the same CTA index of every rank, on
-// barrier plane `plane`: signal every peer (st.release.sys over NVLink),
-// then wait for every peer's signal (ld.acquire.sys), bounded by a timeout
-// that records an error instead of hanging the GPU.
-__device__ __forceinline__ void rank_barrier(const RankView& v, int P, int plane, uint32_t epoch,
-                                             uint32_t cta, bool after_remote_stores = true) {
+// Barrier of CTA index `cta` with the same CTA index of every rank.
+// `count` is this CTA's barrier counter (same value in every thread).
+__device__ __forceinline__ void cta_barrier(const RankView& v, int P, uint32_t cta, uint32_t& count,
+                                            bool after_remote_stores) {
+  ++count;
   // Every warp's posted NVLink stores must be visible system-wide before
   // this CTA's flag is: each warp fences its own stores, then bar.sync.
   if (after_remote_stores) __threadfence_system();
   __syncthreads();
   if (threadIdx.x < P) {
     const int q = threadIdx.x;
-    const uint32_t slot = plane * kSignalPlane + cta * kMaxRanks;
-    st_release_sys(v.signal[q] + slot + v.rank, epoch);
-    const uint32_t* mine = v.signal[v.rank] + slot + q;
-    if (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
+    st_release_sys(v.signal[q] + cta * kMaxRanks + v.rank, count);
+    const uint32_t* mine = v.signal[v.rank] + cta * kMaxRanks + q;
+    if (static_cast<int32_t>(ld_acquire_sys(mine) - count) < 0) {
       const uint64_t t0 = globaltimer_ns();
-      while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
-        if (globaltimer_ns() - t0 > kBarrierTimeoutNs) {
-          atomicExch(v.state + 2, 1u);
+      while (static_cast<int32_t>(ld_acquire_sys(mine) - count) < 0) {
+        if (globaltimer_ns() - t0 > kTimeoutNs) {
+          atomicExch(v.state + kStateError, 1u);
           break;
         }
       }
@@ -123,19 +133,15 @@ __device__ __forceinline__ void rank_barrier(const RankView& v, int P, int plane
   __syncthreads();
 }
 
-// The last CTA of this rank to leave advances the launch counter by `used`
-// epochs (the epoch source of the next launch).
-__device__ __forceinline__ void finish_launch(const RankView& v, uint32_t seq, uint32_t used) {
+__device__ __forceinline__ uint32_t load_cta_count(const RankView& v, uint32_t cta) {
+  __shared__ uint32_t s_count;
+  if (threadIdx.x == 0) s_count = ld_volatile_u32(v.state + kStateCtaBase + cta);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t prev = atomicAdd(v.state + 1, 1u);
-    if (prev == gridDim.x - 1) {
-      atomicExch(v.state + 1, 0u);
-      __threadfence();
-      atomicExch(v.state, seq + used);
-    }
-  }
+  return s_count;
+}
+
+__device__ __forceinline__ void store_cta_count(const RankView& v, uint32_t cta, uint32_t count) {
+  if (threadIdx.x == 0) v.state[kStateCtaBase + cta] = count;
 }
 
 // ---- push data path -------------------------------------------------------
@@ -156,19 +162,20 @@ __device__ __forceinline__ void scatter_tile(const RankView& v, const Tile& t, i
   float4 x[kVecPerThread];
 #pragma unroll
   for (uint32_t k = 0; k < kVecPerThread; ++k) {
-    const uint32_t e = (threadIdx.x + k * kThreads) * 4;
-    if (e < nvec * 4) {
+    const uint32_t i = threadIdx.x + k * kThreads;
+    if (i < nvec) {
+      const uint32_t e = i * 4;
       x[k] = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
       x[k] = mul4(x[k], scale);
     }
   }
 #pragma unroll
   for (uint32_t k = 0; k < kVecPerThread; ++k) {
-    const uint32_t e = (threadIdx.x + k * kThreads) * 4;
-    if (e < nvec * 4) {
+    const uint32_t i = threadIdx.x + k * kThreads;
+    if (i < nvec) {
 #pragma unroll
       for (int q = 0; q < P; ++q) {
-        if (q >= q_begin && q < q_end) st_v4(v.arena[q] + my_slot + t.moff + e, x[k]);
+        if (q >= q_begin && q < q_end) st_v4(v.arena[q] + my_slot + t.moff + i * 4, x[k]);
       }
     }
   }
@@ -205,109 +212,133 @@ __device__ __forceinline__ void reduce_slots(const RankView& v, const Tile& t, u
   }
 }
 
-// One-shot: scatter my tiles to every rank, barrier, reduce the P slots of
-// my tiles locally, unpack + SGD. NVLink: (P-1) * S posted writes per rank.
+template <int P>
+__device__ __forceinline__ void reduce_apply(const RankView& v, const Tile& t, uint64_t slot_stride,
+                                             float lr, int epi) {
+  float4 acc[kVecPerThread];
+  reduce_slots<P>(v, t, slot_stride, acc);
+  const uint32_t layer = t.layer & kLayerMask;
+  float* w = v.weights[layer];
+  float* g = v.grads[layer];
+  const uint32_t nvec = (t.len + 3) >> 2;
+#pragma unroll
+  for (uint32_t k = 0; k < kVecPerThread; ++k) {
+    const uint32_t i = threadIdx.x + k * kThreads;
+    if (i < nvec) epilogue(t, i * 4, acc[k], w, g, lr, epi);
+  }
+}
+
+// One-shot: this CTA's tiles (cta, cta + ncta, ...) in chunks of
+// kOneShotChunk: push the chunk to every rank, barrier, reduce the chunk's P
+// local slots, unpack + SGD. NVLink: (P-1) * S posted writes per rank.
 template <int P>
 __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* tiles,
-                                               uint32_t n_tiles, uint32_t epoch, uint64_t slot_stride,
-                                               float scale, float lr, int epi, uint32_t cta,
-                                               uint32_t ncta) {
+                                               uint32_t n_tiles, uint64_t slot_stride, float scale,
+                                               float lr, int epi, uint32_t cta, uint32_t ncta,
+                                               uint32_t& count) {
   const uint64_t my_slot = static_cast<uint64_t>(v.rank) * slot_stride;
-  for (uint32_t ti = cta; ti < n_tiles; ti += ncta) scatter_tile<P>(v, tiles[ti], 0, P, my_slot, scale);
-  rank_barrier(v, P, 0, epoch, cta);
-  for (uint32_t ti = cta; ti < n_tiles; ti += ncta) {
-    const Tile t = tiles[ti];
-    float4 acc[kVecPerThread];
-    reduce_slots<P>(v, t, slot_stride, acc);
-    const uint32_t layer = t.layer & kLayerMask;
-    float* w = v.weights[layer];
-    float* g = v.grads[layer];
-    const uint32_t nvec = (t.len + 3) >> 2;
-#pragma unroll
-    for (uint32_t k = 0; k < kVecPerThread; ++k) {
-      const uint32_t i = threadIdx.x + k * kThreads;
-      if (i < nvec) epilogue(t, i * 4, acc[k], w, g, lr, epi);
+  for (uint32_t base = cta; base < n_tiles; base += kOneShotChunk * ncta) {
+#pragma unroll 1
+    for (uint32_t j = 0; j < kOneShotChunk; ++j) {
+      const uint32_t ti = base + j * ncta;
+      if (ti < n_tiles) scatter_tile<P>(v, tiles[ti], 0, P, my_slot, scale);
+    }
+    cta_barrier(v, P, cta, count, true);
+#pragma unroll 1
+    for (uint32_t j = 0; j < kOneShotChunk; ++j) {
+      const uint32_t ti = base + j * ncta;
+      if (ti < n_tiles) reduce_apply<P>(v, tiles[ti], slot_stride, lr, epi);
     }
   }
 }
 
-// Two-shot: tile t of super-tile s = tiles [s*P, s*P+P) is owned by rank
-// t % P. Reduce-scatter: scatter each tile to its owner's slot `me`;
-// owners reduce their tiles locally in rank order, apply SGD, and push the
-// reduced tile into slot `owner` of every peer (all-gather); barrier; every
-// rank applies the other owners' reduced tiles from its local slots.
-// NVLink: 2 (P-1)/P * S posted writes per rank.
+// Two-shot: super-tile s = tiles [s*P, s*P+P), tile s*P+q owned by rank q.
+// Per chunk of this CTA's super-tiles: push each tile to its owner's slot
+// `me` (reduce-scatter), barrier; owners reduce their tile locally in rank
+// order, apply SGD and push the result into slot `owner` of every peer
+// (all-gather), barrier; every rank applies the other owners' results from
+// its local slots. NVLink: 2 (P-1)/P * S posted writes per rank.
 template <int P>
 __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* tiles,
-                                               uint32_t n_tiles, uint32_t epoch, uint64_t slot_stride,
-                                               float scale, float lr, int epi, uint32_t cta,
-                                               uint32_t ncta) {
+                                               uint32_t n_tiles, uint64_t slot_stride, float scale,
+                                               float lr, int epi, uint32_t cta, uint32_t ncta,
+                                               uint32_t& count) {
+  constexpr uint32_t C = TwoShotChunk<P>::value;
   const uint64_t my_slot = static_cast<uint64_t>(v.rank) * slot_stride;
   const uint32_t n_super = (n_tiles + P - 1) / P;
-  for (uint32_t s = cta; s < n_super; s += ncta) {
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-      const uint32_t ti = s * P + q;
-      if (ti < n_tiles) scatter_tile<P>(v, tiles[ti], q, q + 1, my_slot, scale);
-    }
-  }
-  rank_barrier(v, P, 0, epoch, cta);
-  for (uint32_t s = cta; s < n_super; s += ncta) {
-    const uint32_t ti = s * P + v.rank;
-    if (ti >= n_tiles) continue;
-    const Tile t = tiles[ti];
-    float4 acc[kVecPerThread];
-    reduce_slots<P>(v, t, slot_stride, acc);
-    const uint32_t layer = t.layer & kLayerMask;
-    float* w = v.weights[layer];
-    float* g = v.grads[layer];
-    const uint32_t nvec = (t.len + 3) >> 2;
-#pragma unroll
-    for (uint32_t k = 0; k < kVecPerThread; ++k) {
-      const uint32_t i = threadIdx.x + k * kThreads;
-      if (i < nvec) {
-#pragma unroll
-        for (int q = 0; q < P; ++q) {
-          if (q != v.rank) st_v4(v.arena[q] + my_slot + t.moff + i * 4, acc[k]);
-        }
-        epilogue(t, i * 4, acc[k], w, g, lr, epi);
+  for (uint32_t base = cta; base < n_super; base += C * ncta) {
+#pragma unroll 1
+    for (uint32_t j = 0; j < C; ++j) {
+      const uint32_t s = base + j * ncta;
+      if (s >= n_super) break;
+#pragma unroll 1
+      for (int q = 0; q < P; ++q) {
+        const uint32_t ti = s * P + q;
+        if (ti < n_tiles) scatter_tile<P>(v, tiles[ti], q, q + 1, my_slot, scale);
       }
     }
-  }
-  rank_barrier(v, P, 1, epoch, cta);
-  for (uint32_t s = cta; s < n_super; s += ncta) {
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-      const uint32_t ti = s * P + q;
-      if (q == v.rank || ti >= n_tiles) continue;
+    cta_barrier(v, P, cta, count, true);
+#pragma unroll 1
+    for (uint32_t j = 0; j < C; ++j) {
+      const uint32_t s = base + j * ncta;
+      const uint32_t ti = s * P + v.rank;
+      if (s >= n_super || ti >= n_tiles) continue;
       const Tile t = tiles[ti];
-      const float* red = v.arena[v.rank] + static_cast<uint64_t>(q) * slot_stride + t.moff;
+      float4 acc[kVecPerThread];
+      reduce_slots<P>(v, t, slot_stride, acc);
       const uint32_t layer = t.layer & kLayerMask;
       float* w = v.weights[layer];
       float* g = v.grads[layer];
       const uint32_t nvec = (t.len + 3) >> 2;
-      float4 x[kVecPerThread];
 #pragma unroll
       for (uint32_t k = 0; k < kVecPerThread; ++k) {
         const uint32_t i = threadIdx.x + k * kThreads;
-        if (i < nvec) x[k] = ld_cg_v4(red + i * 4);
+        if (i < nvec) {
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            if (q != v.rank) st_v4(v.arena[q] + my_slot + t.moff + i * 4, acc[k]);
+          }
+          epilogue(t, i * 4, acc[k], w, g, lr, epi);
+        }
       }
+    }
+    cta_barrier(v, P, cta, count, true);
+#pragma unroll 1
+    for (uint32_t j = 0; j < C; ++j) {
+      const uint32_t s = base + j * ncta;
+      if (s >= n_super) break;
+#pragma unroll 1
+      for (int q = 0; q < P; ++q) {
+        const uint32_t ti = s * P + q;
+        if (q == v.rank || ti >= n_tiles) continue;
+        const Tile t = tiles[ti];
+        const float* red = v.arena[v.rank] + static_cast<uint64_t>(q) * slot_stride + t.moff;
+        const uint32_t layer = t.layer & kLayerMask;
+        float* w = v.weights[layer];
+        float* g = v.grads[layer];
+        const uint32_t nvec = (t.len + 3) >> 2;
+        float4 x[kVecPerThread];
 #pragma unroll
-      for (uint32_t k = 0; k < kVecPerThread; ++k) {
-        const uint32_t i = threadIdx.x + k * kThreads;
-        if (i < nvec) epilogue(t, i * 4, x[k], w, g, lr, epi);
+        for (uint32_t k = 0; k < kVecPerThread; ++k) {
+          const uint32_t i = threadIdx.x + k * kThreads;
+          if (i < nvec) x[k] = ld_cg_v4(red + i * 4);
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kVecPerThread; ++k) {
+          const uint32_t i = threadIdx.x + k * kThreads;
+          if (i < nvec) epilogue(t, i * 4, x[k], w, g, lr, epi);
+        }
       }
     }
   }
 }
 
-// One merge group, executed by CTA `cta` of `ncta`. `epoch` numbers this
-// group's barriers; `copy_off` selects the merge-arena copy.
+// One merge group, executed by CTA `cta` of `ncta`.
 template <int P>
 __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, const Tile* tiles,
-                                          uint32_t n_tiles, uint32_t epoch, uint64_t slot_stride,
-                                          float scale, float lr, int epi, uint32_t cta,
-                                          uint32_t ncta) {
+                                          uint32_t n_tiles, uint64_t slot_stride, float scale,
+                                          float lr, int epi, uint32_t cta, uint32_t ncta,
+                                          uint32_t& count) {
   if constexpr (P == 1) {
     // Single rank: no exchange. grad x 1/P (= 1) straight into the epilogue.
     for (uint32_t ti = cta; ti < n_tiles; ti += ncta) {
@@ -324,47 +355,42 @@ __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, cons
         epilogue(t, e, mul4(x, scale), w, g, lr, epi);
       }
     }
+  } else if (two_shot) {
+    two_shot_group<P>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, count);
   } else {
-    if (two_shot) {
-      two_shot_group<P>(v, tiles, n_tiles, epoch, slot_stride, scale, lr, epi, cta, ncta);
-    } else {
-      one_shot_group<P>(v, tiles, n_tiles, epoch, slot_stride, scale, lr, epi, cta, ncta);
-    }
+    one_shot_group<P>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, count);
   }
 }
 
 template <int P, bool TWO_SHOT, bool LOOPBACK>
-__global__ void __launch_bounds__(kThreads, 1) group_allreduce_kernel(const __grid_constant__ GroupLaunch L) {
+__global__ void __launch_bounds__(kThreads, 1)
+    group_allreduce_kernel(const __grid_constant__ GroupLaunch L) {
   const RankView& v = L.views[LOOPBACK ? blockIdx.y : 0];
-  if constexpr (P == 1) {
-    run_group<1>(false, v, L.tiles, L.n_tiles, 0, 0, L.scale, L.lr, L.epilogue, blockIdx.x,
-                 gridDim.x);
-  } else {
-    __shared__ uint32_t s_seq;
-    if (threadIdx.x == 0) s_seq = ld_volatile_u32(v.state);
-    __syncthreads();
-    const uint32_t seq = s_seq;
-    rank_barrier(v, P, 1, seq + 1, blockIdx.x, false);  // entry: peers have left every older launch
-    run_group<P>(TWO_SHOT, v, L.tiles, L.n_tiles, seq + 2, L.slot_stride, L.scale, L.lr,
-                 L.epilogue, blockIdx.x, gridDim.x);
-    finish_launch(v, seq, 2);
+  uint32_t count = 0;
+  if constexpr (P > 1) {
+    count = load_cta_count(v, blockIdx.x);
+    cta_barrier(v, P, blockIdx.x, count, false);  // entry: peers have left every older launch
   }
+  run_group<P>(TWO_SHOT, v, L.tiles, L.n_tiles, L.slot_stride, L.scale, L.lr, L.epilogue,
+               blockIdx.x, gridDim.x, count);
+  if constexpr (P > 1) store_cta_count(v, blockIdx.x, count);
 }
 
 template <int P>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineLaunch E) {
   const RankView& v = E.v;
-  __shared__ uint32_t s_seq, s_iter;
-  if (threadIdx.x == 0) {
-    s_seq = P > 1 ? ld_volatile_u32(v.state) : 0u;
-    s_iter = ld_volatile_u32(E.pipe + 1);
+  __shared__ uint32_t s_iter;
+  if (threadIdx.x == 0) s_iter = ld_volatile_u32(E.pipe + 1);
+  uint32_t count = 0;
+  if constexpr (P > 1) {
+    count = load_cta_count(v, blockIdx.x);
+    // Entry barrier (runs while the compute stream replays the forward
+    // pass): every peer has finished every older launch before any push.
+    cta_barrier(v, P, blockIdx.x, count, false);
+  } else {
+    __syncthreads();
   }
-  __syncthreads();
-  const uint32_t seq = s_seq;
   const uint32_t iter = s_iter;
-  // Entry barrier (runs while the compute stream replays the forward pass):
-  // every peer has finished every older launch before anything is packed.
-  if constexpr (P > 1) rank_barrier(v, P, 1, seq + 1, blockIdx.x, false);
   for (uint32_t k = 0; k < E.G; ++k) {
     const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
     const EngineGroup grp = E.groups[gi];
@@ -376,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       if (static_cast<int32_t>(ld_acquire_gpu(E.pipe) - target) < 0) {
         const uint64_t t0 = globaltimer_ns();
         while (static_cast<int32_t>(ld_acquire_gpu(E.pipe) - target) < 0) {
-          if (globaltimer_ns() - t0 > kBarrierTimeoutNs) {  // compute side never signalled
+          if (globaltimer_ns() - t0 > kTimeoutNs) {  // compute side never signalled
             atomicExch(E.pipe + 3, 1u);
             break;
           }
@@ -385,8 +411,8 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       if (E.stamps != nullptr && blockIdx.x == 0) E.stamps[2 * gi] = globaltimer_ns();
     }
     __syncthreads();
-    run_group<P>(two, v, E.tiles + grp.tile_first, grp.n_tiles, seq + 2 + k, E.slot_stride,
-                 E.scale, E.lr, E.epilogue, blockIdx.x, gridDim.x);
+    run_group<P>(two, v, E.tiles + grp.tile_first, grp.n_tiles, E.slot_stride, E.scale, E.lr,
+                 E.epilogue, blockIdx.x, gridDim.x, count);
     if (E.stamps != nullptr) {
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -399,6 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       }
     }
   }
+  if constexpr (P > 1) store_cta_count(v, blockIdx.x, count);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -406,7 +433,6 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       atomicExch(E.pipe + 2, 0u);
       __threadfence();
       atomicExch(E.pipe + 1, iter + 1);
-      if (P > 1) atomicExch(v.state, seq + 1 + E.G);
     }
   }
 }
@@ -458,9 +484,10 @@ __global__ void replay_all_kernel(unsigned long long* clock, const unsigned long
   clock[1] = now;
 }
 
-// clock[0]: iteration start (written by the first replay kernel of an
-// iteration), clock[1]: completion time of the latest replay kernel. When
-// `ready` is given, the group is marked ready for the comm engine.
+// One group head of the replay (per-group-launch pipelines). clock[0]:
+// iteration start (written by the first replay kernel of an iteration),
+// clock[1]: completion time of the latest replay kernel. When `ready` is
+// given, the group is marked ready for the comm engine.
 __global__ void replay_kernel(unsigned long long* clock, unsigned long long deadline_ns, int first,
                               uint32_t* ready) {
   if (threadIdx.x != 0) return;
@@ -478,6 +505,18 @@ __global__ void replay_kernel(unsigned long long* clock, unsigned long long dead
   if (ready != nullptr) {
     __threadfence();
     atomicAdd(ready, 1u);
+  }
+}
+
+// L2 eviction between iterations: streaming stores over a buffer larger
+// than L2 from a FEW CTAs, so the flush never occupies every SM (a full-grid
+// memset delayed the concurrently launched one-thread replay kernel by the
+// whole flush, measured ~40 us per iteration).
+__global__ void __launch_bounds__(512) l2_flush_kernel(float4* buf, size_t n_vec, uint32_t salt) {
+  const float4 v = make_float4(__uint_as_float(salt), 0.0f, 0.0f, 0.0f);
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n_vec;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    __stcs(buf + i, v);
   }
 }
 
@@ -573,18 +612,6 @@ cudaError_t launch_replay(unsigned long long* clock, unsigned long long deadline
                           uint32_t* ready, cudaStream_t stream) {
   replay_kernel<<<1, 32, 0, stream>>>(clock, deadline_ns, first, ready);
   return cudaGetLastError();
-}
-
-// L2 eviction between iterations: streaming stores over a buffer larger
-// than L2 from a FEW CTAs, so the flush never occupies every SM (a full-grid
-// memset delayed the concurrently launched one-thread replay kernel by the
-// whole flush, measured ~40 us per iteration).
-__global__ void __launch_bounds__(512) l2_flush_kernel(float4* buf, size_t n_vec, uint32_t salt) {
-  const float4 v = make_float4(__uint_as_float(salt), 0.0f, 0.0f, 0.0f);
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n_vec;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    __stcs(buf + i, v);
-  }
 }
 
 cudaError_t launch_l2_flush(void* buf, size_t bytes, int ctas, cudaStream_t stream) {

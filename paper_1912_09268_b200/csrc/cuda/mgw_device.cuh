@@ -10,11 +10,12 @@
 //                 pre-allocated merge buffers laid out
 //                 once for all groups. Reuse across launches is made safe by
 //                 an entry barrier, not by double buffering.
-//   signal area   two barrier planes x kMaxCtas x kMaxRanks uint32 flags,
-//                 written by peers over NVLink (st.release.sys) and spun on
-//                 locally (ld.acquire.sys).
-//   state         [0] launch counter (epoch source), [1] CTA done counter,
-//                 [2] barrier-timeout error flag.
+//   signal area   kMaxCtas x kMaxRanks uint32 flags: flag [b][q] holds the
+//                 barrier count CTA b of rank q last published (written by
+//                 q over NVLink with st.release.sys, spun on locally with
+//                 ld.acquire.sys).
+//   state         [2] barrier-timeout error flag, [64 + b] barrier count of
+//                 CTA index b (identical on every rank).
 // Work unit: a Tile = up to kTileElems consecutive elements of ONE layer,
 // so pack/unpack read and write contiguous 16-byte vectors.
 #ifndef MGWFBP_DEVICE_CUH_
@@ -32,9 +33,12 @@ constexpr uint32_t kVecPerThread = kTileElems / 4 / kThreads;
 constexpr uint32_t kLayerMask = 0x3fffffffu;
 constexpr uint32_t kGradUnaligned = 0x80000000u;
 constexpr uint32_t kWeightUnaligned = 0x40000000u;
-constexpr int kSignalPlane = kMaxCtas * kMaxRanks;  // uint32 per barrier plane
-constexpr int kSignalWords = 2 * kSignalPlane;
-constexpr int kStateWords = 4;
+constexpr int kSignalWords = kMaxCtas * kMaxRanks;  // flag [cta][src rank]
+// state words: [kStateError] barrier-timeout flag, [kStateCtaBase + b] the
+// barrier count of CTA index b (persists across launches)
+constexpr int kStateError = 2;
+constexpr int kStateCtaBase = 64;
+constexpr int kStateWords = kStateCtaBase + kMaxCtas;
 
 struct Tile {
   uint32_t layer;  // layer index | alignment flags
