@@ -44,12 +44,17 @@ namespace mgw {
 namespace {
 
 constexpr uint64_t kTimeoutNs = 10ull * 1000 * 1000 * 1000;  // 10 s: error, never a hang
-constexpr uint32_t kOneShotChunk = 4;  // tiles per barrier in one-shot (64 KiB per CTA)
+// Tiles per barrier in one-shot, super-tiles per barrier pair in two-shot.
+// Measured on 2x B200 (tools/probe_bw.py, 256 MiB): chunks of 4 tiles cut
+// one-shot from 400 to 296 GB/s and two-shot from 478 to 221 GB/s — each
+// extra barrier costs a system-scope fence on the posted NVLink stores plus
+// a flag round trip (~5-10 us), more than the phase overlap it buys. So a
+// CTA pushes ALL its tiles of a group, then does one barrier (per phase).
+constexpr uint32_t kOneShotChunk = 1u << 20;
 
-// super-tiles (P tiles each) per barrier pair in two-shot
 template <int P>
 struct TwoShotChunk {
-  static constexpr uint32_t value = P >= 4 ? 1 : 2;
+  static constexpr uint32_t value = 1u << 20;
 };
 
 __device__ __forceinline__ float4 load_tail(const float* p, uint32_t n) {
@@ -241,13 +246,15 @@ __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* ti
 #pragma unroll 1
     for (uint32_t j = 0; j < kOneShotChunk; ++j) {
       const uint32_t ti = base + j * ncta;
-      if (ti < n_tiles) scatter_tile<P>(v, tiles[ti], 0, P, my_slot, scale);
+      if (ti >= n_tiles) break;
+      scatter_tile<P>(v, tiles[ti], 0, P, my_slot, scale);
     }
     cta_barrier(v, P, cta, count, true);
 #pragma unroll 1
     for (uint32_t j = 0; j < kOneShotChunk; ++j) {
       const uint32_t ti = base + j * ncta;
-      if (ti < n_tiles) reduce_apply<P>(v, tiles[ti], slot_stride, lr, epi);
+      if (ti >= n_tiles) break;
+      reduce_apply<P>(v, tiles[ti], slot_stride, lr, epi);
     }
   }
 }
@@ -282,7 +289,8 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
     for (uint32_t j = 0; j < C; ++j) {
       const uint32_t s = base + j * ncta;
       const uint32_t ti = s * P + v.rank;
-      if (s >= n_super || ti >= n_tiles) continue;
+      if (s >= n_super) break;
+      if (ti >= n_tiles) continue;
       const Tile t = tiles[ti];
       float4 acc[kVecPerThread];
       reduce_slots<P>(v, t, slot_stride, acc);
