@@ -382,11 +382,24 @@ def main():
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
-    roof.update({"kernel": "group_allreduce_kernel (fused pack+allreduce+unpack/SGD)",
+    # asymptotic per-byte rate of the same fused kernel from the calibration
+    # slope b (s/B): bytes that cross the bound per gradient byte / b
+    per_byte = 3.0 if N == 1 else 2 * (N - 1) / N
+    asym = per_byte / model.b / 1e9 if model.b > 0 else None
+    roof.update({"kernel": ("engine_kernel/run_group (fused pack + push all-reduce + unpack/SGD), "
+                            "per-group %globaltimer stamps" if args.engine_ctas
+                            else "group_allreduce_kernel (fused pack + push all-reduce + unpack/SGD)"),
                  "achieved": achieved, "peak": peak, "unit": "GB/s",
                  "frac": achieved / peak if achieved else None, "traffic": traffic,
+                 "traffic_evidence": "profiles/r1_ncu_group_kernel_p1_16MiB.txt (ncu --set full of run_group "
+                                     "at P=1, 16 MiB: DRAM 33.6 MB read / 0 written vs 50.3 MB algorithmic; "
+                                     "the engine kernel itself cannot run under ncu's serialisation)",
                  "algorithmic_bytes_per_iter": algo_bytes, "kernel_ms_per_iter": kern_s * 1e3,
-                 "launches_per_iter": len(group_ms)})
+                 "launches_per_iter": len(group_ms),
+                 "note": "groups are latency-bound at these sizes (GoogLeNet: 6.6M params over "
+                         f"{len(group_ms)} groups); the per-byte rate is the slope row",
+                 "slope": {"achieved": asym, "frac": asym / peak if asym else None,
+                           "from": "calibration b (fit_model over the on-box sweep)"}})
 
     # merged all-reduce bus GB/s = 2(P-1)/P * S / t: ours (fused kernel, from
     # the calibration sweep) next to NCCL (torch.distributed.all_reduce, same
