@@ -9,8 +9,8 @@
 //        two-shot: tile t is owned by rank t % P; ranks push each tile to its
 //          owner (reduce-scatter), owners reduce + push the result to every
 //          peer (all-gather) fused with SGD; 2 barriers per chunk.
-//      A CTA walks its tiles in CHUNKS (push -> barrier -> reduce per chunk),
-//      so different CTAs overlap NVLink transfer with local HBM work.
+//      A CTA walks its tiles in 256 KiB CHUNKS, software-pipelined: chunk
+//      c+1's posted NVLink stores are issued before chunk c's local work.
 //  engine_kernel<P> — the persistent comm engine: one launch per iteration
 //      runs every group in backward order as soon as the compute side marks
 //      its head ready (paper Algorithm 2's daemon thread, on the GPU; no
@@ -44,17 +44,18 @@ namespace mgw {
 namespace {
 
 constexpr uint64_t kTimeoutNs = 10ull * 1000 * 1000 * 1000;  // 10 s: error, never a hang
-// Tiles per barrier in one-shot, super-tiles per barrier pair in two-shot.
-// Measured on 2x B200 (tools/probe_bw.py, 256 MiB): chunks of 4 tiles cut
-// one-shot from 400 to 296 GB/s and two-shot from 478 to 221 GB/s — each
-// extra barrier costs a system-scope fence on the posted NVLink stores plus
-// a flag round trip (~5-10 us), more than the phase overlap it buys. So a
-// CTA pushes ALL its tiles of a group, then does one barrier (per phase).
-constexpr uint32_t kOneShotChunk = 1u << 20;
+// Software pipelining of the push data path. A CTA walks its tiles in
+// CHUNKS and issues chunk c+1's posted NVLink stores BEFORE chunk c's local
+// HBM work, so the stores drain while the CTA reduces / applies SGD; one
+// barrier per chunk. (Measured on 2x B200, 256 MiB: a non-overlapped
+// barrier per 4-tile chunk cost more than it bought — 296 / 221 GB/s vs
+// 400 / 478 unchunked; the overlap below is what chunks are for, and a
+// chunk is 256 KiB per CTA so barriers stay rare.)
+constexpr uint32_t kOneShotChunk = 16;  // tiles of this CTA per chunk (256 KiB)
 
 template <int P>
-struct TwoShotChunk {
-  static constexpr uint32_t value = 1u << 20;
+struct TwoShotChunk {  // super-tiles (P tiles each) of this CTA per chunk: 256 KiB
+  static constexpr uint32_t value = 16 / P;
 };
 
 __device__ __forceinline__ float4 load_tail(const float* p, uint32_t n) {
@@ -233,38 +234,45 @@ __device__ __forceinline__ void reduce_apply(const RankView& v, const Tile& t, u
   }
 }
 
-// One-shot: this CTA's tiles (cta, cta + ncta, ...) in chunks of
-// kOneShotChunk: push the chunk to every rank, barrier, reduce the chunk's P
-// local slots, unpack + SGD. NVLink: (P-1) * S posted writes per rank.
+// One-shot, pipelined over chunks of this CTA's tiles (cta + j*ncta):
+//   push(0); barrier; for c: push(c+1); reduce+SGD(c); barrier (if c+1<n)
+// push = gather x 1/P into slot `me` of every rank; reduce = rank-order sum
+// of the P local slots. NVLink: (P-1) * S posted writes per rank.
 template <int P>
 __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* tiles,
                                                uint32_t n_tiles, uint64_t slot_stride, float scale,
                                                float lr, int epi, uint32_t cta, uint32_t ncta,
                                                uint32_t& count) {
   const uint64_t my_slot = static_cast<uint64_t>(v.rank) * slot_stride;
-  for (uint32_t base = cta; base < n_tiles; base += kOneShotChunk * ncta) {
+  const uint32_t mine = cta < n_tiles ? (n_tiles - cta + ncta - 1) / ncta : 0;  // my tiles
+  const uint32_t n_chunks = (mine + kOneShotChunk - 1) / kOneShotChunk;
+  auto push = [&](uint32_t c) {
 #pragma unroll 1
-    for (uint32_t j = 0; j < kOneShotChunk; ++j) {
-      const uint32_t ti = base + j * ncta;
-      if (ti >= n_tiles) break;
-      scatter_tile<P>(v, tiles[ti], 0, P, my_slot, scale);
+    for (uint32_t j = c * kOneShotChunk; j < mine && j < (c + 1) * kOneShotChunk; ++j) {
+      scatter_tile<P>(v, tiles[cta + j * ncta], 0, P, my_slot, scale);
     }
-    cta_barrier(v, P, cta, count, true);
+  };
+  // step t: push(t) [t < n], reduce+SGD(t-1) [t >= 1], barrier [t < n]
 #pragma unroll 1
-    for (uint32_t j = 0; j < kOneShotChunk; ++j) {
-      const uint32_t ti = base + j * ncta;
-      if (ti >= n_tiles) break;
-      reduce_apply<P>(v, tiles[ti], slot_stride, lr, epi);
+  for (uint32_t t = 0; t <= n_chunks && n_chunks > 0; ++t) {
+    if (t < n_chunks) push(t);
+    if (t >= 1) {
+#pragma unroll 1
+      for (uint32_t j = (t - 1) * kOneShotChunk; j < mine && j < t * kOneShotChunk; ++j) {
+        reduce_apply<P>(v, tiles[cta + j * ncta], slot_stride, lr, epi);
+      }
     }
+    if (t < n_chunks) cta_barrier(v, P, cta, count, true);
   }
 }
 
 // Two-shot: super-tile s = tiles [s*P, s*P+P), tile s*P+q owned by rank q.
-// Per chunk of this CTA's super-tiles: push each tile to its owner's slot
-// `me` (reduce-scatter), barrier; owners reduce their tile locally in rank
-// order, apply SGD and push the result into slot `owner` of every peer
-// (all-gather), barrier; every rank applies the other owners' results from
-// its local slots. NVLink: 2 (P-1)/P * S posted writes per rank.
+//   RS(c):  push each tile of chunk c to its owner's slot `me`
+//   RA(c):  owner: rank-order sum of its tile's P local slots, SGD, push the
+//           result into slot `owner` of every peer (all-gather)
+//   AP(c):  apply the other owners' results from the local slots (SGD)
+// Pipelined: RS(0); bar; RA(0); RS(1); bar; for c: RA(c+1); RS(c+2); AP(c);
+// bar (if c+1<n). NVLink: 2 (P-1)/P * S posted writes per rank.
 template <int P>
 __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* tiles,
                                                uint32_t n_tiles, uint64_t slot_stride, float scale,
@@ -273,23 +281,23 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
   constexpr uint32_t C = TwoShotChunk<P>::value;
   const uint64_t my_slot = static_cast<uint64_t>(v.rank) * slot_stride;
   const uint32_t n_super = (n_tiles + P - 1) / P;
-  for (uint32_t base = cta; base < n_super; base += C * ncta) {
+  const uint32_t mine = cta < n_super ? (n_super - cta + ncta - 1) / ncta : 0;  // my super-tiles
+  const uint32_t n_chunks = (mine + C - 1) / C;
+  auto rs = [&](uint32_t c) {
 #pragma unroll 1
-    for (uint32_t j = 0; j < C; ++j) {
-      const uint32_t s = base + j * ncta;
-      if (s >= n_super) break;
+    for (uint32_t j = c * C; j < mine && j < (c + 1) * C; ++j) {
+      const uint32_t s = cta + j * ncta;
 #pragma unroll 1
       for (int q = 0; q < P; ++q) {
         const uint32_t ti = s * P + q;
         if (ti < n_tiles) scatter_tile<P>(v, tiles[ti], q, q + 1, my_slot, scale);
       }
     }
-    cta_barrier(v, P, cta, count, true);
+  };
+  auto ra = [&](uint32_t c) {
 #pragma unroll 1
-    for (uint32_t j = 0; j < C; ++j) {
-      const uint32_t s = base + j * ncta;
-      const uint32_t ti = s * P + v.rank;
-      if (s >= n_super) break;
+    for (uint32_t j = c * C; j < mine && j < (c + 1) * C; ++j) {
+      const uint32_t ti = (cta + j * ncta) * P + v.rank;
       if (ti >= n_tiles) continue;
       const Tile t = tiles[ti];
       float4 acc[kVecPerThread];
@@ -310,11 +318,11 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
         }
       }
     }
-    cta_barrier(v, P, cta, count, true);
+  };
+  auto ap = [&](uint32_t c) {
 #pragma unroll 1
-    for (uint32_t j = 0; j < C; ++j) {
-      const uint32_t s = base + j * ncta;
-      if (s >= n_super) break;
+    for (uint32_t j = c * C; j < mine && j < (c + 1) * C; ++j) {
+      const uint32_t s = cta + j * ncta;
 #pragma unroll 1
       for (int q = 0; q < P; ++q) {
         const uint32_t ti = s * P + q;
@@ -338,6 +346,15 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
         }
       }
     }
+  };
+  // step t: RA(t-1) [1 <= t <= n], RS(t) [t < n], AP(t-2) [t >= 2],
+  // barrier [t <= n] (covers the posted stores of RS(t) and RA(t-1))
+#pragma unroll 1
+  for (uint32_t t = 0; t <= n_chunks + 1 && n_chunks > 0; ++t) {
+    if (t >= 1 && t <= n_chunks) ra(t - 1);
+    if (t < n_chunks) rs(t);
+    if (t >= 2) ap(t - 2);
+    if (t <= n_chunks) cta_barrier(v, P, cta, count, true);
   }
 }
 
