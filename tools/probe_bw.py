@@ -23,6 +23,14 @@ for algo in os.environ.get("ALGOS", "oneshot,twoshot").split(","):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         out.append((f"engine {algo} ctas={ctas}", [f * s / tt / 1e9 for s, tt in zip(sizes, t.tolist())],
                     [tt * 1e6 for tt in t.tolist()]))
+for algo in os.environ.get("STANDALONE", "twoshot").split(","):
+    if not algo:
+        continue
+    m = comm.calibrate(sizes, warmup=2, reps=5, algo=algo)
+    t = torch.tensor([x.time_sec for x in m], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    out.append((f"standalone {algo} (grid=occ*SMs)", [f * s / tt / 1e9 for s, tt in zip(sizes, t.tolist())],
+                [tt * 1e6 for tt in t.tolist()]))
 nccl = []
 for s in sizes:
     x = torch.ones(s // 4, device=dev)
