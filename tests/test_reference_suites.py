@@ -29,10 +29,10 @@ def _nlohmann():
     pytest.skip("nlohmann json not found")
 
 
-def _build(tmp_path, sources, name):
+def _build(tmp_path, sources, name, extra=()):
     lib_dir = os.path.join(ROOT, "paper_1912_09268_b200", "lib")
     exe = str(tmp_path / name)
-    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off",
+    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", *extra,
            "-I", os.path.join(ROOT, "tests", "cpp", "catch_shim"), "-I", os.path.join(ROOT, "include"),
            "-I", os.path.join(REFERENCE, "tests"), "-I", _nlohmann(),
            f'-DGRADSCHED_FIXTURE_DIR="{REFERENCE}/tests/fixtures"', f'-DGRADSCHED_DATA_DIR="{REFERENCE}/data"']
@@ -49,6 +49,18 @@ def test_reference_unit_suites_pass_against_our_headers(tmp_path):
     print(r.stdout[-3000:])
     assert r.returncode == 0, r.stdout[-3000:]
     assert "48 test cases" in r.stdout and "0 failed" in r.stdout
+
+
+def test_reference_cli_suite_passes_against_our_cli(tmp_path):
+    """The reference's test_cli.cpp (15 cases: outputs byte-equal to the
+    library exports, exit codes 0/2/3/4) driving OUR CLI binary."""
+    cli = os.path.join(ROOT, "paper_1912_09268_b200", "bin", "gradsched")
+    assert os.path.exists(cli), "build the CLI: make -C paper_1912_09268_b200/csrc"
+    exe = _build(tmp_path, ["test_cli.cpp"], "cli_tests", extra=[f'-DGRADSCHED_CLI_PATH="{cli}"'])
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert "15 test cases" in r.stdout and "0 failed" in r.stdout
 
 
 def test_reference_acceptance_suite_passes(tmp_path):

@@ -1,0 +1,89 @@
+// NVLink egress micro-probe (tools only): GPU 0 writes a 256 MiB buffer into
+// GPU 1 (peer access, one process) with
+//   (a) SM stores, 16-byte per thread (st.global.v4),
+//   (b) SM stores, 32-byte per thread (two v4 to adjacent addresses),
+//   (c) TMA bulk copies smem -> peer global (cp.async.bulk), 16 KiB chunks,
+// for several CTA counts, and cudaMemcpyPeerAsync as the copy-engine
+// reference. Prints GB/s.
+//
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/nvlink_probe tools/nvlink_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
+  std::printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); return 1; } } while (0)
+
+__global__ void st16(float4* dst, size_t n_vec, float v) {
+  const float4 x = make_float4(v, v, v, v);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_vec; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = x;
+}
+
+__global__ void st32(float4* dst, size_t n_vec, float v) {
+  const float4 x = make_float4(v, v, v, v);
+  for (size_t i = 2 * (blockIdx.x * (size_t)blockDim.x + threadIdx.x); i + 1 < n_vec;
+       i += 2 * (size_t)gridDim.x * blockDim.x) {
+    dst[i] = x;
+    dst[i + 1] = x;
+  }
+}
+
+// Each CTA: fill a 16 KiB smem chunk once, then bulk-copy it to successive
+// destination chunks, keeping up to 8 bulk groups in flight.
+__global__ void tma_bulk(char* dst, size_t bytes, float v) {
+  constexpr int kChunk = 16384;
+  __shared__ __align__(128) float buf[kChunk / 4];
+  for (int i = threadIdx.x; i < kChunk / 4; i += blockDim.x) buf[i] = v;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(buf);
+    int inflight = 0;
+    for (size_t off = (size_t)blockIdx.x * kChunk; off + kChunk <= bytes; off += (size_t)gridDim.x * kChunk) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + off), "r"(s),
+                   "n"(kChunk) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (++inflight >= 8) {
+        asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory");
+      }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
+int main() {
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (n < 2) { std::printf("need 2 GPUs\n"); return 0; }
+  const size_t bytes = 256ull << 20;
+  float *src = nullptr, *dst = nullptr;
+  CK(cudaSetDevice(1));
+  CK(cudaMalloc(&dst, bytes));
+  CK(cudaSetDevice(0));
+  CK(cudaMalloc(&src, bytes));
+  CK(cudaDeviceEnablePeerAccess(1, 0));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  auto timeit = [&](auto launch) -> double {
+    for (int w = 0; w < 2; ++w) launch();
+    cudaEventRecord(e0);
+    for (int r = 0; r < 5; ++r) launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return bytes * 5 / (ms * 1e-3) / 1e9;
+  };
+  std::printf("copy engine cudaMemcpyPeerAsync: %.1f GB/s\n",
+              timeit([&] { cudaMemcpyPeerAsync(dst, 1, src, 0, bytes); }));
+  for (int ctas : {16, 32, 64, 140, 296}) {
+    const double a = timeit([&] { st16<<<ctas, 512>>>((float4*)dst, bytes / 16, 1.0f); });
+    const double b = timeit([&] { st32<<<ctas, 512>>>((float4*)dst, bytes / 16, 1.0f); });
+    const double c = timeit([&] { tma_bulk<<<ctas, 128>>>((char*)dst, bytes, 1.0f); });
+    std::printf("ctas=%3d  st16 %.1f  st32 %.1f  tma_bulk %.1f GB/s\n", ctas, a, b, c);
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
