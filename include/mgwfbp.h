@@ -214,6 +214,25 @@ int mgw_pipeline_debug(mgw_pipeline* pipe, uint32_t* engine_state4, uint64_t* cl
  * order (zero for groups without tiles). */
 int mgw_pipeline_stamps(mgw_pipeline* pipe, uint64_t* stamps_2g);
 
+/* Host-driven persistent comm engine for a REAL backward (SURVEY §8f row
+ * 2; paper Algorithm 2 with the daemon thread on the GPU): instead of the
+ * replay, the framework marks each group ready on its compute stream after
+ * the backward of the group's layers (e.g. from autograd post-accumulate
+ * hooks). Per iteration: mgw_engine_begin (launch the engine after the work
+ * queued on after_stream), mgw_engine_mark_ready per group (1-thread kernel
+ * on the compute stream; groups may complete in any order, they are reduced
+ * FIFO in backward order), mgw_engine_join (stream waits until every group's
+ * SGD is done). engine_ctas > 0 should be small so the backward keeps SMs.
+ * Timing / destroy through mgw_pipeline_group_times / mgw_pipeline_stamps /
+ * mgw_pipeline_destroy. */
+int mgw_engine_create(mgw_plan* plan, float lr, int algo, int engine_ctas, int record_group_times,
+                      mgw_pipeline** out);
+int mgw_engine_begin(mgw_pipeline* engine, void* after_stream);
+int mgw_engine_mark_ready(mgw_pipeline* engine, int group, void* stream);
+int mgw_engine_join(mgw_pipeline* engine, void* stream);
+/* Synchronise the engine and report a barrier / ready timeout as an error. */
+int mgw_engine_check(mgw_pipeline* engine);
+
 /* On-box calibration sweep (N1): for each size, warmup + reps timed runs
  * of the fused group kernel on a single-layer group of size/4 elements;
  * writes the median per size. Collective. */

@@ -103,6 +103,11 @@ mgw_pipeline_group_times = _proto("mgw_pipeline_group_times", [vp, f32p])
 mgw_pipeline_stream = _proto("mgw_pipeline_stream", [vp, C.POINTER(vp)])
 mgw_pipeline_debug = _proto("mgw_pipeline_debug", [vp, C.POINTER(C.c_uint32), u64p])
 mgw_pipeline_stamps = _proto("mgw_pipeline_stamps", [vp, u64p])
+mgw_engine_create = _proto("mgw_engine_create", [vp, C.c_float, C.c_int, C.c_int, C.c_int, C.POINTER(vp)])
+mgw_engine_begin = _proto("mgw_engine_begin", [vp, vp])
+mgw_engine_mark_ready = _proto("mgw_engine_mark_ready", [vp, C.c_int, vp])
+mgw_engine_join = _proto("mgw_engine_join", [vp, vp])
+mgw_engine_check = _proto("mgw_engine_check", [vp])
 mgw_kernel_launches = _proto("mgw_kernel_launches", [], C.c_uint64)
 
 # Every symbol the header declares (checked by tests/test_capi_symbols.py).

@@ -423,10 +423,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     const uint32_t units = two ? (grp.n_tiles + P - 1) / P : grp.n_tiles;
     if (blockIdx.x >= units) continue;  // same on every rank: no barrier to skip
     if (threadIdx.x == 0) {
-      const uint32_t target = iter * E.G + k + 1;
-      if (static_cast<int32_t>(ld_acquire_gpu(E.pipe) - target) < 0) {
+      // group gi is ready for iteration `iter` once its flag reached iter+1
+      // (set by the replay, or by a mark kernel after the real backward of
+      // the group's layers — groups may complete out of FIFO order)
+      const uint32_t target = iter + 1;
+      const uint32_t* flag = E.ready + gi;
+      if (static_cast<int32_t>(ld_acquire_gpu(flag) - target) < 0) {
         const uint64_t t0 = globaltimer_ns();
-        while (static_cast<int32_t>(ld_acquire_gpu(E.pipe) - target) < 0) {
+        while (static_cast<int32_t>(ld_acquire_gpu(flag) - target) < 0) {
           if (globaltimer_ns() - t0 > kTimeoutNs) {  // compute side never signalled
             atomicExch(E.pipe + 3, 1u);
             break;
@@ -495,18 +499,28 @@ __global__ void __launch_bounds__(kThreads) unpack_sgd_kernel(const Tile* tiles,
 // mark the group ready for the comm engine. No per-group kernel launches, so
 // the emulated compute stream is continuously busy and its timing exact.
 __global__ void replay_all_kernel(unsigned long long* clock, const unsigned long long* deadlines,
-                                  uint32_t n, uint32_t* ready) {
+                                  uint32_t n, const uint32_t* pipe, uint32_t* flags) {
   if (threadIdx.x != 0) return;
+  // the engine of the previous iteration has finished (graph join), so the
+  // iteration counter is this iteration's
+  const uint32_t stamp = ld_volatile_u32(pipe + 1) + 1;
   const unsigned long long t0 = globaltimer_ns();
   clock[0] = t0;
   unsigned long long now = t0;
   for (uint32_t k = 0; k < n; ++k) {
     const unsigned long long due = t0 + deadlines[k];
     while (now < due) now = globaltimer_ns();
-    __threadfence();
-    atomicAdd(ready, 1u);
+    st_release_gpu(flags + (n - 1 - k), stamp);  // groups in backward order
   }
   clock[1] = now;
+}
+
+// Real-backward integration: after the backward of every layer of group g
+// has been enqueued on the compute stream, this 1-thread kernel marks g
+// ready for the comm engine of the running iteration (stream order makes
+// the group's gradients complete before it runs).
+__global__ void mark_ready_kernel(const uint32_t* pipe, uint32_t* flags, uint32_t g) {
+  if (threadIdx.x == 0) st_release_gpu(flags + g, ld_volatile_u32(pipe + 1) + 1);
 }
 
 // One group head of the replay (per-group-launch pipelines). clock[0]:
@@ -645,8 +659,15 @@ cudaError_t launch_l2_flush(void* buf, size_t bytes, int ctas, cudaStream_t stre
 }
 
 cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long long* deadlines_ns,
-                              uint32_t n, uint32_t* ready, cudaStream_t stream) {
-  replay_all_kernel<<<1, 32, 0, stream>>>(clock, deadlines_ns, n, ready);
+                              uint32_t n, const uint32_t* pipe, uint32_t* flags,
+                              cudaStream_t stream) {
+  replay_all_kernel<<<1, 32, 0, stream>>>(clock, deadlines_ns, n, pipe, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mark_ready(const uint32_t* pipe, uint32_t* flags, uint32_t g,
+                              cudaStream_t stream) {
+  mark_ready_kernel<<<1, 32, 0, stream>>>(pipe, flags, g);
   return cudaGetLastError();
 }
 

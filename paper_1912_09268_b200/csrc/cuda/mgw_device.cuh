@@ -90,7 +90,8 @@ struct EngineLaunch {
   float lr;
   int epilogue;
   uint64_t slot_stride;
-  uint32_t* pipe;                // [0] groups made ready (monotone), [1] iteration, [2] CTA exit count
+  uint32_t* pipe;                // [1] iteration, [2] CTA exit count, [3] ready-timeout flag
+  const uint32_t* ready;         // G flags: group g ready for iteration i when >= i + 1
   uint32_t* group_done;          // G counters for end stamps (NULL: no timing)
   unsigned long long* stamps;    // 2*G: (start, end) %globaltimer of each group (NULL: no timing)
 };
@@ -101,6 +102,10 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

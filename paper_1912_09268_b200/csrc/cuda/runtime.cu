@@ -37,7 +37,10 @@ cudaError_t launch_replay(unsigned long long* clock, unsigned long long deadline
                           uint32_t* ready, cudaStream_t stream);
 cudaError_t launch_engine(const EngineLaunch& E, int ctas, cudaStream_t stream);
 cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long long* deadlines_ns,
-                              uint32_t n, uint32_t* ready, cudaStream_t stream);
+                              uint32_t n, const uint32_t* pipe, uint32_t* flags,
+                              cudaStream_t stream);
+cudaError_t launch_mark_ready(const uint32_t* pipe, uint32_t* flags, uint32_t g,
+                              cudaStream_t stream);
 cudaError_t engine_ctas_per_sm(int nranks, int* out);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, int ctas, cudaStream_t stream);
 
@@ -133,6 +136,9 @@ struct mgw_pipeline {
   unsigned long long* d_stamps = nullptr; // 2G
   mgw::EngineGroup* d_groups = nullptr;   // G
   unsigned long long* d_deadlines = nullptr;  // G group-head ready times (ns), backward order
+  uint32_t* d_ready = nullptr;            // G ready flags (iteration stamps)
+  mgw::EngineLaunch args{};               // engine kernel arguments
+  bool manual = false;                    // host-driven engine (real backward), no graph
 };
 
 namespace mgw {
@@ -616,6 +622,58 @@ int mgw_pipeline_create(mgw_plan* p, const double* t_b, double t_f, float lr, in
 namespace mgw {
 namespace {
 
+// Persistent-engine resources of a pipeline: group table, ready flags,
+// counters, stamps, and the kernel arguments (fixed for the pipeline's life).
+void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, float lr, bool timed) {
+  mgw_comm* c = p->comm;
+  const int G = p->G();
+  int occ = 1;
+  ck(engine_ctas_per_sm(c->nranks, &occ), "engine occupancy");
+  // The engine runs concurrently with the compute stream, whose kernels must
+  // still find SMs: measured on B200, a 1-thread replay kernel is NOT
+  // scheduled next to engine CTAs when every SM holds one (the engine then
+  // waits forever for a ready signal), so kFreeSms SMs are always left
+  // without an engine CTA. A real backward needs SMs too (use few CTAs).
+  constexpr int kFreeSms = 8;
+  const int cap = std::max(1, std::min({kMaxCtas, std::max(1, occ) * c->num_sms - 1,
+                                        c->num_sms - kFreeSms}));
+  pipe->engine_ctas = std::min(cap, engine_ctas < 0 ? cap : engine_ctas);
+  const size_t g1 = static_cast<size_t>(std::max(G, 1));
+  ck(cudaMalloc(&pipe->d_pipe, 4 * sizeof(uint32_t)), "cudaMalloc(pipe)");
+  ck(cudaMemset(pipe->d_pipe, 0, 4 * sizeof(uint32_t)), "memset(pipe)");
+  ck(cudaMalloc(&pipe->d_ready, g1 * sizeof(uint32_t)), "cudaMalloc(ready)");
+  ck(cudaMemset(pipe->d_ready, 0, g1 * sizeof(uint32_t)), "memset(ready)");
+  ck(cudaMalloc(&pipe->d_group_done, g1 * sizeof(uint32_t)), "cudaMalloc");
+  ck(cudaMemset(pipe->d_group_done, 0, g1 * sizeof(uint32_t)), "memset");
+  ck(cudaMalloc(&pipe->d_stamps, 2 * g1 * sizeof(unsigned long long)), "cudaMalloc");
+  ck(cudaMemset(pipe->d_stamps, 0, 2 * g1 * sizeof(unsigned long long)), "memset");
+  std::vector<EngineGroup> groups(G);
+  for (int g = 0; g < G; ++g) {
+    groups[g].tile_first = p->tile_first[g];
+    groups[g].n_tiles = p->tile_first[g + 1] - p->tile_first[g];
+    groups[g].two_shot = use_two_shot(c, group_bytes(p, g), algo) ? 1u : 0u;
+    groups[g].pad = 0;
+  }
+  ck(cudaMalloc(&pipe->d_groups, g1 * sizeof(EngineGroup)), "cudaMalloc(groups)");
+  ck(cudaMemcpy(pipe->d_groups, groups.data(), G * sizeof(EngineGroup), cudaMemcpyHostToDevice),
+     "upload groups");
+  EngineLaunch& E = pipe->args;
+  E = EngineLaunch{};
+  E.v = make_view(c, 0, p->d_grads, p->d_weights);
+  E.tiles = p->d_tiles;
+  E.groups = pipe->d_groups;
+  E.G = static_cast<uint32_t>(G);
+  E.nranks = c->nranks;
+  E.scale = 1.0f / static_cast<float>(c->nranks);
+  E.lr = lr;
+  E.epilogue = MGW_SGD;
+  E.slot_stride = c->arena_elems;
+  E.pipe = pipe->d_pipe;
+  E.ready = pipe->d_ready;
+  E.group_done = timed ? pipe->d_group_done : nullptr;
+  E.stamps = timed ? pipe->d_stamps : nullptr;
+}
+
 // Backward-replay pipeline as one CUDA graph per iteration. engine_ctas == 0:
 // one fused kernel launch per group, each waiting on its head's ready event;
 // engine_ctas != 0: ONE persistent engine kernel (engine_ctas CTAs, < 0 =
@@ -639,33 +697,7 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
     const int G = p->G();
     mgw_comm* c = p->comm;
     if (pipe->engine) {
-      int occ = 1;
-      ck(engine_ctas_per_sm(c->nranks, &occ), "engine occupancy");
-      // The engine runs concurrently with the compute stream, whose kernels
-      // must still find SMs: measured on B200, a 1-thread replay kernel is
-      // NOT scheduled next to engine CTAs when every SM holds one (the
-      // engine then waits forever for a ready signal), so kFreeSms SMs are
-      // always left without an engine CTA. A real backward needs them too.
-      constexpr int kFreeSms = 8;
-      const int cap = std::max(1, std::min({kMaxCtas, std::max(1, occ) * c->num_sms - 1,
-                                            c->num_sms - kFreeSms}));
-      pipe->engine_ctas = std::min(cap, engine_ctas < 0 ? cap : engine_ctas);
-      ck(cudaMalloc(&pipe->d_pipe, 4 * sizeof(uint32_t)), "cudaMalloc(pipe)");
-      ck(cudaMemset(pipe->d_pipe, 0, 4 * sizeof(uint32_t)), "memset(pipe)");
-      ck(cudaMalloc(&pipe->d_group_done, std::max(G, 1) * sizeof(uint32_t)), "cudaMalloc");
-      ck(cudaMemset(pipe->d_group_done, 0, std::max(G, 1) * sizeof(uint32_t)), "memset");
-      ck(cudaMalloc(&pipe->d_stamps, 2 * std::max(G, 1) * sizeof(unsigned long long)), "cudaMalloc");
-      ck(cudaMemset(pipe->d_stamps, 0, 2 * std::max(G, 1) * sizeof(unsigned long long)), "memset");
-      std::vector<EngineGroup> groups(G);
-      for (int g = 0; g < G; ++g) {
-        groups[g].tile_first = p->tile_first[g];
-        groups[g].n_tiles = p->tile_first[g + 1] - p->tile_first[g];
-        groups[g].two_shot = use_two_shot(c, group_bytes(p, g), algo) ? 1u : 0u;
-        groups[g].pad = 0;
-      }
-      ck(cudaMalloc(&pipe->d_groups, std::max(G, 1) * sizeof(EngineGroup)), "cudaMalloc(groups)");
-      ck(cudaMemcpy(pipe->d_groups, groups.data(), G * sizeof(EngineGroup), cudaMemcpyHostToDevice),
-         "upload groups");
+      setup_engine(pipe, p, algo, engine_ctas, lr, timed);
       // ready time of every group head, in backward (comm) order
       std::vector<unsigned long long> dl;
       for (int g = G - 1; g >= 0; --g) {
@@ -707,25 +739,10 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
         ck(launch_l2_flush(pipe->flush_buf, pipe->flush_bytes, 16, pipe->comm), "l2 flush");
       }
       if (pipe->engine) {
-        EngineLaunch E{};
-        E.v = make_view(c, 0, p->d_grads, p->d_weights);
-        E.tiles = p->d_tiles;
-        E.groups = pipe->d_groups;
-        E.G = static_cast<uint32_t>(G);
-        E.nranks = c->nranks;
-        E.scale = 1.0f / static_cast<float>(c->nranks);
-        E.lr = lr;
-        E.epilogue = MGW_SGD;
-        E.slot_stride = c->arena_elems;
-        E.pipe = pipe->d_pipe;
-        E.group_done = timed ? pipe->d_group_done : nullptr;
-        E.stamps = timed ? pipe->d_stamps : nullptr;
-        ck(launch_engine(E, pipe->engine_ctas, pipe->comm), "engine launch");
-      }
-      if (pipe->engine) {
+        ck(launch_engine(pipe->args, pipe->engine_ctas, pipe->comm), "engine launch");
         // one replay kernel walks every group head's ready time
         ck(launch_replay_all(pipe->d_clock, pipe->d_deadlines, static_cast<uint32_t>(G), pipe->d_pipe,
-                             pipe->compute),
+                             pipe->d_ready, pipe->compute),
            "replay");
       }
       bool first = true;
@@ -777,6 +794,7 @@ int mgw_pipeline_destroy(mgw_pipeline* pipe) {
     if (pipe == nullptr) return 0;
     cudaSetDevice(pipe->plan->comm->device);
     cudaStreamSynchronize(pipe->compute);
+    cudaStreamSynchronize(pipe->comm);
     if (pipe->exec) cudaGraphExecDestroy(pipe->exec);
     if (pipe->graph) cudaGraphDestroy(pipe->graph);
     for (auto e : pipe->ready) cudaEventDestroy(e);
@@ -791,6 +809,7 @@ int mgw_pipeline_destroy(mgw_pipeline* pipe) {
     if (pipe->d_stamps) cudaFree(pipe->d_stamps);
     if (pipe->d_groups) cudaFree(pipe->d_groups);
     if (pipe->d_deadlines) cudaFree(pipe->d_deadlines);
+    if (pipe->d_ready) cudaFree(pipe->d_ready);
     cudaStreamDestroy(pipe->compute);
     cudaStreamDestroy(pipe->comm);
     delete pipe;
@@ -800,7 +819,7 @@ int mgw_pipeline_destroy(mgw_pipeline* pipe) {
 
 int mgw_pipeline_launch(mgw_pipeline* pipe, int iters) {
   MGW_TRY {
-    require(pipe != nullptr && iters >= 0, "bad pipeline launch");
+    require(pipe != nullptr && iters >= 0 && !pipe->manual, "bad pipeline launch");
     mgw::set_device(pipe->plan->comm);
     for (int i = 0; i < iters; ++i) {
       ck(cudaGraphLaunch(pipe->exec, pipe->compute), "graph launch");
@@ -812,7 +831,8 @@ int mgw_pipeline_launch(mgw_pipeline* pipe, int iters) {
 
 int mgw_pipeline_run(mgw_pipeline* pipe, int iters, float* iter_ms) {
   MGW_TRY {
-    require(pipe != nullptr && iters >= 1 && iter_ms != nullptr, "bad pipeline run");
+    require(pipe != nullptr && iters >= 1 && iter_ms != nullptr && !pipe->manual,
+            "bad pipeline run");
     mgw::set_device(pipe->plan->comm);
     std::vector<cudaEvent_t> ev(static_cast<size_t>(iters) + 1);
     for (auto& e : ev) ck(cudaEventCreate(&e), "event");
@@ -849,6 +869,7 @@ int mgw_pipeline_group_times(mgw_pipeline* pipe, float* group_ms) {
             "pipeline was created without record_group_times");
     mgw::set_device(pipe->plan->comm);
     ck(cudaStreamSynchronize(pipe->compute), "sync");
+    ck(cudaStreamSynchronize(pipe->comm), "sync");
     if (pipe->engine) {
       const int G = pipe->plan->G();
       std::vector<unsigned long long> st(2 * static_cast<size_t>(G));
@@ -940,12 +961,91 @@ int mgw_pipeline_stream(mgw_pipeline* pipe, void** stream_out) {
   MGW_CATCH
 }
 
+int mgw_engine_create(mgw_plan* p, float lr, int algo, int engine_ctas, int record_group_times,
+                      mgw_pipeline** out) {
+  MGW_TRY {
+    require(p != nullptr && out != nullptr, "bad engine arguments");
+    require(!p->comm->loopback, "engines run on a real communicator");
+    require(engine_ctas != 0, "engine_ctas must be non-zero (< 0: default)");
+    mgw::set_device(p->comm);
+    auto* pipe = new mgw_pipeline();
+    pipe->plan = p;
+    pipe->timed_groups = record_group_times != 0;
+    pipe->engine = true;
+    pipe->manual = true;
+    mgw::setup_engine(pipe, p, algo, engine_ctas, lr, pipe->timed_groups);
+    ck(cudaStreamCreateWithFlags(&pipe->compute, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&pipe->comm, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&pipe->fork, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&pipe->join, cudaEventDisableTiming), "event");
+    ck(cudaMalloc(&pipe->d_clock, 2 * sizeof(unsigned long long)), "cudaMalloc(clock)");
+    ck(cudaMemset(pipe->d_clock, 0, 2 * sizeof(unsigned long long)), "memset(clock)");
+    pipe->kernels_per_iter = 1 + p->G();  // engine + one mark kernel per group
+    *out = pipe;
+  }
+  MGW_CATCH
+}
+
+int mgw_engine_begin(mgw_pipeline* pipe, void* after_stream) {
+  MGW_TRY {
+    require(pipe != nullptr && pipe->manual, "not a host-driven engine");
+    mgw::set_device(pipe->plan->comm);
+    if (after_stream != nullptr) {
+      ck(cudaEventRecord(pipe->fork, static_cast<cudaStream_t>(after_stream)), "fork");
+      ck(cudaStreamWaitEvent(pipe->comm, pipe->fork, 0), "fork wait");
+    }
+    ck(mgw::launch_engine(pipe->args, pipe->engine_ctas, pipe->comm), "engine launch");
+    mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  MGW_CATCH
+}
+
+int mgw_engine_mark_ready(mgw_pipeline* pipe, int group, void* stream) {
+  MGW_TRY {
+    require(pipe != nullptr && pipe->manual, "not a host-driven engine");
+    require(group >= 0 && group < pipe->plan->G(), "group index out of range");
+    mgw::set_device(pipe->plan->comm);
+    ck(mgw::launch_mark_ready(pipe->d_pipe, pipe->d_ready, static_cast<uint32_t>(group),
+                              static_cast<cudaStream_t>(stream)),
+       "mark ready");
+    mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  MGW_CATCH
+}
+
+int mgw_engine_join(mgw_pipeline* pipe, void* stream) {
+  MGW_TRY {
+    require(pipe != nullptr && pipe->manual, "not a host-driven engine");
+    mgw::set_device(pipe->plan->comm);
+    ck(cudaEventRecord(pipe->join, pipe->comm), "join");
+    ck(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pipe->join, 0), "join wait");
+  }
+  MGW_CATCH
+}
+
+int mgw_engine_check(mgw_pipeline* pipe) {
+  MGW_TRY {
+    require(pipe != nullptr && pipe->engine, "not an engine");
+    mgw::set_device(pipe->plan->comm);
+    ck(cudaStreamSynchronize(pipe->comm), "engine sync");
+    mgw::check_barrier_flags(pipe->plan->comm);
+    uint32_t st[4];
+    ck(cudaMemcpy(st, pipe->d_pipe, sizeof st, cudaMemcpyDeviceToHost), "read pipe state");
+    if (st[3] != 0) {
+      throw mgw::CudaFailure("comm engine timed out waiting for a ready group (a group was never "
+                             "marked ready, or the compute stream could not run)");
+    }
+  }
+  MGW_CATCH
+}
+
 int mgw_pipeline_stamps(mgw_pipeline* pipe, uint64_t* stamps_2g) {
   MGW_TRY {
     require(pipe != nullptr && stamps_2g != nullptr && pipe->engine && pipe->timed_groups,
             "stamps need an engine pipeline created with record_group_times");
     mgw::set_device(pipe->plan->comm);
     ck(cudaStreamSynchronize(pipe->compute), "sync");
+    ck(cudaStreamSynchronize(pipe->comm), "sync");
     ck(cudaMemcpy(stamps_2g, pipe->d_stamps, 2 * pipe->plan->G() * sizeof(uint64_t),
                   cudaMemcpyDeviceToHost),
        "read stamps");

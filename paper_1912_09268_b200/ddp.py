@@ -1,0 +1,110 @@
+"""MG-WFBP for a real PyTorch backward (paper Algorithm 2,
+PAPER.md:486-563, and its system design PAPER.md:545-563).
+
+The paper's C++ daemon thread pops layer ids from a queue the backward pushes
+to and all-reduces each merged group when its last layer arrives. Here:
+
+* the "queue" is a per-group ready flag on the GPU: an autograd
+  post-accumulate-grad hook on every parameter counts the group's finished
+  members and, when the group is complete, enqueues a 1-thread mark kernel
+  on the current (compute) stream — no host synchronisation, no GIL wait;
+* the "daemon thread" is the persistent comm engine kernel (launched at the
+  start of the backward on its own stream, a few SMs): it reduces the groups
+  FIFO in backward order over NVLink, fused with the SGD update
+  `W = W - lr * mean(grad)` (paper line 15 of Algorithm 2);
+* gradients live in one flat buffer with 16-byte aligned per-parameter
+  views (`p.grad`), so autograd accumulates in place at stable addresses.
+
+    sync = MGWFBP(model, comm, lr=0.01, plan=plan)
+    for x, y in data:
+        sync.begin()                 # zero grads, launch the engine
+        loss_fn(model(x), y).backward()
+        sync.end()                   # next forward waits for the SGD
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional
+
+import torch
+
+from . import _lib
+from .gradsched import MergePlan, check
+from .runtime import ALGO, Comm, DevicePlan, padded_elems
+
+
+class MGWFBP:
+    def __init__(self, model: torch.nn.Module, comm: Comm, lr: float, plan: Optional[MergePlan] = None,
+                 algo: str = "auto", engine_ctas: int = 16, record_group_times: bool = False):
+        self.params: List[torch.nn.Parameter] = [p for p in model.parameters() if p.requires_grad]
+        for p in self.params:
+            if p.dtype != torch.float32 or not p.is_cuda or not p.is_contiguous():
+                raise ValueError("MGWFBP needs contiguous fp32 CUDA parameters")
+        L = len(self.params)
+        self.plan = plan if plan is not None else MergePlan.all_normal(L)
+        if len(self.plan.tags) != L:
+            raise ValueError(f"plan has {len(self.plan.tags)} tags for {L} parameters")
+        counts = [p.numel() for p in self.params]
+        dev = self.params[0].device
+        self.flat_grad = torch.zeros(max(1, padded_elems(counts)), dtype=torch.float32, device=dev)
+        off = 0
+        grads = []
+        for p, c in zip(self.params, counts):
+            view = self.flat_grad[off:off + c]
+            p.grad = view.view_as(p)
+            grads.append(view)
+            off += (c + 3) & ~3
+        weights = [p.data.view(-1) for p in self.params]
+        self.dplan = DevicePlan(comm, grads, weights, self.plan)
+        h = C.c_void_p()
+        check(_lib.mgw_engine_create(self.dplan.handle, lr, ALGO[algo], engine_ctas,
+                                     int(record_group_times), C.byref(h)))
+        self.handle = h
+        self.groups = self.plan.groups()
+        self.group_of = [0] * L
+        for g, members in enumerate(self.groups):
+            for i in members:
+                self.group_of[i] = g
+        self.remaining = [len(m) for m in self.groups]
+        self._hooks = [p.register_post_accumulate_grad_hook(self._hook(i)) for i, p in enumerate(self.params)]
+
+    def _hook(self, i: int):
+        def hook(_p):
+            g = self.group_of[i]
+            self.remaining[g] -= 1
+            if self.remaining[g] == 0:
+                check(_lib.mgw_engine_mark_ready(self.handle, g, torch.cuda.current_stream().cuda_stream))
+        return hook
+
+    def begin(self) -> None:
+        """Zero the gradients and start this iteration's comm engine."""
+        for p in self.params:
+            if p.grad is None or p.grad.data_ptr() < self.flat_grad.data_ptr():
+                raise RuntimeError("a parameter's .grad was replaced; keep zero_grad(set_to_none=False)")
+        self.flat_grad.zero_()
+        self.remaining = [len(m) for m in self.groups]
+        check(_lib.mgw_engine_begin(self.handle, torch.cuda.current_stream().cuda_stream))
+
+    def end(self) -> None:
+        """Make the current stream wait until every group's SGD is applied."""
+        missing = [g for g, r in enumerate(self.remaining) if r != 0]
+        for g in missing:  # parameters that got no gradient this iteration
+            check(_lib.mgw_engine_mark_ready(self.handle, g, torch.cuda.current_stream().cuda_stream))
+        check(_lib.mgw_engine_join(self.handle, torch.cuda.current_stream().cuda_stream))
+
+    def check(self) -> None:
+        check(_lib.mgw_engine_check(self.handle))
+
+    def group_times_ms(self) -> List[float]:
+        out = (C.c_float * max(1, len(self.groups)))()
+        check(_lib.mgw_pipeline_group_times(self.handle, out))
+        return list(out)[: len(self.groups)]
+
+    def close(self) -> None:
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
+        if self.handle:
+            check(_lib.mgw_pipeline_destroy(self.handle))
+            self.handle = None
+        self.dplan.close()

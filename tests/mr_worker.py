@@ -100,6 +100,37 @@ def main():
         pipe.close()
         dp.close()
 
+    # real backward (autograd hooks -> engine), each rank on different data:
+    # weights after the step == W - lr * (g_0/P + ... + g_{P-1}/P), rank order
+    from paper_1912_09268_b200.ddp import MGWFBP
+
+    torch.manual_seed(0)
+    model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.ReLU(), torch.nn.Linear(256, 10)).cuda()
+    L = len(list(model.parameters()))
+    mplan = gs.MergePlan([gs.LayerTag(0 if i % 2 == 0 else 1) for i in range(L)])
+    sync = MGWFBP(model, comm, LR, plan=mplan, engine_ctas=8)
+    gen = torch.Generator(device="cuda").manual_seed(100 + rank)
+    for step in range(3):
+        w_before = [p.detach().cpu().numpy().copy() for p in model.parameters()]
+        x = torch.randn(16, 64, device="cuda", generator=gen)
+        y = torch.randint(0, 10, (16,), device="cuda", generator=gen)
+        sync.begin()
+        torch.nn.functional.cross_entropy(model(x), y).backward()
+        sync.end()
+        torch.cuda.synchronize()
+        grads = [None] * P
+        dist.all_gather_object(grads, [p.grad.detach().cpu().numpy().copy() for p in model.parameters()])
+        s = np.float32(1.0 / P)
+        for li, p in enumerate(model.parameters()):
+            acc = (grads[0][li] * s).astype(np.float32)
+            for r in range(1, P):
+                acc = (acc + (grads[r][li] * s).astype(np.float32)).astype(np.float32)
+            want = (w_before[li] - (np.float32(LR) * acc).astype(np.float32)).astype(np.float32)
+            if not np.array_equal(p.detach().cpu().numpy(), want):
+                failures.append(f"real backward step {step} param {li}")
+    sync.check()
+    sync.close()
+
     meas = comm.calibrate([4096 << k for k in range(0, 12, 2)], warmup=2, reps=5)  # <= arena
     meas_e = comm.calibrate_engine([4096 << k for k in range(0, 12, 2)], warmup=1, reps=3)
     for mm in (meas, meas_e):
