@@ -665,6 +665,38 @@ cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long lon
   return cudaGetLastError();
 }
 
+// CUDA 12 loads modules lazily, at a kernel's first launch, and that load
+// waits for the context to go idle. A 1-thread mark / replay kernel launched
+// for the first time while the persistent engine spins waiting for it would
+// therefore deadlock (measured: the engine hit its 10 s ready timeout, then
+// the mark kernel ran). Every kernel is loaded up front instead.
+cudaError_t preload_kernels() {
+  const void* fns[] = {
+      reinterpret_cast<const void*>(mark_ready_kernel),
+      reinterpret_cast<const void*>(replay_all_kernel),
+      reinterpret_cast<const void*>(replay_kernel),
+      reinterpret_cast<const void*>(l2_flush_kernel),
+      reinterpret_cast<const void*>(pack_kernel),
+      reinterpret_cast<const void*>(unpack_sgd_kernel),
+      engine_fn(1), engine_fn(2), engine_fn(4), engine_fn(8),
+  };
+  for (const void* f : fns) {
+    cudaFuncAttributes attr;
+    const cudaError_t e = cudaFuncGetAttributes(&attr, f);
+    if (e != cudaSuccess) return e;
+  }
+  for (bool lb : {false, true}) {
+    for (int p : {1, 2, 4, 8}) {
+      for (bool two : {false, true}) {
+        int occ = 0;
+        const cudaError_t e = max_ctas_per_sm(p, two, lb, &occ);
+        if (e != cudaSuccess) return e;
+      }
+    }
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_mark_ready(const uint32_t* pipe, uint32_t* flags, uint32_t g,
                               cudaStream_t stream) {
   mark_ready_kernel<<<1, 32, 0, stream>>>(pipe, flags, g);

@@ -41,6 +41,7 @@ cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long lon
                               cudaStream_t stream);
 cudaError_t launch_mark_ready(const uint32_t* pipe, uint32_t* flags, uint32_t g,
                               cudaStream_t stream);
+cudaError_t preload_kernels();
 cudaError_t engine_ctas_per_sm(int nranks, int* out);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, int ctas, cudaStream_t stream);
 
@@ -167,6 +168,7 @@ void init_common(mgw_comm* c, int device, size_t arena_bytes) {
   c->arena_elems = (arena_bytes / sizeof(float) + 3) & ~size_t{3};
   ck(cudaSetDevice(device), "cudaSetDevice");
   ck(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+  ck(preload_kernels(), "preload kernels (lazy module loading would deadlock the engine)");
   ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
   ck(cudaMalloc(&c->d_clock, 2 * sizeof(unsigned long long)), "cudaMalloc(clock)");
   ck(cudaMemset(c->d_clock, 0, 2 * sizeof(unsigned long long)), "memset(clock)");
