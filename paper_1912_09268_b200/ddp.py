@@ -24,6 +24,7 @@ to and all-reduces each merged group when its last layer arrives. Here:
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import List, Optional
 
 import torch
@@ -66,6 +67,8 @@ class MGWFBP:
             for i in members:
                 self.group_of[i] = g
         self.remaining = [len(m) for m in self.groups]
+        self._iters = 0
+        self._launched = False
         self._hooks = [p.register_post_accumulate_grad_hook(self._hook(i)) for i, p in enumerate(self.params)]
 
     def _hook(self, i: int):
@@ -77,20 +80,33 @@ class MGWFBP:
         return hook
 
     def begin(self) -> None:
-        """Zero the gradients and start this iteration's comm engine."""
+        """Zero the gradients and start this iteration's comm engine.
+
+        The first iteration runs the engine only after the backward: CUDA 12
+        loads modules lazily at a kernel's first launch and that load waits
+        for the context to go idle, so a backward launching kernels for the
+        first time would stall behind the spinning engine (measured). After
+        one iteration every kernel is loaded and the engine overlaps.
+        (CUDA_MODULE_LOADING=EAGER removes the issue from the start.)"""
         for p in self.params:
             if p.grad is None or p.grad.data_ptr() < self.flat_grad.data_ptr():
                 raise RuntimeError("a parameter's .grad was replaced; keep zero_grad(set_to_none=False)")
         self.flat_grad.zero_()
         self.remaining = [len(m) for m in self.groups]
-        check(_lib.mgw_engine_begin(self.handle, torch.cuda.current_stream().cuda_stream))
+        self._launched = self._iters > 0 or os.environ.get("CUDA_MODULE_LOADING", "") == "EAGER"
+        if self._launched:
+            check(_lib.mgw_engine_begin(self.handle, torch.cuda.current_stream().cuda_stream))
 
     def end(self) -> None:
         """Make the current stream wait until every group's SGD is applied."""
+        stream = torch.cuda.current_stream().cuda_stream
         missing = [g for g, r in enumerate(self.remaining) if r != 0]
         for g in missing:  # parameters that got no gradient this iteration
-            check(_lib.mgw_engine_mark_ready(self.handle, g, torch.cuda.current_stream().cuda_stream))
-        check(_lib.mgw_engine_join(self.handle, torch.cuda.current_stream().cuda_stream))
+            check(_lib.mgw_engine_mark_ready(self.handle, g, stream))
+        if not self._launched:
+            check(_lib.mgw_engine_begin(self.handle, stream))
+        check(_lib.mgw_engine_join(self.handle, stream))
+        self._iters += 1
 
     def check(self) -> None:
         check(_lib.mgw_engine_check(self.handle))
