@@ -36,8 +36,12 @@ from .runtime import ALGO, Comm, DevicePlan, padded_elems
 
 class MGWFBP:
     def __init__(self, model: torch.nn.Module, comm: Comm, lr: float, plan: Optional[MergePlan] = None,
-                 algo: str = "auto", engine_ctas: int = 16, record_group_times: bool = False):
-        self.params: List[torch.nn.Parameter] = [p for p in model.parameters() if p.requires_grad]
+                 algo: str = "auto", engine_ctas: int = 16, record_group_times: bool = False,
+                 params: Optional[List[torch.nn.Parameter]] = None):
+        """params: the layer order of the plan / trace (forward order; the
+        backward visits it last to first). Default: model.parameters()."""
+        self.params: List[torch.nn.Parameter] = (list(params) if params is not None else
+                                                 [p for p in model.parameters() if p.requires_grad])
         for p in self.params:
             if p.dtype != torch.float32 or not p.is_cuda or not p.is_contiguous():
                 raise ValueError("MGWFBP needs contiguous fp32 CUDA parameters")

@@ -1,0 +1,137 @@
+"""Real-training comparison (paper §6 "real experiments"):
+a torchvision model trained with synthetic data on N GPUs (torchrun, one
+process per GPU), gradients synchronised by
+  ddp        torch DistributedDataParallel (NCCL, 25 MB buckets) + torch SGD
+  mgwfbp     this repo's persistent comm engine, optimal merge plan from the
+             model's B200-measured trace + the on-box calibration
+  wfbp       same engine, every layer its own group
+  single     same engine, one group (single buffer)
+Prints one JSON line per strategy (rank 0): median iteration ms, images/s.
+
+usage: torchrun --nproc-per-node N tools/train_bench.py --model resnet50 --batch 32
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_1912_09268_b200 import dist as D  # noqa: E402
+from paper_1912_09268_b200 import gradsched as gs  # noqa: E402
+from paper_1912_09268_b200 import runtime as rt  # noqa: E402
+from paper_1912_09268_b200.ddp import MGWFBP  # noqa: E402
+
+
+def build(name):
+    import torchvision
+
+    return getattr(torchvision.models, name)(weights=None)
+
+
+def time_loop(step, iters, warmup):
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    D.barrier()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
+    evs[0].record()
+    for i in range(iters):
+        step()
+        evs[i + 1].record()
+    torch.cuda.synchronize()
+    ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(iters)]
+    return D.max_over_ranks(statistics.median(ms))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--engine-ctas", type=int, default=16)
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--strategies", default="ddp,mgwfbp,wfbp,single")
+    args = ap.parse_args()
+    rank, N, local = D.init("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    torch.backends.cudnn.benchmark = True
+    x = torch.randn(args.batch, 3, 224, 224, device=dev)
+    y = torch.randint(0, 1000, (args.batch,), device=dev)
+    trace = gs.load_trace(os.path.join(ROOT, "traces", f"{args.model}.json"))
+    results = {}
+
+    def fwd_bwd(model):
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = torch.nn.functional.cross_entropy(model(x), y)
+        loss.backward()
+
+    for strat in args.strategies.split(","):
+        torch.manual_seed(0)
+        model = build(args.model).to(dev).train()
+        if strat == "ddp":
+            if N > 1:
+                ddp = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local], bucket_cap_mb=25)
+            else:
+                ddp = model
+            opt = torch.optim.SGD(model.parameters(), lr=args.lr)
+
+            def step():
+                opt.zero_grad(set_to_none=False)
+                fwd_bwd(ddp)
+                opt.step()
+
+            ms = time_loop(step, args.iters, args.warmup)
+            results[strat] = {"iter_ms": ms}
+            del ddp, opt
+        else:
+            named = dict(model.named_parameters())
+            params = [named[l.name] for l in trace.layers]  # the trace's layer order
+            counts = [p.numel() for p in params]
+            comm = rt.Comm(rank, N, local, 4 * rt.padded_elems(counts))
+            if strat == "mgwfbp":
+                sizes = [4096 << k for k in range(0, 20, 2) if (4096 << k) <= 4 * rt.padded_elems(counts)]
+                meas = comm.calibrate_engine(sizes, warmup=1, reps=3, engine_ctas=args.engine_ctas)
+                t = torch.tensor([m.time_sec for m in meas], dtype=torch.float64, device=dev)
+                if N > 1:
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                model_ab = gs.fit_model([gs.CommMeasurement(m.size_bytes, v) for m, v in zip(meas, t.tolist())])
+                plan = gs.optimal_plan(trace, model_ab)
+                D.agree_plan(plan.tags)
+                extra = {"a_us": model_ab.a * 1e6, "b_ps_per_byte": model_ab.b * 1e12}
+            elif strat == "wfbp":
+                plan, extra = gs.MergePlan.all_normal(len(params)), {}
+            else:
+                plan, extra = gs.MergePlan.all_merged(len(params)), {}
+            sync = MGWFBP(model, comm, args.lr, plan=plan, engine_ctas=args.engine_ctas, params=params)
+
+            def step():
+                sync.begin()
+                fwd_bwd(model)
+                sync.end()
+
+            ms = time_loop(step, args.iters, args.warmup)
+            sync.check()
+            results[strat] = {"iter_ms": ms, "groups": len(plan.groups()), **extra}
+            sync.close()
+            comm.close()
+        results[strat]["images_per_s"] = N * args.batch / (results[strat]["iter_ms"] / 1e3)
+        del model
+        torch.cuda.empty_cache()
+    if rank == 0:
+        print(json.dumps({"model": args.model, "batch_per_gpu": args.batch, "n_gpus": N,
+                          "engine_ctas": args.engine_ctas, "results": results}), flush=True)
+    dist.destroy_process_group() if dist.is_initialized() else None
+
+
+if __name__ == "__main__":
+    main()
