@@ -73,6 +73,7 @@ class MGWFBP:
         self.remaining = [len(m) for m in self.groups]
         self._iters = 0
         self._launched = False
+        self._lazy_launch = False
         self._hooks = [p.register_post_accumulate_grad_hook(self._hook(i)) for i, p in enumerate(self.params)]
 
     def _hook(self, i: int):
@@ -80,7 +81,13 @@ class MGWFBP:
             g = self.group_of[i]
             self.remaining[g] -= 1
             if self.remaining[g] == 0:
-                check(_lib.mgw_engine_mark_ready(self.handle, g, torch.cuda.current_stream().cuda_stream))
+                stream = torch.cuda.current_stream().cuda_stream
+                if self._lazy_launch and not self._launched:
+                    # start the engine with the first finished group: the
+                    # forward pass keeps every SM
+                    check(_lib.mgw_engine_begin(self.handle, None))
+                    self._launched = True
+                check(_lib.mgw_engine_mark_ready(self.handle, g, stream))
         return hook
 
     def begin(self) -> None:
@@ -97,9 +104,10 @@ class MGWFBP:
                 raise RuntimeError("a parameter's .grad was replaced; keep zero_grad(set_to_none=False)")
         self.flat_grad.zero_()
         self.remaining = [len(m) for m in self.groups]
-        self._launched = self._iters > 0 or os.environ.get("CUDA_MODULE_LOADING", "") == "EAGER"
-        if self._launched:
-            check(_lib.mgw_engine_begin(self.handle, torch.cuda.current_stream().cuda_stream))
+        self._launched = False
+        # overlap from the 2nd iteration (or from the start with eager module
+        # loading); the engine starts at the first finished group
+        self._lazy_launch = self._iters > 0 or os.environ.get("CUDA_MODULE_LOADING", "") == "EAGER"
 
     def end(self) -> None:
         """Make the current stream wait until every group's SGD is applied."""
