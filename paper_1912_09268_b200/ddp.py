@@ -36,7 +36,7 @@ from .runtime import ALGO, Comm, DevicePlan, padded_elems
 
 class MGWFBP:
     def __init__(self, model: torch.nn.Module, comm: Comm, lr: float, plan: Optional[MergePlan] = None,
-                 algo: str = "auto", engine_ctas: int = 16, record_group_times: bool = False,
+                 algo: str = "auto", engine_ctas: int = 8, record_group_times: bool = False,
                  params: Optional[List[torch.nn.Parameter]] = None):
         """params: the layer order of the plan / trace (forward order; the
         backward visits it last to first). Default: model.parameters()."""

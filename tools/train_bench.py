@@ -57,7 +57,7 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--engine-ctas", type=int, default=16)
+    ap.add_argument("--engine-ctas", type=int, default=8)
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--strategies", default="ddp,mgwfbp,wfbp,single")
     args = ap.parse_args()
