@@ -187,50 +187,94 @@ __device__ __forceinline__ void scatter_tile(const RankView& v, const Tile& t, i
   }
 }
 
-// Rank-order sum of tile t over the P local slots (x0 + x1 + ... + x_{P-1},
-// each already scaled by 1/P); all loads are local (.cg: peers wrote them).
+// Vectors of a thread reduced per batch: all slot loads of a batch are in
+// flight together (B * P <= 8 float4 per thread keeps the engine at <= 128
+// registers without spills).
 template <int P>
-__device__ __forceinline__ void reduce_slots(const RankView& v, const Tile& t, uint64_t slot_stride,
-                                             float4 (&acc)[kVecPerThread]) {
+struct RedBatch {
+  static constexpr uint32_t raw = P >= 4 ? 1 : 4 / P;
+  static constexpr uint32_t value = raw < kVecPerThread ? raw : kVecPerThread;
+};
+
+// SGD (+ optional grad write-back) for B vectors of tile t (thread vector
+// indices i0, i0 + stride, ...): the W loads of the whole batch are issued
+// before any store, so their latency overlaps.
+template <uint32_t B>
+__device__ __forceinline__ void apply_batch(const Tile& t, uint32_t i0, uint32_t stride,
+                                            const float4 (&g)[B], float* w_layer, float* g_layer,
+                                            float lr, int epi) {
+  const uint32_t nvec = (t.len + 3) >> 2;
+  const bool vec_w = (epi & MGW_SGD) && w_layer != nullptr && !(t.layer & kWeightUnaligned);
+  float4 wv[B];
+#pragma unroll
+  for (uint32_t j = 0; j < B; ++j) {
+    const uint32_t i = i0 + j * stride;
+    if (vec_w && i < nvec && i * 4 + 4 <= t.len) wv[j] = ld_v4(w_layer + t.src + i * 4);
+  }
+#pragma unroll
+  for (uint32_t j = 0; j < B; ++j) {
+    const uint32_t i = i0 + j * stride;
+    if (i >= nvec) continue;
+    const uint32_t e = i * 4;
+    if (vec_w && e + 4 <= t.len) {
+      float4 w = wv[j];
+      w.x = sgd1(w.x, g[j].x, lr);
+      w.y = sgd1(w.y, g[j].y, lr);
+      w.z = sgd1(w.z, g[j].z, lr);
+      w.w = sgd1(w.w, g[j].w, lr);
+      st_v4(w_layer + t.src + e, w);
+      if (epi & MGW_WRITE_GRAD) epilogue(t, e, g[j], nullptr, g_layer, lr, MGW_WRITE_GRAD);
+    } else {
+      epilogue(t, e, g[j], w_layer, g_layer, lr, epi);  // tail / unaligned / no-SGD
+    }
+  }
+}
+
+// Rank-order sum of tile t over the P local slots (x0 + x1 + ... + x_{P-1},
+// each already scaled by 1/P; .cg loads: peers wrote them), B vectors per
+// batch; optionally push each sum into slot `my_slot` of every peer (the
+// two-shot owner's all-gather), then SGD.
+template <int P>
+__device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, uint64_t slot_stride,
+                                            bool push_to_peers, uint64_t my_slot, float lr, int epi) {
+  constexpr uint32_t B = RedBatch<P>::value;
   const float* base = v.arena[v.rank] + t.moff;
   const uint32_t nvec = (t.len + 3) >> 2;
-  // all kVecPerThread x P loads in flight for P <= 4; one vector's P loads
-  // at a time for P = 8 (keeps the engine at <= 128 registers, no spills)
-  constexpr uint32_t B = P >= 8 ? 1 : kVecPerThread;
-#pragma unroll
+  const uint32_t layer = t.layer & kLayerMask;
+  float* w = v.weights[layer];
+  float* g = v.grads[layer];
+#pragma unroll 1
   for (uint32_t k0 = 0; k0 < kVecPerThread; k0 += B) {
+    const uint32_t i0 = threadIdx.x + k0 * kThreads;
+    if (i0 >= nvec) break;
     float4 x[B][P];
 #pragma unroll
     for (uint32_t j = 0; j < B; ++j) {
-      const uint32_t i = threadIdx.x + (k0 + j) * kThreads;
+      const uint32_t i = i0 + j * kThreads;
       if (i < nvec) {
 #pragma unroll
         for (int r = 0; r < P; ++r) x[j][r] = ld_cg_v4(base + r * slot_stride + i * 4);
       }
     }
+    float4 s[B];
 #pragma unroll
     for (uint32_t j = 0; j < B; ++j) {
-      float4 s = x[j][0];
+      s[j] = x[j][0];
 #pragma unroll
-      for (int r = 1; r < P; ++r) s = add4(s, x[j][r]);
-      acc[k0 + j] = s;
+      for (int r = 1; r < P; ++r) s[j] = add4(s[j], x[j][r]);
     }
-  }
-}
-
-template <int P>
-__device__ __forceinline__ void reduce_apply(const RankView& v, const Tile& t, uint64_t slot_stride,
-                                             float lr, int epi) {
-  float4 acc[kVecPerThread];
-  reduce_slots<P>(v, t, slot_stride, acc);
-  const uint32_t layer = t.layer & kLayerMask;
-  float* w = v.weights[layer];
-  float* g = v.grads[layer];
-  const uint32_t nvec = (t.len + 3) >> 2;
+    if (push_to_peers) {
 #pragma unroll
-  for (uint32_t k = 0; k < kVecPerThread; ++k) {
-    const uint32_t i = threadIdx.x + k * kThreads;
-    if (i < nvec) epilogue(t, i * 4, acc[k], w, g, lr, epi);
+      for (uint32_t j = 0; j < B; ++j) {
+        const uint32_t i = i0 + j * kThreads;
+        if (i >= nvec) continue;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          if (q != v.rank) st_v4(v.arena[q] + my_slot + t.moff + i * 4, s[j]);
+        }
+      }
+    }
+    apply_batch<B>(t, i0, kThreads, s, w, g, lr, epi);
   }
 }
 
@@ -259,7 +303,7 @@ __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* ti
     if (t >= 1) {
 #pragma unroll 1
       for (uint32_t j = (t - 1) * kOneShotChunk; j < mine && j < t * kOneShotChunk; ++j) {
-        reduce_apply<P>(v, tiles[cta + j * ncta], slot_stride, lr, epi);
+        reduce_tile<P>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, lr, epi);
       }
     }
     if (t < n_chunks) cta_barrier(v, P, cta, count, true);
@@ -298,25 +342,7 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
 #pragma unroll 1
     for (uint32_t j = c * C; j < mine && j < (c + 1) * C; ++j) {
       const uint32_t ti = (cta + j * ncta) * P + v.rank;
-      if (ti >= n_tiles) continue;
-      const Tile t = tiles[ti];
-      float4 acc[kVecPerThread];
-      reduce_slots<P>(v, t, slot_stride, acc);
-      const uint32_t layer = t.layer & kLayerMask;
-      float* w = v.weights[layer];
-      float* g = v.grads[layer];
-      const uint32_t nvec = (t.len + 3) >> 2;
-#pragma unroll
-      for (uint32_t k = 0; k < kVecPerThread; ++k) {
-        const uint32_t i = threadIdx.x + k * kThreads;
-        if (i < nvec) {
-#pragma unroll
-          for (int q = 0; q < P; ++q) {
-            if (q != v.rank) st_v4(v.arena[q] + my_slot + t.moff + i * 4, acc[k]);
-          }
-          epilogue(t, i * 4, acc[k], w, g, lr, epi);
-        }
-      }
+      if (ti < n_tiles) reduce_tile<P>(v, tiles[ti], slot_stride, true, my_slot, lr, epi);
     }
   };
   auto ap = [&](uint32_t c) {
@@ -330,8 +356,6 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
         const Tile t = tiles[ti];
         const float* red = v.arena[v.rank] + static_cast<uint64_t>(q) * slot_stride + t.moff;
         const uint32_t layer = t.layer & kLayerMask;
-        float* w = v.weights[layer];
-        float* g = v.grads[layer];
         const uint32_t nvec = (t.len + 3) >> 2;
         float4 x[kVecPerThread];
 #pragma unroll
@@ -339,11 +363,7 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
           const uint32_t i = threadIdx.x + k * kThreads;
           if (i < nvec) x[k] = ld_cg_v4(red + i * 4);
         }
-#pragma unroll
-        for (uint32_t k = 0; k < kVecPerThread; ++k) {
-          const uint32_t i = threadIdx.x + k * kThreads;
-          if (i < nvec) epilogue(t, i * 4, x[k], w, g, lr, epi);
-        }
+        apply_batch<kVecPerThread>(t, threadIdx.x, kThreads, x, v.weights[layer], v.grads[layer], lr, epi);
       }
     }
   };

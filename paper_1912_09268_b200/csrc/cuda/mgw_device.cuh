@@ -28,7 +28,7 @@ namespace mgw {
 constexpr int kMaxRanks = 8;
 constexpr int kMaxCtas = 1024;           // per-rank CTAs of one collective launch
 constexpr int kThreads = 512;            // threads per CTA of the fused kernel
-constexpr uint32_t kTileElems = 4096;    // 16 KiB of fp32; 2 float4 per thread
+constexpr uint32_t kTileElems = 8192;    // 32 KiB of fp32; 4 float4 per thread (memory-level parallelism)
 constexpr uint32_t kVecPerThread = kTileElems / 4 / kThreads;
 constexpr uint32_t kLayerMask = 0x3fffffffu;
 constexpr uint32_t kGradUnaligned = 0x80000000u;
