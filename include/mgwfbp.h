@@ -193,6 +193,15 @@ int mgw_comm_set_oneshot_max(mgw_comm* comm, uint64_t bytes);
 int mgw_pipeline_create(mgw_plan* plan, const double* t_b, double t_f, float lr, int algo,
                         int record_group_times, size_t l2_flush_bytes, int engine_ctas,
                         mgw_pipeline** out);
+/* Same, with the step's host I/O captured into the graph: h2d_bytes from
+ * pinned h2d_src to device h2d_dst on the comm branch at iteration start
+ * (every group waits for it; it overlaps the forward replay), and d2h_bytes
+ * from device d2h_src to pinned d2h_dst after the last group. One launch =
+ * one end-to-end step. */
+int mgw_pipeline_create_io(mgw_plan* plan, const double* t_b, double t_f, float lr, int algo,
+                           int record_group_times, size_t l2_flush_bytes, int engine_ctas,
+                           const void* h2d_src, void* h2d_dst, size_t h2d_bytes, void* d2h_dst,
+                           const void* d2h_src, size_t d2h_bytes, mgw_pipeline** out);
 int mgw_pipeline_destroy(mgw_pipeline* pipe);
 /* Launch `iters` iterations back to back on the pipeline's compute stream
  * (asynchronous). */

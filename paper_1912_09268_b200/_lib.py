@@ -96,6 +96,11 @@ mgw_calibrate_engine = _proto(
     "mgw_calibrate_engine",
     [vp, u64p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Meas)],
 )
+mgw_pipeline_create_io = _proto(
+    "mgw_pipeline_create_io",
+    [vp, f64p, C.c_double, C.c_float, C.c_int, C.c_int, C.c_size_t, C.c_int, vp, vp, C.c_size_t, vp, vp,
+     C.c_size_t, C.POINTER(vp)],
+)
 mgw_pipeline_destroy = _proto("mgw_pipeline_destroy", [vp])
 mgw_pipeline_launch = _proto("mgw_pipeline_launch", [vp, C.c_int])
 mgw_pipeline_run = _proto("mgw_pipeline_run", [vp, C.c_int, f32p])

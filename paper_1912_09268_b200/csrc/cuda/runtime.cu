@@ -324,8 +324,19 @@ mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* w
   return p;
 }
 
+// Optional per-step host I/O captured into the pipeline graph (e2e runs).
+struct StepIo {
+  const void* h2d_src = nullptr;  // pinned host input (e.g. the step's gradients)
+  void* h2d_dst = nullptr;
+  size_t h2d_bytes = 0;
+  void* d2h_dst = nullptr;        // pinned host result (e.g. a weight checksum)
+  const void* d2h_src = nullptr;
+  size_t d2h_bytes = 0;
+};
+
 mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float lr, int algo,
-                             bool timed, size_t l2_flush_bytes, int engine_ctas);
+                             bool timed, size_t l2_flush_bytes, int engine_ctas,
+                             const StepIo& io = StepIo{});
 
 }  // namespace
 }  // namespace mgw
@@ -619,6 +630,27 @@ int mgw_pipeline_create(mgw_plan* p, const double* t_b, double t_f, float lr, in
   MGW_CATCH
 }
 
+int mgw_pipeline_create_io(mgw_plan* p, const double* t_b, double t_f, float lr, int algo,
+                           int record_group_times, size_t l2_flush_bytes, int engine_ctas,
+                           const void* h2d_src, void* h2d_dst, size_t h2d_bytes, void* d2h_dst,
+                           const void* d2h_src, size_t d2h_bytes, mgw_pipeline** out) {
+  MGW_TRY {
+    require(p != nullptr && t_b != nullptr && out != nullptr, "bad pipeline arguments");
+    require(h2d_bytes == 0 || (h2d_src != nullptr && h2d_dst != nullptr), "bad h2d buffers");
+    require(d2h_bytes == 0 || (d2h_src != nullptr && d2h_dst != nullptr), "bad d2h buffers");
+    mgw::StepIo io;
+    io.h2d_src = h2d_src;
+    io.h2d_dst = h2d_dst;
+    io.h2d_bytes = h2d_bytes;
+    io.d2h_dst = d2h_dst;
+    io.d2h_src = d2h_src;
+    io.d2h_bytes = d2h_bytes;
+    *out = mgw::build_pipeline(p, t_b, t_f, lr, algo, record_group_times != 0, l2_flush_bytes,
+                               engine_ctas, io);
+  }
+  MGW_CATCH
+}
+
 }  // extern "C"
 
 namespace mgw {
@@ -681,7 +713,7 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
 // engine_ctas != 0: ONE persistent engine kernel (engine_ctas CTAs, < 0 =
 // one per SM) that the replay kernels feed through a device ready counter.
 mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float lr, int algo,
-                             bool timed, size_t l2_flush_bytes, int engine_ctas) {
+                             bool timed, size_t l2_flush_bytes, int engine_ctas, const StepIo& io) {
   {
     require(!p->comm->loopback, "pipelines run on a real communicator");
     require(t_f >= 0.0, "t_f must be >= 0");
@@ -735,6 +767,12 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
     try {
       ck(cudaEventRecord(pipe->fork, pipe->compute), "fork");
       ck(cudaStreamWaitEvent(pipe->comm, pipe->fork, 0), "fork wait");
+      if (io.h2d_bytes > 0) {
+        // the step's input arrives on the comm branch while the compute
+        // stream replays the forward pass; every group kernel follows it
+        ck(cudaMemcpyAsync(io.h2d_dst, io.h2d_src, io.h2d_bytes, cudaMemcpyHostToDevice, pipe->comm),
+           "h2d input");
+      }
       if (pipe->flush_bytes > 0) {
         // The comm stream is idle until the first group is ready: evict L2
         // there while the compute stream replays the forward pass.
@@ -768,6 +806,10 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
       }
       ck(cudaEventRecord(pipe->join, pipe->comm), "join");
       ck(cudaStreamWaitEvent(pipe->compute, pipe->join, 0), "join wait");
+      if (io.d2h_bytes > 0) {
+        ck(cudaMemcpyAsync(io.d2h_dst, io.d2h_src, io.d2h_bytes, cudaMemcpyDeviceToHost, pipe->compute),
+           "d2h result");
+      }
     } catch (...) {
       cudaGraph_t g = nullptr;
       cudaStreamEndCapture(pipe->compute, &g);

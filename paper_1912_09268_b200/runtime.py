@@ -166,16 +166,36 @@ class Pipeline:
     layer is ready, one CUDA graph per iteration."""
 
     def __init__(self, dplan: DevicePlan, trace: ModelTrace, lr: float, algo: str = "auto",
-                 record_group_times: bool = False, l2_flush_bytes: int = 0, engine_ctas: int = -1):
+                 record_group_times: bool = False, l2_flush_bytes: int = 0, engine_ctas: int = -1,
+                 h2d: Optional[Tuple[torch.Tensor, torch.Tensor]] = None,
+                 d2h: Optional[Tuple[torch.Tensor, torch.Tensor]] = None):
         """engine_ctas: -1 persistent comm engine with one CTA per SM, > 0 that
-        many CTAs, 0 = one fused kernel launch per group."""
+        many CTAs, 0 = one fused kernel launch per group.
+        h2d=(pinned_host_src, device_dst) / d2h=(pinned_host_dst, device_src):
+        per-step host I/O captured into the iteration graph (end-to-end runs)."""
         self.dplan = dplan
         self.engine_ctas = engine_ctas
+        self._io = (h2d, d2h)  # keep the buffers alive
         tb = arr(C.c_double, (l.backward_time for l in trace.layers))
         h = C.c_void_p()
-        check(_lib.mgw_pipeline_create(dplan.handle, tb, float(trace.forward_time), lr, ALGO[algo],
-                                       int(record_group_times), int(l2_flush_bytes), int(engine_ctas),
-                                       C.byref(h)))
+        if h2d is None and d2h is None:
+            check(_lib.mgw_pipeline_create(dplan.handle, tb, float(trace.forward_time), lr, ALGO[algo],
+                                           int(record_group_times), int(l2_flush_bytes), int(engine_ctas),
+                                           C.byref(h)))
+        else:
+            hs, hd = h2d if h2d is not None else (None, None)
+            dd, ds = d2h if d2h is not None else (None, None)
+            for t in (hs, dd):
+                if t is not None and not t.is_pinned():
+                    raise ValueError("host buffers of the step I/O must be pinned")
+            nb_in = hs.numel() * hs.element_size() if hs is not None else 0
+            nb_out = dd.numel() * dd.element_size() if dd is not None else 0
+            check(_lib.mgw_pipeline_create_io(
+                dplan.handle, tb, float(trace.forward_time), lr, ALGO[algo], int(record_group_times),
+                int(l2_flush_bytes), int(engine_ctas),
+                hs.data_ptr() if hs is not None else None, hd.data_ptr() if hd is not None else None, nb_in,
+                dd.data_ptr() if dd is not None else None, ds.data_ptr() if ds is not None else None, nb_out,
+                C.byref(h)))
         self.handle = h
         s = C.c_void_p()
         check(_lib.mgw_pipeline_stream(h, C.byref(s)))

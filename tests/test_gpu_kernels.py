@@ -215,3 +215,28 @@ def test_pipeline_p1_replays_backward_and_applies_sgd(engine_ctas):
     pipe.close()
     dp.close()
     comm.close()
+
+
+def test_pipeline_step_io_copies_inputs_and_results():
+    """mgw_pipeline_create_io: the step's gradients arrive H2D inside the
+    graph (before any group kernel) and a result is read back D2H."""
+    counts = [1000, 7, 50000]
+    tr = gs.trace_from_arrays(counts, [1e-4, 1e-4, 2e-4], 5e-4)
+    plan = gs.MergePlan.all_normal(3)
+    flat = torch.zeros(rt.padded_elems(counts), device="cuda")
+    offs = pyoracle.merge_offsets(counts)
+    grads = [flat[offs[i]:offs[i] + c] for i, c in enumerate(counts)]
+    weights = [torch.zeros(c, device="cuda") for c in counts]
+    host_in = torch.ones(flat.numel(), pin_memory=True)
+    host_out = torch.zeros(4, pin_memory=True)
+    comm = rt.Comm(0, 1, 0, 4 * flat.numel())
+    dp = rt.DevicePlan(comm, grads, weights, plan)
+    for engine in (-1, 0):
+        pipe = rt.Pipeline(dp, tr, 0.5, engine_ctas=engine, h2d=(host_in, flat), d2h=(host_out, weights[0][:4]))
+        pipe.run(2)
+        torch.cuda.synchronize()
+        want = -1.0 if engine == -1 else -2.0  # two steps per pipeline, cumulative
+        assert torch.all(weights[2] == want) and torch.all(host_out == want), (engine, host_out)
+        pipe.close()
+    dp.close()
+    comm.close()

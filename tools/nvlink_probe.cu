@@ -52,6 +52,31 @@ __global__ void tma_bulk(char* dst, size_t bytes, float v) {
   }
 }
 
+// local -> remote copy, 4 float4 per thread per step (loads batched before
+// stores); optionally a system fence + __syncthreads every `fence_every`
+// steps (what a barrier per chunk costs).
+__global__ void copy_batched(const float4* __restrict__ src, float4* dst, size_t n_vec, int fence_every) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x * 4;
+  int step = 0;
+  for (size_t base = (size_t)blockIdx.x * blockDim.x * 4 + threadIdx.x; base < n_vec; base += stride) {
+    float4 x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const size_t i = base + (size_t)k * blockDim.x;
+      if (i < n_vec) x[k] = __ldg(src + i);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const size_t i = base + (size_t)k * blockDim.x;
+      if (i < n_vec) dst[i] = x[k];
+    }
+    if (fence_every > 0 && ++step % fence_every == 0) {
+      __threadfence_system();
+      __syncthreads();
+    }
+  }
+}
+
 int main() {
   int n = 0;
   CK(cudaGetDeviceCount(&n));
@@ -83,6 +108,13 @@ int main() {
     const double b = timeit([&] { st32<<<ctas, 512>>>((float4*)dst, bytes / 16, 1.0f); });
     const double c = timeit([&] { tma_bulk<<<ctas, 128>>>((char*)dst, bytes, 1.0f); });
     std::printf("ctas=%3d  st16 %.1f  st32 %.1f  tma_bulk %.1f GB/s\n", ctas, a, b, c);
+  }
+  for (int ctas : {8, 16, 32, 140}) {
+    const double d = timeit([&] { copy_batched<<<ctas, 512>>>((const float4*)src, (float4*)dst, bytes / 16, 0); });
+    const double e = timeit([&] { copy_batched<<<ctas, 512>>>((const float4*)src, (float4*)dst, bytes / 16, 16); });
+    const double f = timeit([&] { copy_batched<<<ctas, 512>>>((const float4*)src, (float4*)dst, bytes / 16, 2); });
+    std::printf("ctas=%3d  copy(ld local, st peer) %.1f  +fence/256KiB %.1f  +fence/32KiB %.1f GB/s\n", ctas, d,
+                e, f);
   }
   CK(cudaGetLastError());
   return 0;
