@@ -118,9 +118,10 @@ __device__ __forceinline__ void epilogue(const Tile& t, uint32_t e, float4 g, fl
 __device__ __forceinline__ void cta_barrier(const RankView& v, int P, uint32_t cta, uint32_t& count,
                                             bool after_remote_stores) {
   ++count;
-  // Every warp's posted NVLink stores must be visible system-wide before
-  // this CTA's flag is: each warp fences its own stores, then bar.sync.
-  if (after_remote_stores) __threadfence_system();
+  // bar.sync orders every warp's posted NVLink stores before the flag
+  // writers' st.release.sys, and release is cumulative at system scope, so
+  // a peer that acquires the flag sees the data (no per-thread fence.sys).
+  (void)after_remote_stores;
   __syncthreads();
   if (threadIdx.x < P) {
     const int q = threadIdx.x;

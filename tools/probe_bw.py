@@ -12,7 +12,8 @@ from paper_1912_09268_b200 import runtime as rt  # noqa: E402
 
 rank, P, local = D.init("nccl")
 dev = torch.device("cuda", local)
-sizes = [int(s) << 20 for s in os.environ.get("SIZES_MB", "1,4,16,64,256").split(",")]
+sizes = ([int(s) << 10 for s in os.environ["SIZES_KB"].split(",")] if "SIZES_KB" in os.environ
+         else [int(s) << 20 for s in os.environ.get("SIZES_MB", "1,4,16,64,256").split(",")])
 comm = rt.Comm(rank, P, local, max(sizes) + (1 << 20))
 f = 2 * (P - 1) / P
 out = []
@@ -48,7 +49,7 @@ for s in sizes:
     nccl.append(tt.item())
 out.append(("nccl", [f * s / tt / 1e9 for s, tt in zip(sizes, nccl)], [tt * 1e6 for tt in nccl]))
 if rank == 0:
-    print(f"P={P} sizes(MiB)={[s >> 20 for s in sizes]}  bus GB/s (time us)")
+    print(f"P={P} sizes(KiB)={[s >> 10 for s in sizes]}  bus GB/s (time us)")
     for name, bw, us in out:
         print(f"  {name:28s}", "  ".join(f"{b:7.1f} ({u:8.1f})" for b, u in zip(bw, us)), flush=True)
 comm.close()
