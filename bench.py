@@ -50,7 +50,7 @@ def parse_args():
     ap.add_argument("--trace", default="googlenet")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot"])
-    ap.add_argument("--oneshot-max", type=int, default=512 * 1024)
+    ap.add_argument("--oneshot-max", type=int, default=0, help="0: the library default for N")
     ap.add_argument("--engine-ctas", type=int, default=-1,
                     help="-1: persistent comm engine, one CTA per SM; >0: that many CTAs; "
                          "0: one fused kernel launch per group")
@@ -266,7 +266,8 @@ def main():
                for c in counts]
 
     comm = rt.Comm(rank, N, local, 4 * max(padded, 1 << 20))
-    comm.set_oneshot_max(args.oneshot_max)
+    if args.oneshot_max > 0:
+        comm.set_oneshot_max(args.oneshot_max)
 
     # ---- N1: on-box calibration of the fused kernel at this N, fitted
     sizes = calibration_sizes(total_bytes, 4 * padded)
@@ -444,7 +445,7 @@ def main():
             "config": {"workload": args.trace, "trace": os.path.relpath(trace_path(args.trace), ROOT),
                        "layers": L, "params": sum(counts), "grad_bytes": total_bytes,
                        "plan": "optimal_plan on on-box calibrated (a, b)", "plan_sha256": digest[:16],
-                       "groups": dplans["mgwfbp"].n_groups, "algo": args.algo, "oneshot_max": args.oneshot_max,
+                       "groups": dplans["mgwfbp"].n_groups, "algo": args.algo, "oneshot_max": comm.oneshot_max,
                        "comm": ("persistent engine, %s CTAs" % ("1/SM" if args.engine_ctas < 0 else args.engine_ctas))
                                if args.engine_ctas else "one fused kernel launch per group",
                        "parallelism": f"dp{N}", "l2": f"flushed every iteration ({args.l2_flush_mib} MiB memset "

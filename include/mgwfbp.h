@@ -174,8 +174,10 @@ enum { MGW_SGD = 1, MGW_WRITE_GRAD = 2 };
 int mgw_group_allreduce(mgw_plan* plan, int group, float lr, int epilogue, int algo,
                         void* stream);
 
-/* One-shot/two-shot crossover (bytes) used by MGW_ALGO_AUTO. */
+/* One-shot/two-shot crossover (bytes) used by MGW_ALGO_AUTO (default: the
+ * B200-measured crossover for the communicator's rank count). */
 int mgw_comm_set_oneshot_max(mgw_comm* comm, uint64_t bytes);
+int mgw_comm_get_oneshot_max(const mgw_comm* comm, uint64_t* bytes);
 
 /* Backward-replay pipeline (paper Algorithm 2): a compute stream spins
  * until each group head's ready time (t_f + backward of the layers above,

@@ -192,6 +192,15 @@ RankView make_view(const mgw_comm* c, int r, float* const* grads, float* const* 
   return v;
 }
 
+// Default one-shot/two-shot crossover, measured on B200 NVLink with the
+// persistent engine (tools/probe_bw.py): one-shot pushes (P-1)*S bytes per
+// rank behind one barrier, two-shot 2(P-1)/P*S behind two.
+uint64_t default_oneshot_max(int nranks) {
+  if (nranks <= 2) return 8ull << 20;
+  if (nranks <= 4) return 3ull << 20;
+  return 1ull << 20;
+}
+
 bool use_two_shot(const mgw_comm* c, uint64_t bytes, int algo) {
   if (c->nranks == 1) return false;
   if (algo == MGW_ALGO_ONESHOT) return false;
@@ -355,6 +364,7 @@ int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_co
     auto* c = new mgw_comm();
     c->rank = rank;
     c->nranks = nranks;
+    c->oneshot_max = mgw::default_oneshot_max(nranks);
     mgw::init_common(c, device, arena_bytes);
     c->arenas.push_back(mgw::alloc_arena(c->arena_elems, nranks));
     c->signals.push_back(mgw::alloc_zero_u32(mgw::kSignalWords));
@@ -374,6 +384,7 @@ int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_com
     require(nranks == 1 || nranks == 2 || nranks == 4 || nranks == 8, "nranks must be 1, 2, 4 or 8");
     auto* c = new mgw_comm();
     c->nranks = nranks;
+    c->oneshot_max = mgw::default_oneshot_max(nranks);
     c->loopback = true;
     mgw::init_common(c, device, arena_bytes);
     for (int r = 0; r < nranks; ++r) {
@@ -427,6 +438,14 @@ int mgw_comm_set_oneshot_max(mgw_comm* c, uint64_t bytes) {
   MGW_TRY {
     require(c != nullptr, "comm is NULL");
     c->oneshot_max = bytes;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_get_oneshot_max(const mgw_comm* c, uint64_t* bytes) {
+  MGW_TRY {
+    require(c != nullptr && bytes != nullptr, "comm / out is NULL");
+    *bytes = c->oneshot_max;
   }
   MGW_CATCH
 }

@@ -66,6 +66,12 @@ class Comm:
     def set_oneshot_max(self, nbytes: int) -> None:
         check(_lib.mgw_comm_set_oneshot_max(self.handle, int(nbytes)))
 
+    @property
+    def oneshot_max(self) -> int:
+        v = C.c_uint64()
+        check(_lib.mgw_comm_get_oneshot_max(self.handle, C.byref(v)))
+        return v.value
+
     def allreduce_(self, buf: torch.Tensor, algo: str = "auto", stream=None) -> torch.Tensor:
         """In-place SUM all-reduce (rank order) of a contiguous fp32 tensor."""
         assert buf.dtype == torch.float32 and buf.is_cuda and buf.is_contiguous()
