@@ -44,19 +44,11 @@ namespace mgw {
 namespace {
 
 constexpr uint64_t kTimeoutNs = 10ull * 1000 * 1000 * 1000;  // 10 s: error, never a hang
-// Software pipelining of the push data path. A CTA walks its tiles in
-// CHUNKS and issues chunk c+1's posted NVLink stores BEFORE chunk c's local
-// HBM work, so the stores drain while the CTA reduces / applies SGD; one
-// barrier per chunk. (Measured on 2x B200, 256 MiB: a non-overlapped
-// barrier per 4-tile chunk cost more than it bought — 296 / 221 GB/s vs
-// 400 / 478 unchunked; the overlap below is what chunks are for, and a
-// chunk is 256 KiB per CTA so barriers stay rare.)
-constexpr uint32_t kOneShotChunk = 16;  // tiles of this CTA per chunk (256 KiB)
-
-template <int P>
-struct TwoShotChunk {  // super-tiles (P tiles each) of this CTA per chunk: 256 KiB
-  static constexpr uint32_t value = 16 / P;
-};
+constexpr int kStages = 4;                           // TMA ring depth (32 KiB stages)
+constexpr uint32_t kStageBytes = kTileElems * 4;
+// Software pipelining: a CTA walks its tiles in CHUNKS; while the producer
+// warp pushes chunk c over NVLink the data warps reduce / apply chunk c-1
+// (c-2); one barrier per chunk.
 
 __device__ __forceinline__ float4 load_tail(const float* p, uint32_t n) {
   float4 v;
@@ -115,13 +107,12 @@ __device__ __forceinline__ void epilogue(const Tile& t, uint32_t e, float4 g, fl
 
 // Barrier of CTA index `cta` with the same CTA index of every rank.
 // `count` is this CTA's barrier counter (same value in every thread).
-__device__ __forceinline__ void cta_barrier(const RankView& v, int P, uint32_t cta, uint32_t& count,
-                                            bool after_remote_stores) {
+// bar.sync orders every warp's posted NVLink stores (and the producer warp's
+// completed, proxy-fenced bulk copies) before the flag writers'
+// st.release.sys; release is cumulative at system scope, so a peer that
+// acquires the flag sees the data (no per-thread fence.sys).
+__device__ __forceinline__ void cta_barrier(const RankView& v, int P, uint32_t cta, uint32_t& count) {
   ++count;
-  // bar.sync orders every warp's posted NVLink stores before the flag
-  // writers' st.release.sys, and release is cumulative at system scope, so
-  // a peer that acquires the flag sees the data (no per-thread fence.sys).
-  (void)after_remote_stores;
   __syncthreads();
   if (threadIdx.x < P) {
     const int q = threadIdx.x;
@@ -154,64 +145,193 @@ __device__ __forceinline__ void store_cta_count(const RankView& v, uint32_t cta,
 // ---- push data path -------------------------------------------------------
 // Every rank's merge arena holds one SLOT per source rank (slot r at element
 // r * slot_stride, laid out like the merge buffer). Transfers are posted
-// NVLink stores into the peers' slots (no remote-load latency on the
+// NVLink writes into the peers' slots (no remote-load latency on the
 // critical path); every reduction reads local HBM only.
+//
+// Warp roles inside a CTA (kBlock = 16 warps):
+//   data warps (threads [0, kThreads))  reduce / SGD / all-gather pushes
+//   producer warp (the last warp)       the gradient pushes, as TMA bulk
+//       copies: lane 0 streams tiles global -> shared (cp.async.bulk +
+//       mbarrier complete_tx) -> the peers' arenas (cp.async.bulk
+//       shared -> global over NVLink), kStages x 32 KiB in flight, no
+//       register traffic. The whole warp handles the rare tiles TMA cannot
+//       (16-byte-unaligned layer views) and the < 4-element layer tails.
+// The gradients are pushed UNSCALED; the receiver multiplies every source
+// by 1/P before the rank-order sum — fl(x * 1/P) is the same value wherever
+// it is computed, so the result is unchanged bit for bit. A rank's own
+// contribution is read straight from its gradients (no self-slot copy).
 
-// Gather + scale tile t of this rank's gradients and store it into slot
-// `me` of the arenas of ranks [q_begin, q_end) — the pack kernel fused with
-// the scatter. kVecPerThread loads are issued before any store.
-template <int P>
-__device__ __forceinline__ void scatter_tile(const RankView& v, const Tile& t, int q_begin, int q_end,
-                                             uint64_t my_slot, float scale) {
-  const float* src = v.grads[t.layer & kLayerMask] + t.src;
-  const bool aligned = !(t.layer & kGradUnaligned);
-  const uint32_t nvec = (t.len + 3) >> 2;
-  float4 x[kVecPerThread];
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Producer state (meaningful in lane 0 of the producer warp only): the next
+// stage of the ring and the phase parity of each stage's mbarrier.
+struct PushRing {
+  uint32_t head;
+  uint32_t phase;  // bit k: parity to wait for on stage k
+};
+
+__device__ __forceinline__ void ring_init(uint64_t* bars) {
 #pragma unroll
-  for (uint32_t k = 0; k < kVecPerThread; ++k) {
-    const uint32_t i = threadIdx.x + k * kThreads;
-    if (i < nvec) {
-      const uint32_t e = i * 4;
-      x[k] = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
-      x[k] = mul4(x[k], scale);
+  for (int k = 0; k < kStages; ++k) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + k)) : "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load(uint32_t stage_addr, const float* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(stage_addr),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store(float* dst, uint32_t stage_addr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(stage_addr), "r"(bytes)
+               : "memory");
+}
+
+// Wait for stage `bar` to reach `parity`; a 10 s timeout raises the error
+// flag instead of hanging.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, uint32_t* err) {
+  uint32_t done = 0;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(done)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  if (done) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (!done && globaltimer_ns() - t0 > kTimeoutNs) {
+      atomicExch(err, 1u);
+      return;
     }
   }
-#pragma unroll
-  for (uint32_t k = 0; k < kVecPerThread; ++k) {
-    const uint32_t i = threadIdx.x + k * kThreads;
-    if (i < nvec) {
+}
+
+// Bulk copies of the tile's 16-byte-aligned body are the TMA's; the rest
+// (unaligned layer view: the whole tile; else the < 4-element tail) goes
+// through registers.
+__device__ __forceinline__ bool tma_able(const Tile& t) {
+  return !(t.layer & kGradUnaligned) && t.len >= 4;
+}
+
+// One push item: a tile and the ranks it goes to.
+struct PushItem {
+  Tile t;
+  uint32_t mask;  // bit q: push into rank q's arena (0: no tile)
+};
+
+// Push the items of one chunk, enumerated by `item(i)`. Producer warp only.
+template <int P, typename Item>
+__device__ __forceinline__ void push_items(const RankView& v, uint32_t n_items, uint64_t my_slot,
+                                           PushRing& ring, uint8_t* stages, uint64_t* bars, Item item) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (lane == 0) {
+    // gradients were written by generic-proxy stores (backward / earlier
+    // kernels, ordered by the ready flag): make them visible to the TMA
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    const uint32_t s0 = smem_u32(stages);
+    uint32_t iL = 0, iS = 0, nl = 0, ns = 0;
+    for (;;) {
+      // prefill kStages loads; then refill the stage of item nl - kStages
+      // once its store group has read it: wait_group.read 1 leaves only the
+      // latest group (item ns - 1) pending, so that needs nl <= ns + kStages - 2
+      while (iL < n_items && (nl < kStages || nl + 2 <= ns + kStages)) {
+        const PushItem it = item(iL++);
+        if (it.mask == 0 || !tma_able(it.t)) continue;
+        if (nl >= kStages) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        const uint32_t k = (ring.head + nl) % kStages;
+        tma_load(s0 + k * kStageBytes, v.grads[it.t.layer & kLayerMask] + it.t.src, (it.t.len & ~3u) * 4u,
+                 smem_u32(bars + k));
+        ++nl;
+      }
+      if (ns == nl) break;
+      PushItem it;
+      do {
+        it = item(iS++);
+      } while (it.mask == 0 || !tma_able(it.t));
+      const uint32_t k = (ring.head + ns) % kStages;
+      mbar_wait(smem_u32(bars + k), (ring.phase >> k) & 1u, v.state + kStateError);
+      ring.phase ^= 1u << k;
+      const uint32_t bytes = (it.t.len & ~3u) * 4u;
 #pragma unroll
       for (int q = 0; q < P; ++q) {
-        if (q >= q_begin && q < q_end) st_v4(v.arena[q] + my_slot + t.moff + i * 4, x[k]);
+        if (it.mask & (1u << q)) tma_store(v.arena[q] + my_slot + it.t.moff, s0 + k * kStageBytes, bytes);
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      ++ns;
+    }
+    ring.head = (ring.head + nl) % kStages;
+  }
+  __syncwarp();
+  // register path: unaligned tiles (whole warp) and tails (lane 0)
+  for (uint32_t i = 0; i < n_items; ++i) {
+    const PushItem it = item(i);
+    if (it.mask == 0 || (tma_able(it.t) && !(it.t.len & 3u))) continue;
+    const float* src = v.grads[it.t.layer & kLayerMask] + it.t.src;
+    const uint32_t first = tma_able(it.t) ? (it.t.len & ~3u) : 0;  // elements the TMA did
+    const uint32_t nvec = (it.t.len - first + 3) >> 2;
+    for (uint32_t j = lane; j < nvec; j += 32) {
+      const uint32_t e = first + j * 4;
+      const float4 x = load_tail(src + e, it.t.len - e);
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        if (it.mask & (1u << q)) st_v4(v.arena[q] + my_slot + it.t.moff + e, x);
       }
     }
   }
 }
 
-// Vectors of a thread reduced per batch: all slot loads of a batch are in
-// flight together (B * P <= 8 float4 per thread keeps the engine at <= 128
-// registers without spills).
+// End of a step for the producer: its bulk copies are complete (written to
+// the peers) and ordered before the generic-proxy flag release.
+__device__ __forceinline__ void push_drain() {
+  if ((threadIdx.x & 31) == 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  __syncwarp();
+}
+
+// Vectors of a thread reduced per batch: all slot, own-gradient and weight
+// loads of a batch are in flight together (one memory latency per batch);
+// B = 2 at P = 2, else 1, keeps the engine within 128 registers, no spills.
 template <int P>
 struct RedBatch {
-  static constexpr uint32_t raw = P >= 4 ? 1 : 4 / P;
+  static constexpr uint32_t raw = P == 2 ? 2 : 1;
   static constexpr uint32_t value = raw < kVecPerThread ? raw : kVecPerThread;
 };
 
-// SGD (+ optional grad write-back) for B vectors of tile t (thread vector
-// indices i0, i0 + stride, ...): the W loads of the whole batch are issued
-// before any store, so their latency overlaps.
+// Weight vectors of B vectors of tile t (thread vector indices i0, i0 +
+// stride, ...), loaded up front so their latency overlaps the gradient loads.
 template <uint32_t B>
-__device__ __forceinline__ void apply_batch(const Tile& t, uint32_t i0, uint32_t stride,
-                                            const float4 (&g)[B], float* w_layer, float* g_layer,
-                                            float lr, int epi) {
+__device__ __forceinline__ void load_w_batch(const Tile& t, uint32_t i0, uint32_t stride, const float* w_layer,
+                                             int epi, float4 (&wv)[B]) {
   const uint32_t nvec = (t.len + 3) >> 2;
   const bool vec_w = (epi & MGW_SGD) && w_layer != nullptr && !(t.layer & kWeightUnaligned);
-  float4 wv[B];
 #pragma unroll
   for (uint32_t j = 0; j < B; ++j) {
     const uint32_t i = i0 + j * stride;
     if (vec_w && i < nvec && i * 4 + 4 <= t.len) wv[j] = ld_v4(w_layer + t.src + i * 4);
   }
+}
+
+// SGD (+ optional grad write-back) for the B vectors, with their weights wv
+// from load_w_batch.
+template <uint32_t B>
+__device__ __forceinline__ void apply_batch(const Tile& t, uint32_t i0, uint32_t stride,
+                                            const float4 (&g)[B], const float4 (&wv)[B], float* w_layer,
+                                            float* g_layer, float lr, int epi) {
+  const uint32_t nvec = (t.len + 3) >> 2;
+  const bool vec_w = (epi & MGW_SGD) && w_layer != nullptr && !(t.layer & kWeightUnaligned);
 #pragma unroll
   for (uint32_t j = 0; j < B; ++j) {
     const uint32_t i = i0 + j * stride;
@@ -231,38 +351,46 @@ __device__ __forceinline__ void apply_batch(const Tile& t, uint32_t i0, uint32_t
   }
 }
 
-// Rank-order sum of tile t over the P local slots (x0 + x1 + ... + x_{P-1},
-// each already scaled by 1/P; .cg loads: peers wrote them), B vectors per
-// batch; optionally push each sum into slot `my_slot` of every peer (the
-// two-shot owner's all-gather), then SGD.
+// Rank-order sum of tile t: x_r from slot r of the local arena (.cg loads:
+// peers wrote them) and this rank's own gradients, each times 1/P, summed
+// x0 + x1 + ... + x_{P-1}; B vectors per batch; optionally push each sum
+// into slot `my_slot` of every peer (the two-shot owner's all-gather), then
+// SGD. Data warps only.
 template <int P>
 __device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, uint64_t slot_stride,
-                                            bool push_to_peers, uint64_t my_slot, float lr, int epi) {
+                                            bool push_to_peers, uint64_t my_slot, float scale, float lr,
+                                            int epi) {
   constexpr uint32_t B = RedBatch<P>::value;
   const float* base = v.arena[v.rank] + t.moff;
   const uint32_t nvec = (t.len + 3) >> 2;
   const uint32_t layer = t.layer & kLayerMask;
   float* w = v.weights[layer];
   float* g = v.grads[layer];
+  const float* own = g + t.src;
+  const bool own_aligned = !(t.layer & kGradUnaligned);
 #pragma unroll 1
   for (uint32_t k0 = 0; k0 < kVecPerThread; k0 += B) {
     const uint32_t i0 = threadIdx.x + k0 * kThreads;
     if (i0 >= nvec) break;
     float4 x[B][P];
+    float4 wv[B];
 #pragma unroll
     for (uint32_t j = 0; j < B; ++j) {
       const uint32_t i = i0 + j * kThreads;
       if (i < nvec) {
+        const uint32_t e = i * 4;
+        const float4 o = (own_aligned && e + 4 <= t.len) ? ld_stream_v4(own + e) : load_tail(own + e, t.len - e);
 #pragma unroll
-        for (int r = 0; r < P; ++r) x[j][r] = ld_cg_v4(base + r * slot_stride + i * 4);
+        for (int r = 0; r < P; ++r) x[j][r] = ld_cg_v4_or(base + r * slot_stride + e, r != v.rank, o);
       }
     }
+    load_w_batch<B>(t, i0, kThreads, w, epi, wv);
     float4 s[B];
 #pragma unroll
     for (uint32_t j = 0; j < B; ++j) {
-      s[j] = x[j][0];
+      s[j] = mul4(x[j][0], scale);
 #pragma unroll
-      for (int r = 1; r < P; ++r) s[j] = add4(s[j], x[j][r]);
+      for (int r = 1; r < P; ++r) s[j] = add4(s[j], mul4(x[j][r], scale));
     }
     if (push_to_peers) {
 #pragma unroll
@@ -275,107 +403,123 @@ __device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, ui
         }
       }
     }
-    apply_batch<B>(t, i0, kThreads, s, w, g, lr, epi);
+    apply_batch<B>(t, i0, kThreads, s, wv, w, g, lr, epi);
   }
 }
 
+// Everything a CTA needs to run groups: its barrier counter and, for the
+// producer warp, the TMA ring.
+struct CtaCtx {
+  uint32_t count;
+  PushRing ring;
+  uint8_t* stages;
+  uint64_t* bars;
+  bool producer;
+};
+
 // One-shot, pipelined over chunks of this CTA's tiles (cta + j*ncta):
-//   push(0); barrier; for c: push(c+1); reduce+SGD(c); barrier (if c+1<n)
-// push = gather x 1/P into slot `me` of every rank; reduce = rank-order sum
-// of the P local slots. NVLink: (P-1) * S posted writes per rank.
+//   step t: producer pushes chunk t to every peer (TMA) | data warps reduce
+//   + SGD chunk t-1 from the local slots; barrier (if t < n).
+// NVLink: (P-1) * S posted writes per rank.
 template <int P>
 __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* tiles,
                                                uint32_t n_tiles, uint64_t slot_stride, float scale,
                                                float lr, int epi, uint32_t cta, uint32_t ncta,
-                                               uint32_t& count) {
+                                               uint32_t chunk, CtaCtx& cx) {
   const uint64_t my_slot = static_cast<uint64_t>(v.rank) * slot_stride;
   const uint32_t mine = cta < n_tiles ? (n_tiles - cta + ncta - 1) / ncta : 0;  // my tiles
-  const uint32_t n_chunks = (mine + kOneShotChunk - 1) / kOneShotChunk;
-  auto push = [&](uint32_t c) {
-#pragma unroll 1
-    for (uint32_t j = c * kOneShotChunk; j < mine && j < (c + 1) * kOneShotChunk; ++j) {
-      scatter_tile<P>(v, tiles[cta + j * ncta], 0, P, my_slot, scale);
-    }
-  };
-  // step t: push(t) [t < n], reduce+SGD(t-1) [t >= 1], barrier [t < n]
+  const uint32_t C = chunk;
+  const uint32_t n_chunks = (mine + C - 1) / C;
+  const uint32_t peers = ((1u << P) - 1u) & ~(1u << v.rank);
 #pragma unroll 1
   for (uint32_t t = 0; t <= n_chunks && n_chunks > 0; ++t) {
-    if (t < n_chunks) push(t);
-    if (t >= 1) {
+    if (cx.producer) {
+      if (t < n_chunks) {
+        const uint32_t j0 = t * C;
+        const uint32_t n = mine - j0 < C ? mine - j0 : C;
+        push_items<P>(v, n, my_slot, cx.ring, cx.stages, cx.bars, [&](uint32_t i) {
+          return PushItem{tiles[cta + (j0 + i) * ncta], peers};
+        });
+        push_drain();
+      }
+    } else if (t >= 1) {
 #pragma unroll 1
-      for (uint32_t j = (t - 1) * kOneShotChunk; j < mine && j < t * kOneShotChunk; ++j) {
-        reduce_tile<P>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, lr, epi);
+      for (uint32_t j = (t - 1) * C; j < mine && j < t * C; ++j) {
+        reduce_tile<P>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, scale, lr, epi);
       }
     }
-    if (t < n_chunks) cta_barrier(v, P, cta, count, true);
+    if (t < n_chunks) cta_barrier(v, P, cta, cx.count);
   }
 }
 
 // Two-shot: super-tile s = tiles [s*P, s*P+P), tile s*P+q owned by rank q.
-//   RS(c):  push each tile of chunk c to its owner's slot `me`
-//   RA(c):  owner: rank-order sum of its tile's P local slots, SGD, push the
-//           result into slot `owner` of every peer (all-gather)
+//   RS(c):  push each tile of chunk c to its owner's slot `me` (producer, TMA)
+//   RA(c):  owner: rank-order sum of its tile, SGD, push the result into
+//           slot `owner` of every peer (all-gather)
 //   AP(c):  apply the other owners' results from the local slots (SGD)
-// Pipelined: RS(0); bar; RA(0); RS(1); bar; for c: RA(c+1); RS(c+2); AP(c);
-// bar (if c+1<n). NVLink: 2 (P-1)/P * S posted writes per rank.
+// step t: RS(t) [producer] | RA(t-1), AP(t-2) [data warps]; barrier (t <= n).
+// NVLink: 2 (P-1)/P * S posted writes per rank.
 template <int P>
 __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* tiles,
                                                uint32_t n_tiles, uint64_t slot_stride, float scale,
                                                float lr, int epi, uint32_t cta, uint32_t ncta,
-                                               uint32_t& count) {
-  constexpr uint32_t C = TwoShotChunk<P>::value;
+                                               uint32_t chunk, CtaCtx& cx) {
+  const uint32_t C = chunk > P ? chunk / P : 1;
   const uint64_t my_slot = static_cast<uint64_t>(v.rank) * slot_stride;
   const uint32_t n_super = (n_tiles + P - 1) / P;
   const uint32_t mine = cta < n_super ? (n_super - cta + ncta - 1) / ncta : 0;  // my super-tiles
   const uint32_t n_chunks = (mine + C - 1) / C;
-  auto rs = [&](uint32_t c) {
-#pragma unroll 1
-    for (uint32_t j = c * C; j < mine && j < (c + 1) * C; ++j) {
-      const uint32_t s = cta + j * ncta;
-#pragma unroll 1
-      for (int q = 0; q < P; ++q) {
-        const uint32_t ti = s * P + q;
-        if (ti < n_tiles) scatter_tile<P>(v, tiles[ti], q, q + 1, my_slot, scale);
-      }
-    }
-  };
-  auto ra = [&](uint32_t c) {
-#pragma unroll 1
-    for (uint32_t j = c * C; j < mine && j < (c + 1) * C; ++j) {
-      const uint32_t ti = (cta + j * ncta) * P + v.rank;
-      if (ti < n_tiles) reduce_tile<P>(v, tiles[ti], slot_stride, true, my_slot, lr, epi);
-    }
-  };
-  auto ap = [&](uint32_t c) {
-#pragma unroll 1
-    for (uint32_t j = c * C; j < mine && j < (c + 1) * C; ++j) {
-      const uint32_t s = cta + j * ncta;
-#pragma unroll 1
-      for (int q = 0; q < P; ++q) {
-        const uint32_t ti = s * P + q;
-        if (q == v.rank || ti >= n_tiles) continue;
-        const Tile t = tiles[ti];
-        const float* red = v.arena[v.rank] + static_cast<uint64_t>(q) * slot_stride + t.moff;
-        const uint32_t layer = t.layer & kLayerMask;
-        const uint32_t nvec = (t.len + 3) >> 2;
-        float4 x[kVecPerThread];
-#pragma unroll
-        for (uint32_t k = 0; k < kVecPerThread; ++k) {
-          const uint32_t i = threadIdx.x + k * kThreads;
-          if (i < nvec) x[k] = ld_cg_v4(red + i * 4);
-        }
-        apply_batch<kVecPerThread>(t, threadIdx.x, kThreads, x, v.weights[layer], v.grads[layer], lr, epi);
-      }
-    }
-  };
-  // step t: RA(t-1) [1 <= t <= n], RS(t) [t < n], AP(t-2) [t >= 2],
-  // barrier [t <= n] (covers the posted stores of RS(t) and RA(t-1))
+  const int me = v.rank;
 #pragma unroll 1
   for (uint32_t t = 0; t <= n_chunks + 1 && n_chunks > 0; ++t) {
-    if (t >= 1 && t <= n_chunks) ra(t - 1);
-    if (t < n_chunks) rs(t);
-    if (t >= 2) ap(t - 2);
-    if (t <= n_chunks) cta_barrier(v, P, cta, count, true);
+    if (cx.producer) {
+      if (t < n_chunks) {
+        const uint32_t j0 = t * C;
+        const uint32_t ns = mine - j0 < C ? mine - j0 : C;
+        push_items<P>(v, ns * (P - 1), my_slot, cx.ring, cx.stages, cx.bars,
+                      [&](uint32_t i) {
+                        const uint32_t s = cta + (j0 + i / (P - 1)) * ncta;
+                        const int qi = static_cast<int>(i % (P - 1));
+                        const int q = qi < me ? qi : qi + 1;
+                        const uint32_t ti = s * P + q;
+                        return ti < n_tiles ? PushItem{tiles[ti], 1u << q} : PushItem{Tile{}, 0u};
+                      });
+        push_drain();
+      }
+    } else {
+      if (t >= 1 && t <= n_chunks) {  // RA(t-1)
+#pragma unroll 1
+        for (uint32_t j = (t - 1) * C; j < mine && j < t * C; ++j) {
+          const uint32_t ti = (cta + j * ncta) * P + me;
+          if (ti < n_tiles) reduce_tile<P>(v, tiles[ti], slot_stride, true, my_slot, scale, lr, epi);
+        }
+      }
+      if (t >= 2) {  // AP(t-2)
+#pragma unroll 1
+        for (uint32_t j = (t - 2) * C; j < mine && j < (t - 1) * C; ++j) {
+          const uint32_t s = cta + j * ncta;
+#pragma unroll 1
+          for (int q = 0; q < P; ++q) {
+            const uint32_t ti = s * P + q;
+            if (q == me || ti >= n_tiles) continue;
+            const Tile tl = tiles[ti];
+            const float* red = v.arena[me] + static_cast<uint64_t>(q) * slot_stride + tl.moff;
+            const uint32_t layer = tl.layer & kLayerMask;
+            const uint32_t nvec = (tl.len + 3) >> 2;
+            float4 x[kVecPerThread], wv[kVecPerThread];
+#pragma unroll
+            for (uint32_t k = 0; k < kVecPerThread; ++k) {
+              const uint32_t i = threadIdx.x + k * kThreads;
+              if (i < nvec) x[k] = ld_cg_v4(red + i * 4);
+            }
+            load_w_batch<kVecPerThread>(tl, threadIdx.x, kThreads, v.weights[layer], epi, wv);
+            apply_batch<kVecPerThread>(tl, threadIdx.x, kThreads, x, wv, v.weights[layer], v.grads[layer], lr,
+                                       epi);
+          }
+        }
+      }
+    }
+    if (t <= n_chunks) cta_barrier(v, P, cta, cx.count);
   }
 }
 
@@ -384,7 +528,7 @@ template <int P>
 __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, const Tile* tiles,
                                           uint32_t n_tiles, uint64_t slot_stride, float scale,
                                           float lr, int epi, uint32_t cta, uint32_t ncta,
-                                          uint32_t& count) {
+                                          uint32_t chunk, CtaCtx& cx) {
   if constexpr (P == 1) {
     // Single rank: no exchange. grad x 1/P (= 1) straight into the epilogue.
     for (uint32_t ti = cta; ti < n_tiles; ti += ncta) {
@@ -402,40 +546,54 @@ __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, cons
       }
     }
   } else if (two_shot) {
-    two_shot_group<P>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, count);
+    two_shot_group<P>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, chunk, cx);
   } else {
-    one_shot_group<P>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, count);
+    one_shot_group<P>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, chunk, cx);
+  }
+}
+
+// Per-CTA set-up: barrier counter, TMA ring (P > 1).
+template <int P>
+__device__ __forceinline__ void cta_ctx_init(CtaCtx& cx, const RankView& v, uint8_t* dsmem, uint64_t* bars) {
+  cx.producer = threadIdx.x >= kThreads;
+  cx.stages = dsmem;
+  cx.bars = bars;
+  cx.ring.head = 0;
+  cx.ring.phase = 0;
+  cx.count = 0;
+  if constexpr (P > 1) {
+    if (threadIdx.x == kThreads) ring_init(bars);
+    cx.count = load_cta_count(v, blockIdx.x);  // (its __syncthreads also publishes the ring init)
+    // entry: peers have left every older launch before any push
+    cta_barrier(v, P, blockIdx.x, cx.count);
+  } else {
+    __syncthreads();
   }
 }
 
 template <int P, bool TWO_SHOT, bool LOOPBACK>
-__global__ void __launch_bounds__(kThreads, 1)
-    group_allreduce_kernel(const __grid_constant__ GroupLaunch L) {
+__global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid_constant__ GroupLaunch L) {
+  extern __shared__ __align__(1024) uint8_t dsmem[];
+  __shared__ __align__(8) uint64_t bars[kStages];
   const RankView& v = L.views[LOOPBACK ? blockIdx.y : 0];
-  uint32_t count = 0;
-  if constexpr (P > 1) {
-    count = load_cta_count(v, blockIdx.x);
-    cta_barrier(v, P, blockIdx.x, count, false);  // entry: peers have left every older launch
-  }
+  CtaCtx cx;
+  cta_ctx_init<P>(cx, v, dsmem, bars);
   run_group<P>(TWO_SHOT, v, L.tiles, L.n_tiles, L.slot_stride, L.scale, L.lr, L.epilogue,
-               blockIdx.x, gridDim.x, count);
-  if constexpr (P > 1) store_cta_count(v, blockIdx.x, count);
+               blockIdx.x, gridDim.x, L.chunk, cx);
+  if constexpr (P > 1) store_cta_count(v, blockIdx.x, cx.count);
 }
 
 template <int P>
-__global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineLaunch E) {
+__global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant__ EngineLaunch E) {
+  extern __shared__ __align__(1024) uint8_t dsmem[];
+  __shared__ __align__(8) uint64_t bars[kStages];
   const RankView& v = E.v;
   __shared__ uint32_t s_iter;
   if (threadIdx.x == 0) s_iter = ld_volatile_u32(E.pipe + 1);
-  uint32_t count = 0;
-  if constexpr (P > 1) {
-    count = load_cta_count(v, blockIdx.x);
-    // Entry barrier (runs while the compute stream replays the forward
-    // pass): every peer has finished every older launch before any push.
-    cta_barrier(v, P, blockIdx.x, count, false);
-  } else {
-    __syncthreads();
-  }
+  // Entry barrier inside (runs while the compute stream replays the forward
+  // pass): every peer has finished every older launch before any push.
+  CtaCtx cx;
+  cta_ctx_init<P>(cx, v, dsmem, bars);
   const uint32_t iter = s_iter;
   for (uint32_t k = 0; k < E.G; ++k) {
     const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
@@ -462,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     }
     __syncthreads();
     run_group<P>(two, v, E.tiles + grp.tile_first, grp.n_tiles, E.slot_stride, E.scale, E.lr,
-                 E.epilogue, blockIdx.x, gridDim.x, count);
+                 E.epilogue, blockIdx.x, gridDim.x, E.chunk, cx);
     if (E.stamps != nullptr) {
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -475,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       }
     }
   }
-  if constexpr (P > 1) store_cta_count(v, blockIdx.x, count);
+  if constexpr (P > 1) store_cta_count(v, blockIdx.x, cx.count);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -580,15 +738,19 @@ __global__ void __launch_bounds__(512) l2_flush_kernel(float4* buf, size_t n_vec
   }
 }
 
+constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes;
+
+constexpr size_t smem_for(int P) { return P > 1 ? kSmemBytes : 0; }
+
 template <int P, bool TWO, bool LB>
 cudaError_t launch_t(const GroupLaunch& L, dim3 grid, cudaStream_t stream) {
   auto* fn = group_allreduce_kernel<P, TWO, LB>;
   if constexpr (LB) {
     void* args[] = {const_cast<GroupLaunch*>(&L)};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), grid, dim3(kThreads), args, 0,
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), grid, dim3(kBlock), args, smem_for(P),
                                        stream);
   } else {
-    fn<<<grid, kThreads, 0, stream>>>(L);
+    fn<<<grid, kBlock, smem_for(P), stream>>>(L);
     return cudaGetLastError();
   }
 }
@@ -614,6 +776,23 @@ const void* engine_fn(int nranks) {
   }
 }
 
+const void* group_fn(int nranks, bool two_shot, bool loopback) {
+#define MGW_PICK(P, TWO, LB) return reinterpret_cast<const void*>(group_allreduce_kernel<P, TWO, LB>)
+  if (loopback) {
+    if (nranks == 1) MGW_PICK(1, false, true);
+    if (nranks == 2) { if (two_shot) MGW_PICK(2, true, true); MGW_PICK(2, false, true); }
+    if (nranks == 4) { if (two_shot) MGW_PICK(4, true, true); MGW_PICK(4, false, true); }
+    if (nranks == 8) { if (two_shot) MGW_PICK(8, true, true); MGW_PICK(8, false, true); }
+  } else {
+    if (nranks == 1) MGW_PICK(1, false, false);
+    if (nranks == 2) { if (two_shot) MGW_PICK(2, true, false); MGW_PICK(2, false, false); }
+    if (nranks == 4) { if (two_shot) MGW_PICK(4, true, false); MGW_PICK(4, false, false); }
+    if (nranks == 8) { if (two_shot) MGW_PICK(8, true, false); MGW_PICK(8, false, false); }
+  }
+#undef MGW_PICK
+  return nullptr;
+}
+
 }  // namespace
 
 cudaError_t launch_group_allreduce(const GroupLaunch& L, int ctas_per_rank, bool two_shot,
@@ -627,31 +806,19 @@ cudaError_t launch_engine(const EngineLaunch& E, int ctas, cudaStream_t stream) 
   const void* fn = engine_fn(E.nranks);
   if (fn == nullptr) return cudaErrorInvalidValue;
   void* args[] = {const_cast<EngineLaunch*>(&E)};
-  return cudaLaunchKernel(fn, dim3(ctas), dim3(kThreads), args, 0, stream);
+  return cudaLaunchKernel(fn, dim3(ctas), dim3(kBlock), args, smem_for(E.nranks), stream);
 }
 
 cudaError_t engine_ctas_per_sm(int nranks, int* out) {
   const void* fn = engine_fn(nranks);
   if (fn == nullptr) return cudaErrorInvalidValue;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kThreads, 0);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kBlock, smem_for(nranks));
 }
 
 cudaError_t max_ctas_per_sm(int nranks, bool two_shot, bool loopback, int* out) {
-  const void* fn = nullptr;
-#define MGW_PICK(P, TWO, LB) fn = reinterpret_cast<const void*>(group_allreduce_kernel<P, TWO, LB>)
-  if (loopback) {
-    if (nranks == 1) MGW_PICK(1, false, true);
-    else if (nranks == 2) { if (two_shot) MGW_PICK(2, true, true); else MGW_PICK(2, false, true); }
-    else if (nranks == 4) { if (two_shot) MGW_PICK(4, true, true); else MGW_PICK(4, false, true); }
-    else { if (two_shot) MGW_PICK(8, true, true); else MGW_PICK(8, false, true); }
-  } else {
-    if (nranks == 1) MGW_PICK(1, false, false);
-    else if (nranks == 2) { if (two_shot) MGW_PICK(2, true, false); else MGW_PICK(2, false, false); }
-    else if (nranks == 4) { if (two_shot) MGW_PICK(4, true, false); else MGW_PICK(4, false, false); }
-    else { if (two_shot) MGW_PICK(8, true, false); else MGW_PICK(8, false, false); }
-  }
-#undef MGW_PICK
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kThreads, 0);
+  const void* fn = group_fn(nranks, two_shot, loopback);
+  if (fn == nullptr) return cudaErrorInvalidValue;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kBlock, smem_for(nranks));
 }
 
 cudaError_t launch_pack(const Tile* tiles, uint32_t n_tiles, float* const* grads, float* merge,
@@ -705,6 +872,16 @@ cudaError_t preload_kernels() {
     cudaFuncAttributes attr;
     const cudaError_t e = cudaFuncGetAttributes(&attr, f);
     if (e != cudaSuccess) return e;
+  }
+  // the TMA ring lives in dynamic shared memory (> the 48 KiB default)
+  for (int p : {2, 4, 8}) {
+    const void* ks[] = {engine_fn(p), group_fn(p, false, false), group_fn(p, true, false),
+                        group_fn(p, false, true), group_fn(p, true, true)};
+    for (const void* f : ks) {
+      const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kSmemBytes));
+      if (e != cudaSuccess) return e;
+    }
   }
   for (bool lb : {false, true}) {
     for (int p : {1, 2, 4, 8}) {

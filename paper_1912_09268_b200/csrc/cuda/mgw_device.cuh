@@ -27,9 +27,10 @@ namespace mgw {
 
 constexpr int kMaxRanks = 8;
 constexpr int kMaxCtas = 1024;           // per-rank CTAs of one collective launch
-constexpr int kThreads = 512;            // threads per CTA of the fused kernel
-constexpr uint32_t kTileElems = 8192;    // 32 KiB of fp32; 4 float4 per thread (memory-level parallelism)
-constexpr uint32_t kVecPerThread = kTileElems / 4 / kThreads;
+constexpr int kBlock = 512;              // threads per CTA of the fused kernel (16 warps, 128 regs)
+constexpr int kThreads = kBlock - 32;    // data threads; the last warp is the TMA producer
+constexpr uint32_t kTileElems = 8192;    // 32 KiB of fp32 (one TMA stage); <= 5 float4 per data thread
+constexpr uint32_t kVecPerThread = (kTileElems / 4 + kThreads - 1) / kThreads;
 constexpr uint32_t kLayerMask = 0x3fffffffu;
 constexpr uint32_t kGradUnaligned = 0x80000000u;
 constexpr uint32_t kWeightUnaligned = 0x40000000u;
@@ -66,6 +67,7 @@ struct GroupLaunch {
   float lr;
   int epilogue;          // MGW_SGD | MGW_WRITE_GRAD
   uint64_t slot_stride;  // elements between the per-source-rank slots of an arena
+  uint32_t chunk;        // tiles per pipelined chunk of one CTA (two-shot: max(1, chunk/P) super-tiles)
   RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
 };
 
@@ -90,6 +92,7 @@ struct EngineLaunch {
   float lr;
   int epilogue;
   uint64_t slot_stride;
+  uint32_t chunk;                // as GroupLaunch::chunk
   uint32_t* pipe;                // [1] iteration, [2] CTA exit count, [3] ready-timeout flag
   const uint32_t* ready;         // G flags: group g ready for iteration i when >= i + 1
   uint32_t* group_done;          // G counters for end stamps (NULL: no timing)
@@ -137,6 +140,17 @@ __device__ __forceinline__ float4 ld_cg_v4(const float* p) {
   asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "l"(p));
+  return v;
+}
+
+// ld_cg_v4(p) when `pred`, else `other` (a predicated load: no branch, no
+// dynamically indexed register array).
+__device__ __forceinline__ float4 ld_cg_v4_or(const float* p, bool pred, float4 other) {
+  float4 v = other;
+  asm volatile(
+      "{ .reg .pred q; setp.ne.u32 q, %5, 0; @q ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4]; }"
+      : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
+      : "l"(p), "r"(static_cast<uint32_t>(pred)));
   return v;
 }
 

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -80,6 +81,7 @@ struct mgw_comm {
   size_t arena_elems = 0;  // per copy
   uint64_t oneshot_max = 512 * 1024;
   int num_sms = 148;
+  uint32_t chunk_tiles = 16;  // pipelined chunk per CTA (MGW_CHUNK_TILES overrides, for probing)
   // own allocations (loopback: one per emulated rank)
   std::vector<float*> arenas;
   std::vector<uint32_t*> signals;
@@ -201,6 +203,12 @@ uint64_t default_oneshot_max(int nranks) {
   return 1ull << 20;
 }
 
+uint32_t default_chunk_tiles() {
+  const char* e = std::getenv("MGW_CHUNK_TILES");
+  const long v = e != nullptr ? std::strtol(e, nullptr, 10) : 0;
+  return v > 0 ? static_cast<uint32_t>(v) : 16u;
+}
+
 bool use_two_shot(const mgw_comm* c, uint64_t bytes, int algo) {
   if (c->nranks == 1) return false;
   if (algo == MGW_ALGO_ONESHOT) return false;
@@ -238,6 +246,7 @@ void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStre
   L.lr = lr;
   L.epilogue = epilogue;
   L.slot_stride = c->arena_elems;
+  L.chunk = c->chunk_tiles;
   for (int r = 0; r < p->n_views; ++r) {
     L.views[r] = make_view(c, r, p->d_grads + static_cast<size_t>(r) * p->L,
                            p->d_weights + static_cast<size_t>(r) * p->L);
@@ -365,6 +374,7 @@ int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_co
     c->rank = rank;
     c->nranks = nranks;
     c->oneshot_max = mgw::default_oneshot_max(nranks);
+    c->chunk_tiles = mgw::default_chunk_tiles();
     mgw::init_common(c, device, arena_bytes);
     c->arenas.push_back(mgw::alloc_arena(c->arena_elems, nranks));
     c->signals.push_back(mgw::alloc_zero_u32(mgw::kSignalWords));
@@ -385,6 +395,7 @@ int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_com
     auto* c = new mgw_comm();
     c->nranks = nranks;
     c->oneshot_max = mgw::default_oneshot_max(nranks);
+    c->chunk_tiles = mgw::default_chunk_tiles();
     c->loopback = true;
     mgw::init_common(c, device, arena_bytes);
     for (int r = 0; r < nranks; ++r) {
@@ -568,6 +579,7 @@ int mgw_allreduce(mgw_comm* c, float* buf, size_t n, int algo, void* stream) {
     L.lr = 0.0f;
     L.epilogue = MGW_WRITE_GRAD;
     L.slot_stride = c->arena_elems;
+    L.chunk = c->chunk_tiles;
     L.views[0] = mgw::make_view(c, 0, p->d_grads, p->d_weights);
     const bool two = mgw::use_two_shot(c, static_cast<uint64_t>(n) * 4, algo);
     ck(mgw::launch_group_allreduce(L, mgw::grid_for(c, L.n_tiles, two), two, false,
@@ -721,6 +733,7 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
   E.lr = lr;
   E.epilogue = MGW_SGD;
   E.slot_stride = c->arena_elems;
+  E.chunk = c->chunk_tiles;
   E.pipe = pipe->d_pipe;
   E.ready = pipe->d_ready;
   E.group_done = timed ? pipe->d_group_done : nullptr;

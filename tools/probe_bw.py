@@ -19,7 +19,7 @@ f = 2 * (P - 1) / P
 out = []
 for algo in os.environ.get("ALGOS", "oneshot,twoshot").split(","):
     for ctas in [int(c) for c in os.environ.get("CTAS", "64,140").split(",")]:
-        m = comm.calibrate_engine(sizes, warmup=1, reps=3, algo=algo, engine_ctas=ctas)
+        m = comm.calibrate_engine(sizes, warmup=2, reps=int(os.environ.get("REPS", "10")), algo=algo, engine_ctas=ctas)
         t = torch.tensor([x.time_sec for x in m], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         out.append((f"engine {algo} ctas={ctas}", [f * s / tt / 1e9 for s, tt in zip(sizes, t.tolist())],
