@@ -272,7 +272,7 @@ def main():
     # ---- N1: on-box calibration of the fused kernel at this N, fitted
     sizes = calibration_sizes(total_bytes, 4 * padded)
     if args.engine_ctas != 0:
-        meas = comm.calibrate_engine(sizes, warmup=2, reps=5, algo=args.algo, engine_ctas=args.engine_ctas)
+        meas = comm.calibrate_engine(sizes, warmup=3, reps=15, algo=args.algo, engine_ctas=args.engine_ctas)
     else:
         meas = comm.calibrate(sizes, warmup=3, reps=15, algo=args.algo)
     tvec = torch.tensor([m.time_sec for m in meas], dtype=torch.float64, device=dev)

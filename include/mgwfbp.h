@@ -250,10 +250,10 @@ int mgw_engine_check(mgw_pipeline* engine);
 int mgw_calibrate(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int warmup, int reps,
                   int algo, mgw_meas* out);
 
-/* Calibration of the persistent comm engine: per size, iterations of an
- * engine over 8 equal groups that are all ready at once; the median
- * per-group device duration (%globaltimer, first CTA start -> last CTA end)
- * is the sample. This is the T(M) the planner sees in engine pipelines. */
+/* Calibration of the persistent comm engine: per size, `reps` iterations of
+ * an engine running ONE group of that size, ready at once; the median group
+ * device duration (%globaltimer, first CTA start -> last CTA end) is the
+ * sample. This is the T(M) the planner sees in engine pipelines. */
 int mgw_calibrate_engine(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int warmup,
                          int reps, int algo, int engine_ctas, mgw_meas* out);
 

@@ -975,7 +975,11 @@ int mgw_calibrate_engine(mgw_comm* c, const uint64_t* sizes, size_t n, int warmu
     uint64_t max_bytes = 16;
     for (size_t i = 0; i < n; ++i) max_bytes = std::max(max_bytes, sizes[i]);
     const size_t max_elems = (max_bytes + 3) / 4;
-    constexpr int kGroups = 8;  // groups per calibration iteration (all ready at t = 0)
+    // ONE group per iteration, ready at t = 0: the planner's cost T(M) is a
+    // group's time on an idle engine (back-to-back groups overlap at CTA
+    // granularity, which made per-group stamps of a multi-group iteration
+    // unreliable at large sizes).
+    constexpr int kGroups = 1;
     float* grad = nullptr;
     float* w = nullptr;
     ck(cudaMalloc(&grad, max_elems * sizeof(float)), "cudaMalloc(calib grad)");

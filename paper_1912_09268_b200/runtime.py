@@ -89,7 +89,7 @@ class Comm:
     def calibrate_engine(self, sizes: Sequence[int], warmup: int = 2, reps: int = 5,
                          algo: str = "auto", engine_ctas: int = -1) -> List[CommMeasurement]:
         """N1 for engine pipelines: median per-group device time in the
-        persistent comm engine (8 equal groups, all ready at once)."""
+        persistent comm engine (one group per iteration, ready at once)."""
         out = (_lib.Meas * len(sizes))()
         check(_lib.mgw_calibrate_engine(self.handle, arr(C.c_uint64, sizes), len(sizes), warmup, reps,
                                         ALGO[algo], engine_ctas, out))
