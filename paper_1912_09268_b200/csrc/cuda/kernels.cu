@@ -59,16 +59,26 @@ __device__ __forceinline__ float4 load_tail(const float* p, uint32_t n) {
   return v;
 }
 
+// Standalone pack of tile t: gather + x scale into the merge buffer; each
+// thread has all its kPackVec loads in flight before any store.
+constexpr uint32_t kPackVec = kTileElems / 4 / kBlock;
 __device__ __forceinline__ void pack_tile(const Tile& t, float* const* grads, float* dst_base,
                                           float scale) {
   const float* src = grads[t.layer & kLayerMask] + t.src;
   float* dst = dst_base + t.moff;
   const bool aligned = !(t.layer & kGradUnaligned);
   const uint32_t nvec = (t.len + 3) >> 2;
-  for (uint32_t i = threadIdx.x; i < nvec; i += blockDim.x) {
+  float4 x[kPackVec];
+#pragma unroll
+  for (uint32_t k = 0; k < kPackVec; ++k) {
+    const uint32_t i = threadIdx.x + k * kBlock;
     const uint32_t e = i * 4;
-    const float4 x = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
-    st_v4(dst + e, mul4(x, scale));
+    if (i < nvec) x[k] = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < kPackVec; ++k) {
+    const uint32_t i = threadIdx.x + k * kBlock;
+    if (i < nvec) st_v4(dst + i * 4, mul4(x[k], scale));
   }
 }
 
@@ -530,7 +540,9 @@ __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, cons
                                           float lr, int epi, uint32_t cta, uint32_t ncta,
                                           uint32_t chunk, CtaCtx& cx) {
   if constexpr (P == 1) {
-    // Single rank: no exchange. grad x 1/P (= 1) straight into the epilogue.
+    // Single rank: no exchange. grad x 1/P (= 1) straight into the epilogue;
+    // all kB gradient and weight loads of a thread are in flight together.
+    constexpr uint32_t kB = kTileElems / 4 / kBlock;
     for (uint32_t ti = cta; ti < n_tiles; ti += ncta) {
       const Tile t = tiles[ti];
       const uint32_t layer = t.layer & kLayerMask;
@@ -539,11 +551,17 @@ __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, cons
       float* g = v.grads[layer];
       const bool aligned = !(t.layer & kGradUnaligned);
       const uint32_t nvec = (t.len + 3) >> 2;
-      for (uint32_t i = threadIdx.x; i < nvec; i += blockDim.x) {
+      float4 x[kB], wv[kB];
+#pragma unroll
+      for (uint32_t k = 0; k < kB; ++k) {
+        const uint32_t i = threadIdx.x + k * kBlock;
         const uint32_t e = i * 4;
-        const float4 x = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
-        epilogue(t, e, mul4(x, scale), w, g, lr, epi);
+        if (i < nvec) x[k] = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
       }
+      load_w_batch<kB>(t, threadIdx.x, kBlock, w, epi, wv);
+#pragma unroll
+      for (uint32_t k = 0; k < kB; ++k) x[k] = mul4(x[k], scale);
+      apply_batch<kB>(t, threadIdx.x, kBlock, x, wv, w, g, lr, epi);
     }
   } else if (two_shot) {
     two_shot_group<P>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, chunk, cx);
@@ -645,9 +663,8 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
   }
 }
 
-__global__ void __launch_bounds__(kThreads) pack_kernel(const Tile* tiles, uint32_t n_tiles,
-                                                         float* const* grads, float* merge,
-                                                         uint64_t begin, float scale) {
+__global__ void __launch_bounds__(kBlock) pack_kernel(const Tile* tiles, uint32_t n_tiles, float* const* grads,
+                                                       float* merge, uint64_t begin, float scale) {
   for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
     Tile t = tiles[ti];
     t.moff = static_cast<uint32_t>(t.moff - begin);
@@ -655,11 +672,10 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const Tile* tiles, uint3
   }
 }
 
-__global__ void __launch_bounds__(kThreads) unpack_sgd_kernel(const Tile* tiles, uint32_t n_tiles,
-                                                               float* const* grads,
-                                                               float* const* weights,
-                                                               const float* merge, uint64_t begin,
-                                                               float lr, int epi) {
+__global__ void __launch_bounds__(kBlock) unpack_sgd_kernel(const Tile* tiles, uint32_t n_tiles,
+                                                             float* const* grads, float* const* weights,
+                                                             const float* merge, uint64_t begin, float lr,
+                                                             int epi) {
   for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
     const Tile t = tiles[ti];
     const uint32_t layer = t.layer & kLayerMask;
@@ -667,9 +683,14 @@ __global__ void __launch_bounds__(kThreads) unpack_sgd_kernel(const Tile* tiles,
     float* w = weights[layer];
     float* g = grads[layer];
     const uint32_t nvec = (t.len + 3) >> 2;
-    for (uint32_t i = threadIdx.x; i < nvec; i += blockDim.x) {
-      epilogue(t, i * 4, ld_v4(red + i * 4), w, g, lr, epi);
+    float4 x[kPackVec], wv[kPackVec];
+#pragma unroll
+    for (uint32_t k = 0; k < kPackVec; ++k) {
+      const uint32_t i = threadIdx.x + k * kBlock;
+      if (i < nvec) x[k] = ld_v4(red + i * 4);
     }
+    load_w_batch<kPackVec>(t, threadIdx.x, kBlock, w, epi, wv);
+    apply_batch<kPackVec>(t, threadIdx.x, kBlock, x, wv, w, g, lr, epi);
   }
 }
 
@@ -823,14 +844,14 @@ cudaError_t max_ctas_per_sm(int nranks, bool two_shot, bool loopback, int* out) 
 
 cudaError_t launch_pack(const Tile* tiles, uint32_t n_tiles, float* const* grads, float* merge,
                         uint64_t begin, float scale, int ctas, cudaStream_t stream) {
-  pack_kernel<<<ctas, kThreads, 0, stream>>>(tiles, n_tiles, grads, merge, begin, scale);
+  pack_kernel<<<ctas, kBlock, 0, stream>>>(tiles, n_tiles, grads, merge, begin, scale);
   return cudaGetLastError();
 }
 
 cudaError_t launch_unpack_sgd(const Tile* tiles, uint32_t n_tiles, float* const* grads,
                               float* const* weights, const float* merge, uint64_t begin, float lr,
                               int epi, int ctas, cudaStream_t stream) {
-  unpack_sgd_kernel<<<ctas, kThreads, 0, stream>>>(tiles, n_tiles, grads, weights, merge, begin,
+  unpack_sgd_kernel<<<ctas, kBlock, 0, stream>>>(tiles, n_tiles, grads, weights, merge, begin,
                                                    lr, epi);
   return cudaGetLastError();
 }
