@@ -57,6 +57,9 @@ def parse_args():
     ap.add_argument("--l2-flush-mib", type=int, default=256)
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--model", default="",
+                    help="A_US,B_PS_PER_BYTE: skip the calibration and plan with this (a, b) "
+                         "(ncu runs, where a calibration under kernel serialisation is meaningless)")
     return ap.parse_args()
 
 
@@ -271,6 +274,9 @@ def main():
 
     # ---- N1: on-box calibration of the fused kernel at this N, fitted
     sizes = calibration_sizes(total_bytes, 4 * padded)
+    if args.model:
+        a_us, b_ps = (float(x) for x in args.model.split(","))
+        sizes = sizes[:2]  # (a short sweep still exercises the calibration kernels)
     if args.engine_ctas != 0:
         meas = comm.calibrate_engine(sizes, warmup=3, reps=15, algo=args.algo, engine_ctas=args.engine_ctas)
     else:
@@ -280,6 +286,8 @@ def main():
         torch.distributed.all_reduce(tvec, op=torch.distributed.ReduceOp.MAX)
     meas = [gs.CommMeasurement(m.size_bytes, float(t)) for m, t in zip(meas, tvec.tolist())]
     model, fit_how = fit_with_fallback(gs, meas)
+    if args.model:
+        model, fit_how = gs.AllReduceModel(a_us * 1e-6, b_ps * 1e-12), "given by --model (not calibrated)"
     out_dir = os.environ.get("MGW_OUT_DIR")
     if out_dir and rank == 0:
         os.makedirs(out_dir, exist_ok=True)
