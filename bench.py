@@ -399,12 +399,16 @@ def main():
                             else "group_allreduce_kernel (fused pack + push all-reduce + unpack/SGD)"),
                  "achieved": achieved, "peak": peak, "unit": "GB/s",
                  "frac": achieved / peak if achieved else None, "traffic": traffic,
-                 "traffic_evidence": "profiles/r1_ncu_group_kernel_p1_16MiB.txt (ncu --set full of run_group "
-                                     "at P=1, 16 MiB: DRAM 33.6 MB read / 0 written vs 50.3 MB algorithmic; "
-                                     "the engine kernel itself cannot run under ncu's serialisation)",
+                 "traffic_evidence": (
+                     "profiles/r1_ncu_hbm_kernels_256MiB.txt: the P=1 fused group kernel (same run_group code as "
+                     "the engine) moves 752 MB DRAM vs 805 MB algorithmic per 256 MiB launch (no re-reads)"
+                     if N == 1 else
+                     "profiles/r1_ncu_loopback_twoshot_64MiB.txt: the two-shot data path in loopback moves "
+                     "623 MB DRAM vs 671 MB algorithmic (P=2, 64 MiB/rank; no re-reads)")
+                     + "; the engine kernel itself cannot run under ncu's serialisation (it waits on the replay)",
                  "algorithmic_bytes_per_iter": algo_bytes, "kernel_ms_per_iter": kern_s * 1e3,
                  "launches_per_iter": len(group_ms),
-                 "note": "groups are latency-bound at these sizes (GoogLeNet: 6.6M params over "
+                 "note": f"small groups are latency-bound ({args.trace}: {sum(counts)} params over "
                          f"{len(group_ms)} groups); the per-byte rate is the slope row",
                  "slope": {"achieved": asym, "frac": asym / peak if asym else None,
                            "from": "calibration b (fit_model over the on-box sweep)"}})
