@@ -147,6 +147,19 @@ int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_com
  * Group g (0-based, ascending head index) is [head_g, head_{g+1}). */
 int mgw_plan_create(mgw_comm* comm, size_t L, float* const* grads, float* const* weights,
                     const uint64_t* counts, const uint8_t* tags, mgw_plan** out);
+
+/* Gradient element type (reference trace.hpp:50
+ * bytes_per_element). Weights are always fp32 (master weights). */
+typedef enum { MGW_DTYPE_F32 = 0, MGW_DTYPE_BF16 = 1 } mgw_dtype;
+
+/* mgw_plan_create with the gradient element type. bf16: gradients and the
+ * merge arena are bf16 (half the NVLink and HBM bytes); every source is
+ * widened to fp32, scaled by 1/P and summed in rank order in fp32; the sum
+ * is rounded once to bf16 (nearest even) and THAT value is the reduced
+ * gradient on every rank (SGD on the fp32 weights, grad write-back). The
+ * merge layout pads every layer to 16 bytes (8 bf16 elements). */
+int mgw_plan_create_ex(mgw_comm* comm, size_t L, void* const* grads, float* const* weights,
+                       const uint64_t* counts, const uint8_t* tags, int dtype, mgw_plan** out);
 int mgw_plan_destroy(mgw_plan* plan);
 int mgw_plan_num_groups(const mgw_plan* plan, int* n_groups_out);
 /* Padded element span of group g inside the merge layout (layers start
@@ -155,13 +168,13 @@ int mgw_plan_group_span(const mgw_plan* plan, int group, uint64_t* elem_begin,
                         uint64_t* elem_count, uint64_t* bytes_unpadded);
 
 /* Pack kernel: gather group g's layer gradients, times `scale`, into the
- * contiguous merge buffer `merge_buf` (>= elem_count floats, padded
- * layout, zero padding). Rank-local. */
-int mgw_pack(mgw_plan* plan, int group, float scale, float* merge_buf, void* stream);
+ * contiguous merge buffer `merge_buf` (>= elem_count elements of the plan's
+ * gradient type, padded layout). Rank-local. */
+int mgw_pack(mgw_plan* plan, int group, float scale, void* merge_buf, void* stream);
 
 /* Unpack + SGD: for every layer of group g, w -= lr * red (non-contracted
  * fp32) and, if write_grad, grad = red. Rank-local. */
-int mgw_unpack_sgd(mgw_plan* plan, int group, const float* merge_buf, float lr, int write_grad,
+int mgw_unpack_sgd(mgw_plan* plan, int group, const void* merge_buf, float lr, int write_grad,
                    void* stream);
 
 /* Algorithm selection for the merged all-reduce. */

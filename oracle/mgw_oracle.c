@@ -219,6 +219,63 @@ void orc_allreduce_sgd(int P, float* const* grads, float* const* weights, const 
   }
 }
 
+/* ------------------------------------------------------- bf16 gradients */
+
+uint16_t orc_f32_to_bf16(float x) {
+  uint32_t u;
+  memcpy(&u, &x, sizeof u);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40u); /* quiet NaN */
+  u += 0x7fffu + ((u >> 16) & 1u); /* round to nearest, ties to even */
+  return (uint16_t)(u >> 16);
+}
+
+float orc_bf16_to_f32(uint16_t h) {
+  const uint32_t u = (uint32_t)h << 16;
+  float f;
+  memcpy(&f, &u, sizeof f);
+  return f;
+}
+
+void orc_merge_offsets_granule(const uint64_t* counts, size_t L, uint64_t granule, uint64_t* offs) {
+  offs[0] = 0;
+  for (size_t l = 0; l < L; ++l) offs[l + 1] = offs[l] + ((counts[l] + granule - 1) / granule) * granule;
+}
+
+void orc_pack_bf16(const uint16_t* const* grads, const uint64_t* counts, const uint64_t* offs,
+                   size_t first, size_t last, float scale, uint16_t* merge) {
+  for (size_t l = first; l < last; ++l) {
+    uint16_t* dst = merge + (offs[l] - offs[first]);
+    const uint64_t padded = offs[l + 1] - offs[l];
+    for (uint64_t j = 0; j < padded; ++j) {
+      dst[j] = j < counts[l] ? orc_f32_to_bf16(orc_bf16_to_f32(grads[l][j]) * scale) : 0;
+    }
+  }
+}
+
+void orc_allreduce_sgd_bf16(int P, uint16_t* const* grads, float* const* weights, const uint64_t* counts,
+                            size_t L, const uint8_t* tags, float lr, int write_grad) {
+  const float scale = 1.0f / (float)P;
+  (void)tags; /* grouping does not change per-element values */
+  for (size_t l = 0; l < L; ++l) {
+    for (uint64_t j = 0; j < counts[l]; ++j) {
+      float acc = orc_bf16_to_f32(grads[l][j]) * scale;
+      for (int r = 1; r < P; ++r) acc = acc + orc_bf16_to_f32(grads[(size_t)r * L + l][j]) * scale;
+      const uint16_t red_bits = orc_f32_to_bf16(acc);
+      const float red = orc_bf16_to_f32(red_bits);
+      for (int r = 0; r < P; ++r) {
+        float* w = weights[(size_t)r * L + l];
+        if (w) {
+          const volatile float step = lr * red; /* no contraction into an FMA */
+          w[j] = w[j] - step;
+        }
+      }
+      if (write_grad) {
+        for (int r = 0; r < P; ++r) grads[(size_t)r * L + l][j] = red_bits;
+      }
+    }
+  }
+}
+
 /* --------------------------------------------------- CPU Algorithm 2 run */
 
 static double now_sec(void) {

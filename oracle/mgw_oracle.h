@@ -57,6 +57,28 @@ void orc_pack(const float* const* grads, const uint64_t* counts, const uint64_t*
 void orc_allreduce_sgd(int P, float* const* grads, float* const* weights, const uint64_t* counts,
                        size_t L, const uint8_t* tags, float lr, int write_grad);
 
+/* --- bf16 gradients (reference trace.hpp:50
+ * bytes_per_element = 2). The build's semantics, restated: every source is
+ * widened to fp32 (exact), times 1/P, summed in rank order in fp32; the sum
+ * is rounded ONCE to bf16 (round to nearest even) and that value is the
+ * reduced gradient of every rank: w = fl(w - fl(lr * red)) on fp32 weights,
+ * grads overwritten with it when write_grad. --- */
+
+/* fp32 -> bf16 bits, round to nearest even (NaN -> quiet NaN). */
+uint16_t orc_f32_to_bf16(float x);
+float orc_bf16_to_f32(uint16_t h);
+
+/* Merge layout with layers starting on a `granule`-element boundary (16
+ * bytes: 4 for fp32, 8 for bf16). */
+void orc_merge_offsets_granule(const uint64_t* counts, size_t L, uint64_t granule, uint64_t* offs);
+
+/* bf16 pack: merge[j] = bf16(f32(g[j]) * scale), zero padding. */
+void orc_pack_bf16(const uint16_t* const* grads, const uint64_t* counts, const uint64_t* offs,
+                   size_t first, size_t last, float scale, uint16_t* merge);
+
+void orc_allreduce_sgd_bf16(int P, uint16_t* const* grads, float* const* weights, const uint64_t* counts,
+                            size_t L, const uint8_t* tags, float lr, int write_grad);
+
 /* --- CPU runtime of paper Algorithm 2 (bench reference arm) --- */
 
 /* Runs `iters` iterations: the calling thread replays the backward schedule

@@ -48,6 +48,16 @@ if ORC is not None:
     ORC.orc_allreduce_sgd.restype = None
     ORC.orc_pipeline_run.argtypes = [C.c_int, fpp, fpp, u64p, f64p, C.c_size_t, C.c_double, u8p,
                                      C.c_float, C.c_int, C.c_int, f64p]
+    ORC.orc_f32_to_bf16.argtypes = [C.c_float]
+    ORC.orc_f32_to_bf16.restype = C.c_uint16
+    ORC.orc_bf16_to_f32.argtypes = [C.c_uint16]
+    ORC.orc_bf16_to_f32.restype = C.c_float
+    ORC.orc_merge_offsets_granule.argtypes = [u64p, C.c_size_t, C.c_uint64, u64p]
+    ORC.orc_merge_offsets_granule.restype = None
+    ORC.orc_pack_bf16.argtypes = [fpp, u64p, u64p, C.c_size_t, C.c_size_t, C.c_float, C.c_void_p]
+    ORC.orc_pack_bf16.restype = None
+    ORC.orc_allreduce_sgd_bf16.argtypes = [C.c_int, fpp, fpp, u64p, C.c_size_t, u8p, C.c_float, C.c_int]
+    ORC.orc_allreduce_sgd_bf16.restype = None
 
 if REF is not None:
     REF.ref_optimal_plan.argtypes = _P + [u8p]
@@ -147,6 +157,51 @@ def allreduce_sgd(grads: List[List[np.ndarray]], weights: List[List[np.ndarray]]
     ORC.orc_allreduce_sgd(P, _ptrs([g for per in grads for g in per]),
                           _ptrs([w for per in weights for w in per]),
                           (C.c_uint64 * L)(*counts), L, (C.c_uint8 * L)(*tags), lr, int(write_grad))
+
+
+# ---- bf16 gradients -----------------------------------
+
+def f32_to_bf16(x: np.ndarray) -> np.ndarray:
+    """fp32 -> bf16 bits (uint16), round to nearest even: the vectorised
+    restatement of orc_f32_to_bf16 (tests check it against the C oracle and
+    against torch's conversion)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    nan = (u & 0x7FFFFFFF) > 0x7F800000
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    r[nan] = ((u[nan] >> 16) | 0x40).astype(np.uint16)
+    return r
+
+
+def bf16_to_f32(h: np.ndarray) -> np.ndarray:
+    return (np.ascontiguousarray(h, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def merge_offsets_granule(counts: Sequence[int], granule: int) -> List[int]:
+    L = len(counts)
+    out = (C.c_uint64 * (L + 1))()
+    ORC.orc_merge_offsets_granule((C.c_uint64 * L)(*counts), L, granule, out)
+    return list(out)
+
+
+def pack_bf16(grads: Sequence[np.ndarray], first: int, last: int, scale: float) -> np.ndarray:
+    """grads: uint16 (bf16 bits) arrays; returns the uint16 merge buffer."""
+    counts = [g.size for g in grads]
+    offs = merge_offsets_granule(counts, 8)
+    out = np.zeros(offs[last] - offs[first], dtype=np.uint16)
+    ORC.orc_pack_bf16(_ptrs(grads), (C.c_uint64 * len(counts))(*counts),
+                      (C.c_uint64 * len(offs))(*offs), first, last, scale, out.ctypes.data)
+    return out
+
+
+def allreduce_sgd_bf16(grads: List[List[np.ndarray]], weights: List[List[np.ndarray]], tags, lr: float,
+                       write_grad: bool = False) -> None:
+    """In place: grads[r][l] uint16 (bf16 bits), weights[r][l] float32."""
+    P, L = len(grads), len(grads[0])
+    counts = [g.size for g in grads[0]]
+    ORC.orc_allreduce_sgd_bf16(P, _ptrs([g for per in grads for g in per]),
+                               _ptrs([w for per in weights for w in per]),
+                               (C.c_uint64 * L)(*counts), L, (C.c_uint8 * L)(*tags), lr, int(write_grad))
 
 
 def pipeline_run(grads, weights, counts, t_b, t_f, tags, lr, threads, iters) -> List[float]:

@@ -79,6 +79,9 @@ mgw_comm_get_oneshot_max = _proto("mgw_comm_get_oneshot_max", [vp, u64p])
 mgw_plan_create = _proto(
     "mgw_plan_create", [vp, C.c_size_t, C.POINTER(vp), C.POINTER(vp), u64p, u8p, C.POINTER(vp)]
 )
+mgw_plan_create_ex = _proto(
+    "mgw_plan_create_ex", [vp, C.c_size_t, C.POINTER(vp), C.POINTER(vp), u64p, u8p, C.c_int, C.POINTER(vp)]
+)
 mgw_plan_destroy = _proto("mgw_plan_destroy", [vp])
 mgw_plan_num_groups = _proto("mgw_plan_num_groups", [vp, C.POINTER(C.c_int)])
 mgw_plan_group_span = _proto("mgw_plan_group_span", [vp, C.c_int, u64p, u64p, u64p])

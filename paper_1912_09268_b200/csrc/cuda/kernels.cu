@@ -34,6 +34,7 @@
 // contraction, bit-exact with the CPU oracle's fl(fl(x0*s) + x1*s)... in
 // rank order.
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "mgw_device.cuh"
@@ -59,13 +60,152 @@ __device__ __forceinline__ float4 load_tail(const float* p, uint32_t n) {
   return v;
 }
 
+// ---- gradient element types ------------------------------------------------
+// Gradients and merge arenas are fp32 or bf16; weights
+// and every sum are fp32. A "vector" is 4 consecutive elements (16 bytes of
+// fp32, 8 of bf16) carried as a float4; bf16 -> fp32 is exact, fp32 -> bf16
+// rounds to nearest even (__float2bfloat16_rn).
+using bf16 = __nv_bfloat16;
+
+template <typename T>
+struct Elem;
+template <>
+struct Elem<float> {
+  static constexpr uint32_t kVec = 4;  // elements per 16 bytes (TMA / layout granule)
+};
+template <>
+struct Elem<bf16> {
+  static constexpr uint32_t kVec = 8;
+};
+
+template <typename T>
+__device__ __forceinline__ T* as(float* p) {
+  return reinterpret_cast<T*>(p);
+}
+
+__device__ __forceinline__ float4 unpack_bf16x4(uint32_t a, uint32_t b) {
+  return make_float4(__uint_as_float(a << 16), __uint_as_float(a & 0xffff0000u), __uint_as_float(b << 16),
+                     __uint_as_float(b & 0xffff0000u));
+}
+
+__device__ __forceinline__ uint32_t bf16_bits(float x) {
+  return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(x)));
+}
+
+// 4 elements -> float4: L1-bypassing (peer-written arena data)
+template <typename T>
+__device__ __forceinline__ float4 ld4_cg(const T* p);
+template <>
+__device__ __forceinline__ float4 ld4_cg<float>(const float* p) {
+  return ld_cg_v4(p);
+}
+template <>
+__device__ __forceinline__ float4 ld4_cg<bf16>(const bf16* p) {
+  uint32_t a, b;
+  asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
+  return unpack_bf16x4(a, b);
+}
+
+// ld4_cg(p) when `pred`, else `other` (predicated: no branch, no dynamically
+// indexed register array)
+template <typename T>
+__device__ __forceinline__ float4 ld4_cg_or(const T* p, bool pred, float4 other);
+template <>
+__device__ __forceinline__ float4 ld4_cg_or<float>(const float* p, bool pred, float4 other) {
+  return ld_cg_v4_or(p, pred, other);
+}
+template <>
+__device__ __forceinline__ float4 ld4_cg_or<bf16>(const bf16* p, bool pred, float4 other) {
+  uint32_t a = 0, b = 0;
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %3, 0; @q ld.global.cg.v2.u32 {%0,%1}, [%2]; }"
+               : "+r"(a), "+r"(b)
+               : "l"(p), "r"(static_cast<uint32_t>(pred)));
+  return pred ? unpack_bf16x4(a, b) : other;
+}
+
+// 4 elements -> float4: streaming read-once gradients
+template <typename T>
+__device__ __forceinline__ float4 ld4_stream(const T* p);
+template <>
+__device__ __forceinline__ float4 ld4_stream<float>(const float* p) {
+  return ld_stream_v4(p);
+}
+template <>
+__device__ __forceinline__ float4 ld4_stream<bf16>(const bf16* p) {
+  uint32_t a, b;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
+  return unpack_bf16x4(a, b);
+}
+
+template <typename T>
+__device__ __forceinline__ float4 ld4(const T* p) {
+  if constexpr (sizeof(T) == 4) {
+    return ld_v4(reinterpret_cast<const float*>(p));
+  } else {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    return unpack_bf16x4(u.x, u.y);
+  }
+}
+
+// First n (< 4 allowed) elements, zero-filled, any alignment.
+template <typename T>
+__device__ __forceinline__ float4 ld4_tail(const T* p, uint32_t n) {
+  if constexpr (sizeof(T) == 4) {
+    return load_tail(reinterpret_cast<const float*>(p), n);
+  } else {
+    float4 v;
+    v.x = n > 0 ? __bfloat162float(p[0]) : 0.0f;
+    v.y = n > 1 ? __bfloat162float(p[1]) : 0.0f;
+    v.z = n > 2 ? __bfloat162float(p[2]) : 0.0f;
+    v.w = n > 3 ? __bfloat162float(p[3]) : 0.0f;
+    return v;
+  }
+}
+
+// float4 -> 4 elements (bf16: round to nearest even)
+template <typename T>
+__device__ __forceinline__ void st4(T* p, float4 v) {
+  if constexpr (sizeof(T) == 4) {
+    st_v4(reinterpret_cast<float*>(p), v);
+  } else {
+    *reinterpret_cast<uint2*>(p) =
+        make_uint2(bf16_bits(v.x) | (bf16_bits(v.y) << 16), bf16_bits(v.z) | (bf16_bits(v.w) << 16));
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void st_tail(T* p, float4 v, uint32_t n) {
+  if constexpr (sizeof(T) == 4) {
+    if (n > 0) p[0] = v.x;
+    if (n > 1) p[1] = v.y;
+    if (n > 2) p[2] = v.z;
+    if (n > 3) p[3] = v.w;
+  } else {
+    if (n > 0) p[0] = __float2bfloat16_rn(v.x);
+    if (n > 1) p[1] = __float2bfloat16_rn(v.y);
+    if (n > 2) p[2] = __float2bfloat16_rn(v.z);
+    if (n > 3) p[3] = __float2bfloat16_rn(v.w);
+  }
+}
+
+// The reduced gradient in the gradient type: identity for fp32; bf16 rounds
+// the fp32 rank-order sum once, and every rank applies that same value.
+template <typename T>
+__device__ __forceinline__ float4 round4(float4 v) {
+  if constexpr (sizeof(T) == 4) {
+    return v;
+  } else {
+    return unpack_bf16x4(bf16_bits(v.x) | (bf16_bits(v.y) << 16), bf16_bits(v.z) | (bf16_bits(v.w) << 16));
+  }
+}
+
 // Standalone pack of tile t: gather + x scale into the merge buffer; each
 // thread has all its kPackVec loads in flight before any store.
 constexpr uint32_t kPackVec = kTileElems / 4 / kBlock;
-__device__ __forceinline__ void pack_tile(const Tile& t, float* const* grads, float* dst_base,
-                                          float scale) {
-  const float* src = grads[t.layer & kLayerMask] + t.src;
-  float* dst = dst_base + t.moff;
+template <typename T>
+__device__ __forceinline__ void pack_tile(const Tile& t, float* const* grads, T* dst_base, float scale) {
+  const T* src = as<T>(grads[t.layer & kLayerMask]) + t.src;
+  T* dst = dst_base + t.moff;
   const bool aligned = !(t.layer & kGradUnaligned);
   const uint32_t nvec = (t.len + 3) >> 2;
   float4 x[kPackVec];
@@ -73,18 +213,19 @@ __device__ __forceinline__ void pack_tile(const Tile& t, float* const* grads, fl
   for (uint32_t k = 0; k < kPackVec; ++k) {
     const uint32_t i = threadIdx.x + k * kBlock;
     const uint32_t e = i * 4;
-    if (i < nvec) x[k] = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
+    if (i < nvec) x[k] = (aligned && e + 4 <= t.len) ? ld4_stream<T>(src + e) : ld4_tail<T>(src + e, t.len - e);
   }
 #pragma unroll
   for (uint32_t k = 0; k < kPackVec; ++k) {
     const uint32_t i = threadIdx.x + k * kBlock;
-    if (i < nvec) st_v4(dst + i * 4, mul4(x[k], scale));
+    if (i < nvec) st4<T>(dst + i * 4, mul4(x[k], scale));
   }
 }
 
 // Element group e..e+3 of tile t receives the reduced gradient `g`.
-__device__ __forceinline__ void epilogue(const Tile& t, uint32_t e, float4 g, float* w_layer,
-                                         float* g_layer, float lr, int epi) {
+template <typename T>
+__device__ __forceinline__ void epilogue(const Tile& t, uint32_t e, float4 g, float* w_layer, T* g_layer,
+                                         float lr, int epi) {
   const uint32_t n = t.len - e < 4 ? t.len - e : 4;
   if ((epi & MGW_SGD) && w_layer != nullptr) {
     float* w = w_layer + t.src + e;
@@ -103,14 +244,11 @@ __device__ __forceinline__ void epilogue(const Tile& t, uint32_t e, float4 g, fl
     }
   }
   if (epi & MGW_WRITE_GRAD) {
-    float* d = g_layer + t.src + e;
+    T* d = g_layer + t.src + e;
     if (n == 4 && !(t.layer & kGradUnaligned)) {
-      st_v4(d, g);
+      st4<T>(d, g);
     } else {
-      if (n > 0) d[0] = g.x;
-      if (n > 1) d[1] = g.y;
-      if (n > 2) d[2] = g.z;
-      if (n > 3) d[3] = g.w;
+      st_tail<T>(d, g, n);
     }
   }
 }
@@ -190,7 +328,7 @@ __device__ __forceinline__ void ring_init(uint64_t* bars) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-__device__ __forceinline__ void tma_load(uint32_t stage_addr, const float* src, uint32_t bytes, uint32_t bar) {
+__device__ __forceinline__ void tma_load(uint32_t stage_addr, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(stage_addr),
@@ -198,7 +336,7 @@ __device__ __forceinline__ void tma_load(uint32_t stage_addr, const float* src, 
       : "memory");
 }
 
-__device__ __forceinline__ void tma_store(float* dst, uint32_t stage_addr, uint32_t bytes) {
+__device__ __forceinline__ void tma_store(void* dst, uint32_t stage_addr, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(stage_addr), "r"(bytes)
                : "memory");
 }
@@ -227,11 +365,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, uint32_
   }
 }
 
-// Bulk copies of the tile's 16-byte-aligned body are the TMA's; the rest
-// (unaligned layer view: the whole tile; else the < 4-element tail) goes
-// through registers.
+// Bulk copies of the tile's 16-byte body (a multiple of Elem<T>::kVec
+// elements) are the TMA's; the rest (unaligned layer view: the whole tile;
+// else the < 16-byte tail) goes through registers.
+template <typename T>
 __device__ __forceinline__ bool tma_able(const Tile& t) {
-  return !(t.layer & kGradUnaligned) && t.len >= 4;
+  return !(t.layer & kGradUnaligned) && t.len >= Elem<T>::kVec;
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t tma_body(const Tile& t) {
+  return t.len & ~(Elem<T>::kVec - 1);
 }
 
 // One push item: a tile and the ranks it goes to.
@@ -241,7 +385,7 @@ struct PushItem {
 };
 
 // Push the items of one chunk, enumerated by `item(i)`. Producer warp only.
-template <int P, typename Item>
+template <int P, typename T, typename Item>
 __device__ __forceinline__ void push_items(const RankView& v, uint32_t n_items, uint64_t my_slot,
                                            PushRing& ring, uint8_t* stages, uint64_t* bars, Item item) {
   const uint32_t lane = threadIdx.x & 31;
@@ -257,25 +401,25 @@ __device__ __forceinline__ void push_items(const RankView& v, uint32_t n_items, 
       // latest group (item ns - 1) pending, so that needs nl <= ns + kStages - 2
       while (iL < n_items && (nl < kStages || nl + 2 <= ns + kStages)) {
         const PushItem it = item(iL++);
-        if (it.mask == 0 || !tma_able(it.t)) continue;
+        if (it.mask == 0 || !tma_able<T>(it.t)) continue;
         if (nl >= kStages) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         const uint32_t k = (ring.head + nl) % kStages;
-        tma_load(s0 + k * kStageBytes, v.grads[it.t.layer & kLayerMask] + it.t.src, (it.t.len & ~3u) * 4u,
-                 smem_u32(bars + k));
+        tma_load(s0 + k * kStageBytes, as<T>(v.grads[it.t.layer & kLayerMask]) + it.t.src,
+                 tma_body<T>(it.t) * static_cast<uint32_t>(sizeof(T)), smem_u32(bars + k));
         ++nl;
       }
       if (ns == nl) break;
       PushItem it;
       do {
         it = item(iS++);
-      } while (it.mask == 0 || !tma_able(it.t));
+      } while (it.mask == 0 || !tma_able<T>(it.t));
       const uint32_t k = (ring.head + ns) % kStages;
       mbar_wait(smem_u32(bars + k), (ring.phase >> k) & 1u, v.state + kStateError);
       ring.phase ^= 1u << k;
-      const uint32_t bytes = (it.t.len & ~3u) * 4u;
+      const uint32_t bytes = tma_body<T>(it.t) * static_cast<uint32_t>(sizeof(T));
 #pragma unroll
       for (int q = 0; q < P; ++q) {
-        if (it.mask & (1u << q)) tma_store(v.arena[q] + my_slot + it.t.moff, s0 + k * kStageBytes, bytes);
+        if (it.mask & (1u << q)) tma_store(as<T>(v.arena[q]) + my_slot + it.t.moff, s0 + k * kStageBytes, bytes);
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       ++ns;
@@ -286,16 +430,16 @@ __device__ __forceinline__ void push_items(const RankView& v, uint32_t n_items, 
   // register path: unaligned tiles (whole warp) and tails (lane 0)
   for (uint32_t i = 0; i < n_items; ++i) {
     const PushItem it = item(i);
-    if (it.mask == 0 || (tma_able(it.t) && !(it.t.len & 3u))) continue;
-    const float* src = v.grads[it.t.layer & kLayerMask] + it.t.src;
-    const uint32_t first = tma_able(it.t) ? (it.t.len & ~3u) : 0;  // elements the TMA did
+    if (it.mask == 0 || (tma_able<T>(it.t) && tma_body<T>(it.t) == it.t.len)) continue;
+    const T* src = as<T>(v.grads[it.t.layer & kLayerMask]) + it.t.src;
+    const uint32_t first = tma_able<T>(it.t) ? tma_body<T>(it.t) : 0;  // elements the TMA did
     const uint32_t nvec = (it.t.len - first + 3) >> 2;
     for (uint32_t j = lane; j < nvec; j += 32) {
       const uint32_t e = first + j * 4;
-      const float4 x = load_tail(src + e, it.t.len - e);
+      const float4 x = ld4_tail<T>(src + e, it.t.len - e);  // (bf16 -> fp32 -> bf16 is exact)
 #pragma unroll
       for (int q = 0; q < P; ++q) {
-        if (it.mask & (1u << q)) st_v4(v.arena[q] + my_slot + it.t.moff + e, x);
+        if (it.mask & (1u << q)) st4<T>(as<T>(v.arena[q]) + my_slot + it.t.moff + e, x);
       }
     }
   }
@@ -336,10 +480,10 @@ __device__ __forceinline__ void load_w_batch(const Tile& t, uint32_t i0, uint32_
 
 // SGD (+ optional grad write-back) for the B vectors, with their weights wv
 // from load_w_batch.
-template <uint32_t B>
+template <uint32_t B, typename T>
 __device__ __forceinline__ void apply_batch(const Tile& t, uint32_t i0, uint32_t stride,
                                             const float4 (&g)[B], const float4 (&wv)[B], float* w_layer,
-                                            float* g_layer, float lr, int epi) {
+                                            T* g_layer, float lr, int epi) {
   const uint32_t nvec = (t.len + 3) >> 2;
   const bool vec_w = (epi & MGW_SGD) && w_layer != nullptr && !(t.layer & kWeightUnaligned);
 #pragma unroll
@@ -354,9 +498,9 @@ __device__ __forceinline__ void apply_batch(const Tile& t, uint32_t i0, uint32_t
       w.z = sgd1(w.z, g[j].z, lr);
       w.w = sgd1(w.w, g[j].w, lr);
       st_v4(w_layer + t.src + e, w);
-      if (epi & MGW_WRITE_GRAD) epilogue(t, e, g[j], nullptr, g_layer, lr, MGW_WRITE_GRAD);
+      if (epi & MGW_WRITE_GRAD) epilogue<T>(t, e, g[j], nullptr, g_layer, lr, MGW_WRITE_GRAD);
     } else {
-      epilogue(t, e, g[j], w_layer, g_layer, lr, epi);  // tail / unaligned / no-SGD
+      epilogue<T>(t, e, g[j], w_layer, g_layer, lr, epi);  // tail / unaligned / no-SGD
     }
   }
 }
@@ -366,17 +510,17 @@ __device__ __forceinline__ void apply_batch(const Tile& t, uint32_t i0, uint32_t
 // x0 + x1 + ... + x_{P-1}; B vectors per batch; optionally push each sum
 // into slot `my_slot` of every peer (the two-shot owner's all-gather), then
 // SGD. Data warps only.
-template <int P>
+template <int P, typename T>
 __device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, uint64_t slot_stride,
                                             bool push_to_peers, uint64_t my_slot, float scale, float lr,
                                             int epi) {
   constexpr uint32_t B = RedBatch<P>::value;
-  const float* base = v.arena[v.rank] + t.moff;
+  const T* base = as<T>(v.arena[v.rank]) + t.moff;
   const uint32_t nvec = (t.len + 3) >> 2;
   const uint32_t layer = t.layer & kLayerMask;
   float* w = v.weights[layer];
-  float* g = v.grads[layer];
-  const float* own = g + t.src;
+  T* g = as<T>(v.grads[layer]);
+  const T* own = g + t.src;
   const bool own_aligned = !(t.layer & kGradUnaligned);
 #pragma unroll 1
   for (uint32_t k0 = 0; k0 < kVecPerThread; k0 += B) {
@@ -389,9 +533,9 @@ __device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, ui
       const uint32_t i = i0 + j * kThreads;
       if (i < nvec) {
         const uint32_t e = i * 4;
-        const float4 o = (own_aligned && e + 4 <= t.len) ? ld_stream_v4(own + e) : load_tail(own + e, t.len - e);
+        const float4 o = (own_aligned && e + 4 <= t.len) ? ld4_stream<T>(own + e) : ld4_tail<T>(own + e, t.len - e);
 #pragma unroll
-        for (int r = 0; r < P; ++r) x[j][r] = ld_cg_v4_or(base + r * slot_stride + e, r != v.rank, o);
+        for (int r = 0; r < P; ++r) x[j][r] = ld4_cg_or<T>(base + r * slot_stride + e, r != v.rank, o);
       }
     }
     load_w_batch<B>(t, i0, kThreads, w, epi, wv);
@@ -401,6 +545,7 @@ __device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, ui
       s[j] = mul4(x[j][0], scale);
 #pragma unroll
       for (int r = 1; r < P; ++r) s[j] = add4(s[j], mul4(x[j][r], scale));
+      s[j] = round4<T>(s[j]);
     }
     if (push_to_peers) {
 #pragma unroll
@@ -409,11 +554,11 @@ __device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, ui
         if (i >= nvec) continue;
 #pragma unroll
         for (int q = 0; q < P; ++q) {
-          if (q != v.rank) st_v4(v.arena[q] + my_slot + t.moff + i * 4, s[j]);
+          if (q != v.rank) st4<T>(as<T>(v.arena[q]) + my_slot + t.moff + i * 4, s[j]);
         }
       }
     }
-    apply_batch<B>(t, i0, kThreads, s, wv, w, g, lr, epi);
+    apply_batch<B, T>(t, i0, kThreads, s, wv, w, g, lr, epi);
   }
 }
 
@@ -431,7 +576,7 @@ struct CtaCtx {
 //   step t: producer pushes chunk t to every peer (TMA) | data warps reduce
 //   + SGD chunk t-1 from the local slots; barrier (if t < n).
 // NVLink: (P-1) * S posted writes per rank.
-template <int P>
+template <int P, typename T>
 __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* tiles,
                                                uint32_t n_tiles, uint64_t slot_stride, float scale,
                                                float lr, int epi, uint32_t cta, uint32_t ncta,
@@ -447,7 +592,7 @@ __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* ti
       if (t < n_chunks) {
         const uint32_t j0 = t * C;
         const uint32_t n = mine - j0 < C ? mine - j0 : C;
-        push_items<P>(v, n, my_slot, cx.ring, cx.stages, cx.bars, [&](uint32_t i) {
+        push_items<P, T>(v, n, my_slot, cx.ring, cx.stages, cx.bars, [&](uint32_t i) {
           return PushItem{tiles[cta + (j0 + i) * ncta], peers};
         });
         push_drain();
@@ -455,7 +600,7 @@ __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* ti
     } else if (t >= 1) {
 #pragma unroll 1
       for (uint32_t j = (t - 1) * C; j < mine && j < t * C; ++j) {
-        reduce_tile<P>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, scale, lr, epi);
+        reduce_tile<P, T>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, scale, lr, epi);
       }
     }
     if (t < n_chunks) cta_barrier(v, P, cta, cx.count);
@@ -469,7 +614,7 @@ __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* ti
 //   AP(c):  apply the other owners' results from the local slots (SGD)
 // step t: RS(t) [producer] | RA(t-1), AP(t-2) [data warps]; barrier (t <= n).
 // NVLink: 2 (P-1)/P * S posted writes per rank.
-template <int P>
+template <int P, typename T>
 __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* tiles,
                                                uint32_t n_tiles, uint64_t slot_stride, float scale,
                                                float lr, int epi, uint32_t cta, uint32_t ncta,
@@ -486,7 +631,7 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
       if (t < n_chunks) {
         const uint32_t j0 = t * C;
         const uint32_t ns = mine - j0 < C ? mine - j0 : C;
-        push_items<P>(v, ns * (P - 1), my_slot, cx.ring, cx.stages, cx.bars,
+        push_items<P, T>(v, ns * (P - 1), my_slot, cx.ring, cx.stages, cx.bars,
                       [&](uint32_t i) {
                         const uint32_t s = cta + (j0 + i / (P - 1)) * ncta;
                         const int qi = static_cast<int>(i % (P - 1));
@@ -501,7 +646,7 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
 #pragma unroll 1
         for (uint32_t j = (t - 1) * C; j < mine && j < t * C; ++j) {
           const uint32_t ti = (cta + j * ncta) * P + me;
-          if (ti < n_tiles) reduce_tile<P>(v, tiles[ti], slot_stride, true, my_slot, scale, lr, epi);
+          if (ti < n_tiles) reduce_tile<P, T>(v, tiles[ti], slot_stride, true, my_slot, scale, lr, epi);
         }
       }
       if (t >= 2) {  // AP(t-2)
@@ -513,18 +658,18 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
             const uint32_t ti = s * P + q;
             if (q == me || ti >= n_tiles) continue;
             const Tile tl = tiles[ti];
-            const float* red = v.arena[me] + static_cast<uint64_t>(q) * slot_stride + tl.moff;
+            const T* red = as<T>(v.arena[me]) + static_cast<uint64_t>(q) * slot_stride + tl.moff;
             const uint32_t layer = tl.layer & kLayerMask;
             const uint32_t nvec = (tl.len + 3) >> 2;
             float4 x[kVecPerThread], wv[kVecPerThread];
 #pragma unroll
             for (uint32_t k = 0; k < kVecPerThread; ++k) {
               const uint32_t i = threadIdx.x + k * kThreads;
-              if (i < nvec) x[k] = ld_cg_v4(red + i * 4);
+              if (i < nvec) x[k] = ld4_cg<T>(red + i * 4);
             }
             load_w_batch<kVecPerThread>(tl, threadIdx.x, kThreads, v.weights[layer], epi, wv);
-            apply_batch<kVecPerThread>(tl, threadIdx.x, kThreads, x, wv, v.weights[layer], v.grads[layer], lr,
-                                       epi);
+            apply_batch<kVecPerThread, T>(tl, threadIdx.x, kThreads, x, wv, v.weights[layer],
+                                          as<T>(v.grads[layer]), lr, epi);
           }
         }
       }
@@ -534,7 +679,7 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
 }
 
 // One merge group, executed by CTA `cta` of `ncta`.
-template <int P>
+template <int P, typename T>
 __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, const Tile* tiles,
                                           uint32_t n_tiles, uint64_t slot_stride, float scale,
                                           float lr, int epi, uint32_t cta, uint32_t ncta,
@@ -546,9 +691,9 @@ __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, cons
     for (uint32_t ti = cta; ti < n_tiles; ti += ncta) {
       const Tile t = tiles[ti];
       const uint32_t layer = t.layer & kLayerMask;
-      const float* src = v.grads[layer] + t.src;
+      T* g = as<T>(v.grads[layer]);
+      const T* src = g + t.src;
       float* w = v.weights[layer];
-      float* g = v.grads[layer];
       const bool aligned = !(t.layer & kGradUnaligned);
       const uint32_t nvec = (t.len + 3) >> 2;
       float4 x[kB], wv[kB];
@@ -556,17 +701,17 @@ __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, cons
       for (uint32_t k = 0; k < kB; ++k) {
         const uint32_t i = threadIdx.x + k * kBlock;
         const uint32_t e = i * 4;
-        if (i < nvec) x[k] = (aligned && e + 4 <= t.len) ? ld_stream_v4(src + e) : load_tail(src + e, t.len - e);
+        if (i < nvec) x[k] = (aligned && e + 4 <= t.len) ? ld4_stream<T>(src + e) : ld4_tail<T>(src + e, t.len - e);
       }
       load_w_batch<kB>(t, threadIdx.x, kBlock, w, epi, wv);
 #pragma unroll
-      for (uint32_t k = 0; k < kB; ++k) x[k] = mul4(x[k], scale);
-      apply_batch<kB>(t, threadIdx.x, kBlock, x, wv, w, g, lr, epi);
+      for (uint32_t k = 0; k < kB; ++k) x[k] = round4<T>(mul4(x[k], scale));
+      apply_batch<kB, T>(t, threadIdx.x, kBlock, x, wv, w, g, lr, epi);
     }
   } else if (two_shot) {
-    two_shot_group<P>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, chunk, cx);
+    two_shot_group<P, T>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, chunk, cx);
   } else {
-    one_shot_group<P>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, chunk, cx);
+    one_shot_group<P, T>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, chunk, cx);
   }
 }
 
@@ -589,19 +734,19 @@ __device__ __forceinline__ void cta_ctx_init(CtaCtx& cx, const RankView& v, uint
   }
 }
 
-template <int P, bool TWO_SHOT, bool LOOPBACK>
+template <int P, bool TWO_SHOT, bool LOOPBACK, typename T>
 __global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid_constant__ GroupLaunch L) {
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t bars[kStages];
   const RankView& v = L.views[LOOPBACK ? blockIdx.y : 0];
   CtaCtx cx;
   cta_ctx_init<P>(cx, v, dsmem, bars);
-  run_group<P>(TWO_SHOT, v, L.tiles, L.n_tiles, L.slot_stride, L.scale, L.lr, L.epilogue,
+  run_group<P, T>(TWO_SHOT, v, L.tiles, L.n_tiles, L.slot_stride, L.scale, L.lr, L.epilogue,
                blockIdx.x, gridDim.x, L.chunk, cx);
   if constexpr (P > 1) store_cta_count(v, blockIdx.x, cx.count);
 }
 
-template <int P>
+template <int P, typename T>
 __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant__ EngineLaunch E) {
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t bars[kStages];
@@ -637,7 +782,7 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
       if (E.stamps != nullptr && blockIdx.x == 0) E.stamps[2 * gi] = globaltimer_ns();
     }
     __syncthreads();
-    run_group<P>(two, v, E.tiles + grp.tile_first, grp.n_tiles, E.slot_stride, E.scale, E.lr,
+    run_group<P, T>(two, v, E.tiles + grp.tile_first, grp.n_tiles, E.slot_stride, E.scale, E.lr,
                  E.epilogue, blockIdx.x, gridDim.x, E.chunk, cx);
     if (E.stamps != nullptr) {
       __syncthreads();
@@ -663,34 +808,36 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
   }
 }
 
+template <typename T>
 __global__ void __launch_bounds__(kBlock) pack_kernel(const Tile* tiles, uint32_t n_tiles, float* const* grads,
-                                                       float* merge, uint64_t begin, float scale) {
+                                                       T* merge, uint64_t begin, float scale) {
   for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
     Tile t = tiles[ti];
     t.moff = static_cast<uint32_t>(t.moff - begin);
-    pack_tile(t, grads, merge, scale);
+    pack_tile<T>(t, grads, merge, scale);
   }
 }
 
+template <typename T>
 __global__ void __launch_bounds__(kBlock) unpack_sgd_kernel(const Tile* tiles, uint32_t n_tiles,
                                                              float* const* grads, float* const* weights,
-                                                             const float* merge, uint64_t begin, float lr,
+                                                             const T* merge, uint64_t begin, float lr,
                                                              int epi) {
   for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
     const Tile t = tiles[ti];
     const uint32_t layer = t.layer & kLayerMask;
-    const float* red = merge + (t.moff - begin);
+    const T* red = merge + (t.moff - begin);
     float* w = weights[layer];
-    float* g = grads[layer];
+    T* g = as<T>(grads[layer]);
     const uint32_t nvec = (t.len + 3) >> 2;
     float4 x[kPackVec], wv[kPackVec];
 #pragma unroll
     for (uint32_t k = 0; k < kPackVec; ++k) {
       const uint32_t i = threadIdx.x + k * kBlock;
-      if (i < nvec) x[k] = ld_v4(red + i * 4);
+      if (i < nvec) x[k] = ld4<T>(red + i * 4);
     }
     load_w_batch<kPackVec>(t, threadIdx.x, kBlock, w, epi, wv);
-    apply_batch<kPackVec>(t, threadIdx.x, kBlock, x, wv, w, g, lr, epi);
+    apply_batch<kPackVec, T>(t, threadIdx.x, kBlock, x, wv, w, g, lr, epi);
   }
 }
 
@@ -763,9 +910,9 @@ constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes;
 
 constexpr size_t smem_for(int P) { return P > 1 ? kSmemBytes : 0; }
 
-template <int P, bool TWO, bool LB>
+template <int P, bool TWO, bool LB, typename T>
 cudaError_t launch_t(const GroupLaunch& L, dim3 grid, cudaStream_t stream) {
-  auto* fn = group_allreduce_kernel<P, TWO, LB>;
+  auto* fn = group_allreduce_kernel<P, TWO, LB, T>;
   if constexpr (LB) {
     void* args[] = {const_cast<GroupLaunch*>(&L)};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), grid, dim3(kBlock), args, smem_for(P),
@@ -776,29 +923,35 @@ cudaError_t launch_t(const GroupLaunch& L, dim3 grid, cudaStream_t stream) {
   }
 }
 
-template <bool LB>
+template <bool LB, typename T>
 cudaError_t launch_lb(const GroupLaunch& L, dim3 grid, bool two, cudaStream_t s) {
   switch (L.nranks) {
-    case 1: return launch_t<1, false, LB>(L, grid, s);
-    case 2: return two ? launch_t<2, true, LB>(L, grid, s) : launch_t<2, false, LB>(L, grid, s);
-    case 4: return two ? launch_t<4, true, LB>(L, grid, s) : launch_t<4, false, LB>(L, grid, s);
-    case 8: return two ? launch_t<8, true, LB>(L, grid, s) : launch_t<8, false, LB>(L, grid, s);
+    case 1: return launch_t<1, false, LB, T>(L, grid, s);
+    case 2: return two ? launch_t<2, true, LB, T>(L, grid, s) : launch_t<2, false, LB, T>(L, grid, s);
+    case 4: return two ? launch_t<4, true, LB, T>(L, grid, s) : launch_t<4, false, LB, T>(L, grid, s);
+    case 8: return two ? launch_t<8, true, LB, T>(L, grid, s) : launch_t<8, false, LB, T>(L, grid, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
-const void* engine_fn(int nranks) {
+template <typename T>
+const void* engine_fn_t(int nranks) {
   switch (nranks) {
-    case 1: return reinterpret_cast<const void*>(engine_kernel<1>);
-    case 2: return reinterpret_cast<const void*>(engine_kernel<2>);
-    case 4: return reinterpret_cast<const void*>(engine_kernel<4>);
-    case 8: return reinterpret_cast<const void*>(engine_kernel<8>);
+    case 1: return reinterpret_cast<const void*>(engine_kernel<1, T>);
+    case 2: return reinterpret_cast<const void*>(engine_kernel<2, T>);
+    case 4: return reinterpret_cast<const void*>(engine_kernel<4, T>);
+    case 8: return reinterpret_cast<const void*>(engine_kernel<8, T>);
     default: return nullptr;
   }
 }
 
-const void* group_fn(int nranks, bool two_shot, bool loopback) {
-#define MGW_PICK(P, TWO, LB) return reinterpret_cast<const void*>(group_allreduce_kernel<P, TWO, LB>)
+const void* engine_fn(int nranks, int dtype) {
+  return dtype == MGW_DTYPE_BF16 ? engine_fn_t<bf16>(nranks) : engine_fn_t<float>(nranks);
+}
+
+template <typename T>
+const void* group_fn_t(int nranks, bool two_shot, bool loopback) {
+#define MGW_PICK(P, TWO, LB) return reinterpret_cast<const void*>(group_allreduce_kernel<P, TWO, LB, T>)
   if (loopback) {
     if (nranks == 1) MGW_PICK(1, false, true);
     if (nranks == 2) { if (two_shot) MGW_PICK(2, true, true); MGW_PICK(2, false, true); }
@@ -814,45 +967,64 @@ const void* group_fn(int nranks, bool two_shot, bool loopback) {
   return nullptr;
 }
 
+const void* group_fn(int nranks, bool two_shot, bool loopback, int dtype) {
+  return dtype == MGW_DTYPE_BF16 ? group_fn_t<bf16>(nranks, two_shot, loopback)
+                                 : group_fn_t<float>(nranks, two_shot, loopback);
+}
+
 }  // namespace
 
 cudaError_t launch_group_allreduce(const GroupLaunch& L, int ctas_per_rank, bool two_shot,
                                    bool loopback, cudaStream_t stream) {
   const dim3 grid(ctas_per_rank, loopback ? L.nranks : 1);
-  return loopback ? launch_lb<true>(L, grid, two_shot, stream)
-                  : launch_lb<false>(L, grid, two_shot, stream);
+  if (L.dtype == MGW_DTYPE_BF16) {
+    return loopback ? launch_lb<true, bf16>(L, grid, two_shot, stream)
+                    : launch_lb<false, bf16>(L, grid, two_shot, stream);
+  }
+  return loopback ? launch_lb<true, float>(L, grid, two_shot, stream)
+                  : launch_lb<false, float>(L, grid, two_shot, stream);
 }
 
 cudaError_t launch_engine(const EngineLaunch& E, int ctas, cudaStream_t stream) {
-  const void* fn = engine_fn(E.nranks);
+  const void* fn = engine_fn(E.nranks, E.dtype);
   if (fn == nullptr) return cudaErrorInvalidValue;
   void* args[] = {const_cast<EngineLaunch*>(&E)};
   return cudaLaunchKernel(fn, dim3(ctas), dim3(kBlock), args, smem_for(E.nranks), stream);
 }
 
-cudaError_t engine_ctas_per_sm(int nranks, int* out) {
-  const void* fn = engine_fn(nranks);
+cudaError_t engine_ctas_per_sm(int nranks, int dtype, int* out) {
+  const void* fn = engine_fn(nranks, dtype);
   if (fn == nullptr) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kBlock, smem_for(nranks));
 }
 
-cudaError_t max_ctas_per_sm(int nranks, bool two_shot, bool loopback, int* out) {
-  const void* fn = group_fn(nranks, two_shot, loopback);
+cudaError_t max_ctas_per_sm(int nranks, bool two_shot, bool loopback, int dtype, int* out) {
+  const void* fn = group_fn(nranks, two_shot, loopback, dtype);
   if (fn == nullptr) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kBlock, smem_for(nranks));
 }
 
-cudaError_t launch_pack(const Tile* tiles, uint32_t n_tiles, float* const* grads, float* merge,
-                        uint64_t begin, float scale, int ctas, cudaStream_t stream) {
-  pack_kernel<<<ctas, kBlock, 0, stream>>>(tiles, n_tiles, grads, merge, begin, scale);
+cudaError_t launch_pack(const Tile* tiles, uint32_t n_tiles, float* const* grads, void* merge,
+                        uint64_t begin, float scale, int dtype, int ctas, cudaStream_t stream) {
+  if (dtype == MGW_DTYPE_BF16) {
+    pack_kernel<bf16><<<ctas, kBlock, 0, stream>>>(tiles, n_tiles, grads, static_cast<bf16*>(merge), begin, scale);
+  } else {
+    pack_kernel<float><<<ctas, kBlock, 0, stream>>>(tiles, n_tiles, grads, static_cast<float*>(merge), begin,
+                                                     scale);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_unpack_sgd(const Tile* tiles, uint32_t n_tiles, float* const* grads,
-                              float* const* weights, const float* merge, uint64_t begin, float lr,
-                              int epi, int ctas, cudaStream_t stream) {
-  unpack_sgd_kernel<<<ctas, kBlock, 0, stream>>>(tiles, n_tiles, grads, weights, merge, begin,
-                                                   lr, epi);
+                              float* const* weights, const void* merge, uint64_t begin, float lr,
+                              int epi, int dtype, int ctas, cudaStream_t stream) {
+  if (dtype == MGW_DTYPE_BF16) {
+    unpack_sgd_kernel<bf16><<<ctas, kBlock, 0, stream>>>(tiles, n_tiles, grads, weights,
+                                                          static_cast<const bf16*>(merge), begin, lr, epi);
+  } else {
+    unpack_sgd_kernel<float><<<ctas, kBlock, 0, stream>>>(tiles, n_tiles, grads, weights,
+                                                           static_cast<const float*>(merge), begin, lr, epi);
+  }
   return cudaGetLastError();
 }
 
@@ -885,30 +1057,27 @@ cudaError_t preload_kernels() {
       reinterpret_cast<const void*>(replay_all_kernel),
       reinterpret_cast<const void*>(replay_kernel),
       reinterpret_cast<const void*>(l2_flush_kernel),
-      reinterpret_cast<const void*>(pack_kernel),
-      reinterpret_cast<const void*>(unpack_sgd_kernel),
-      engine_fn(1), engine_fn(2), engine_fn(4), engine_fn(8),
+      reinterpret_cast<const void*>(pack_kernel<float>),
+      reinterpret_cast<const void*>(pack_kernel<bf16>),
+      reinterpret_cast<const void*>(unpack_sgd_kernel<float>),
+      reinterpret_cast<const void*>(unpack_sgd_kernel<bf16>),
   };
   for (const void* f : fns) {
     cudaFuncAttributes attr;
     const cudaError_t e = cudaFuncGetAttributes(&attr, f);
     if (e != cudaSuccess) return e;
   }
-  // the TMA ring lives in dynamic shared memory (> the 48 KiB default)
-  for (int p : {2, 4, 8}) {
-    const void* ks[] = {engine_fn(p), group_fn(p, false, false), group_fn(p, true, false),
-                        group_fn(p, false, true), group_fn(p, true, true)};
-    for (const void* f : ks) {
-      const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(kSmemBytes));
-      if (e != cudaSuccess) return e;
-    }
-  }
-  for (bool lb : {false, true}) {
+  for (int dt : {MGW_DTYPE_F32, MGW_DTYPE_BF16}) {
     for (int p : {1, 2, 4, 8}) {
-      for (bool two : {false, true}) {
-        int occ = 0;
-        const cudaError_t e = max_ctas_per_sm(p, two, lb, &occ);
+      const void* ks[] = {engine_fn(p, dt), group_fn(p, false, false, dt), group_fn(p, true, false, dt),
+                          group_fn(p, false, true, dt), group_fn(p, true, true, dt)};
+      for (const void* f : ks) {
+        cudaFuncAttributes attr;
+        cudaError_t e = cudaFuncGetAttributes(&attr, f);
+        // the TMA ring lives in dynamic shared memory (> the 48 KiB default)
+        if (e == cudaSuccess && p > 1) {
+          e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+        }
         if (e != cudaSuccess) return e;
       }
     }

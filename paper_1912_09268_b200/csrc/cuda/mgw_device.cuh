@@ -68,6 +68,7 @@ struct GroupLaunch {
   int epilogue;          // MGW_SGD | MGW_WRITE_GRAD
   uint64_t slot_stride;  // elements between the per-source-rank slots of an arena
   uint32_t chunk;        // tiles per pipelined chunk of one CTA (two-shot: max(1, chunk/P) super-tiles)
+  int dtype;             // MGW_DTYPE_* of the gradients / arena
   RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
 };
 
@@ -93,6 +94,7 @@ struct EngineLaunch {
   int epilogue;
   uint64_t slot_stride;
   uint32_t chunk;                // as GroupLaunch::chunk
+  int dtype;                     // MGW_DTYPE_* of the gradients / arena
   uint32_t* pipe;                // [1] iteration, [2] CTA exit count, [3] ready-timeout flag
   const uint32_t* ready;         // G flags: group g ready for iteration i when >= i + 1
   uint32_t* group_done;          // G counters for end stamps (NULL: no timing)

@@ -28,12 +28,12 @@ namespace mgw {
 
 cudaError_t launch_group_allreduce(const GroupLaunch& L, int ctas_per_rank, bool two_shot,
                                    bool loopback, cudaStream_t stream);
-cudaError_t max_ctas_per_sm(int nranks, bool two_shot, bool loopback, int* out);
-cudaError_t launch_pack(const Tile* tiles, uint32_t n_tiles, float* const* grads, float* merge,
-                        uint64_t begin, float scale, int ctas, cudaStream_t stream);
+cudaError_t max_ctas_per_sm(int nranks, bool two_shot, bool loopback, int dtype, int* out);
+cudaError_t launch_pack(const Tile* tiles, uint32_t n_tiles, float* const* grads, void* merge,
+                        uint64_t begin, float scale, int dtype, int ctas, cudaStream_t stream);
 cudaError_t launch_unpack_sgd(const Tile* tiles, uint32_t n_tiles, float* const* grads,
-                              float* const* weights, const float* merge, uint64_t begin, float lr,
-                              int epi, int ctas, cudaStream_t stream);
+                              float* const* weights, const void* merge, uint64_t begin, float lr,
+                              int epi, int dtype, int ctas, cudaStream_t stream);
 cudaError_t launch_replay(unsigned long long* clock, unsigned long long deadline_ns, int first,
                           uint32_t* ready, cudaStream_t stream);
 cudaError_t launch_engine(const EngineLaunch& E, int ctas, cudaStream_t stream);
@@ -43,7 +43,7 @@ cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long lon
 cudaError_t launch_mark_ready(const uint32_t* pipe, uint32_t* flags, uint32_t g,
                               cudaStream_t stream);
 cudaError_t preload_kernels();
-cudaError_t engine_ctas_per_sm(int nranks, int* out);
+cudaError_t engine_ctas_per_sm(int nranks, int dtype, int* out);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, int ctas, cudaStream_t stream);
 
 std::atomic<uint64_t> g_kernel_launches{0};
@@ -93,7 +93,7 @@ struct mgw_comm {
   bool peers_ready = false;
   cudaStream_t stream = nullptr;  // calibrate / plain all-reduce
   unsigned long long* d_clock = nullptr;  // calibration spin clock
-  int occ_cache[2] = {0, 0};           // CTAs/SM of the one-shot / two-shot kernel
+  int occ_cache[2][2] = {{0, 0}, {0, 0}};  // [dtype][two_shot]           // CTAs/SM of the one-shot / two-shot kernel
   // cached single-buffer plan for mgw_allreduce
   mgw_plan* ar_plan = nullptr;
   float* ar_buf = nullptr;
@@ -103,6 +103,9 @@ struct mgw_comm {
 struct mgw_plan {
   mgw_comm* comm = nullptr;
   size_t L = 0;
+  int dtype = MGW_DTYPE_F32;        // gradient / arena element type
+  size_t esize = 4;                 // bytes per gradient element
+  uint64_t slot_stride = 0;         // arena slot stride in gradient elements
   int n_views = 1;
   std::vector<uint64_t> counts;
   std::vector<uint64_t> offs;       // L+1 padded element offsets
@@ -216,9 +219,9 @@ bool use_two_shot(const mgw_comm* c, uint64_t bytes, int algo) {
   return bytes > c->oneshot_max;
 }
 
-int grid_for(mgw_comm* c, uint32_t n_tiles, bool two_shot) {
-  int& occ = c->occ_cache[two_shot ? 1 : 0];
-  if (occ == 0) ck(max_ctas_per_sm(c->nranks, two_shot, c->loopback, &occ), "occupancy");
+int grid_for(mgw_comm* c, uint32_t n_tiles, bool two_shot, int dtype = MGW_DTYPE_F32) {
+  int& occ = c->occ_cache[dtype == MGW_DTYPE_BF16 ? 1 : 0][two_shot ? 1 : 0];
+  if (occ == 0) ck(max_ctas_per_sm(c->nranks, two_shot, c->loopback, dtype, &occ), "occupancy");
   int cap = std::max(1, occ) * c->num_sms;
   if (c->loopback) cap = std::max(1, cap / c->nranks);
   cap = std::min(cap, kMaxCtas);
@@ -228,7 +231,7 @@ int grid_for(mgw_comm* c, uint32_t n_tiles, bool two_shot) {
 
 uint64_t group_bytes(const mgw_plan* p, int g) {
   uint64_t s = 0;
-  for (size_t l = p->heads[g]; l < p->heads[g + 1]; ++l) s += p->counts[l] * sizeof(float);
+  for (size_t l = p->heads[g]; l < p->heads[g + 1]; ++l) s += p->counts[l] * p->esize;
   return s;
 }
 
@@ -245,14 +248,15 @@ void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStre
   L.scale = 1.0f / static_cast<float>(c->nranks);
   L.lr = lr;
   L.epilogue = epilogue;
-  L.slot_stride = c->arena_elems;
+  L.slot_stride = p->slot_stride;
   L.chunk = c->chunk_tiles;
+  L.dtype = p->dtype;
   for (int r = 0; r < p->n_views; ++r) {
     L.views[r] = make_view(c, r, p->d_grads + static_cast<size_t>(r) * p->L,
                            p->d_weights + static_cast<size_t>(r) * p->L);
   }
   const bool two = use_two_shot(c, group_bytes(p, g), algo);
-  ck(launch_group_allreduce(L, grid_for(c, L.n_tiles, two), two, c->loopback, stream),
+  ck(launch_group_allreduce(L, grid_for(c, L.n_tiles, two, p->dtype), two, c->loopback, stream),
      "group_allreduce launch");
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -274,7 +278,7 @@ void destroy_plan(mgw_plan* p) {
 }
 
 mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* weights,
-                     const uint64_t* counts, const uint8_t* tags) {
+                     const uint64_t* counts, const uint8_t* tags, int dtype = MGW_DTYPE_F32) {
   require(c != nullptr, "comm is NULL");
   require(L >= 1, "plan needs at least one layer");
   require(grads != nullptr && counts != nullptr && tags != nullptr, "NULL plan arrays");
@@ -283,18 +287,23 @@ mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* w
   auto* p = new mgw_plan();
   p->comm = c;
   p->L = L;
+  require(dtype == MGW_DTYPE_F32 || dtype == MGW_DTYPE_BF16, "dtype must be MGW_DTYPE_F32 or MGW_DTYPE_BF16");
+  p->dtype = dtype;
+  p->esize = dtype == MGW_DTYPE_BF16 ? 2 : 4;
+  p->slot_stride = c->arena_elems * (sizeof(float) / p->esize);  // the arena is reinterpreted
+  const uint64_t granule = 16 / p->esize;                         // layers start 16-byte aligned
   p->n_views = c->loopback ? c->nranks : 1;
   p->counts.assign(counts, counts + L);
   p->offs.resize(L + 1, 0);
   for (size_t l = 0; l < L; ++l) {
     require(tags[l] <= 1, "tags must be 0 or 1");
     require(counts[l] < (uint64_t{1} << 32), "layer too large (>= 2^32 elements)");
-    p->offs[l + 1] = p->offs[l] + ((counts[l] + 3) & ~uint64_t{3});
+    p->offs[l + 1] = p->offs[l] + ((counts[l] + granule - 1) & ~(granule - 1));
     if (l == 0 || tags[l] == 0) p->heads.push_back(l);
   }
   p->heads.push_back(L);
-  if (p->offs[L] > c->arena_elems) {
-    const std::string msg = "plan needs " + std::to_string(p->offs[L] * 4) +
+  if (p->offs[L] > p->slot_stride) {
+    const std::string msg = "plan needs " + std::to_string(p->offs[L] * p->esize) +
                             " arena bytes; communicator has " + std::to_string(c->arena_elems * 4);
     delete p;
     throw gradsched::ValidationError(msg);
@@ -487,6 +496,17 @@ int mgw_plan_create(mgw_comm* comm, size_t L, float* const* grads, float* const*
   MGW_CATCH
 }
 
+int mgw_plan_create_ex(mgw_comm* comm, size_t L, void* const* grads, float* const* weights,
+                       const uint64_t* counts, const uint8_t* tags, int dtype, mgw_plan** out) {
+  MGW_TRY {
+    require(out != nullptr, "out is NULL");
+    // the layer tables hold untyped device pointers; kernels reinterpret
+    // them as the plan's element type
+    *out = mgw::build_plan(comm, L, reinterpret_cast<float* const*>(grads), weights, counts, tags, dtype);
+  }
+  MGW_CATCH
+}
+
 int mgw_plan_destroy(mgw_plan* plan) {
   MGW_TRY {
     if (plan) cudaSetDevice(plan->comm->device);
@@ -514,21 +534,21 @@ int mgw_plan_group_span(const mgw_plan* p, int g, uint64_t* begin, uint64_t* cou
   MGW_CATCH
 }
 
-int mgw_pack(mgw_plan* p, int g, float scale, float* merge_buf, void* stream) {
+int mgw_pack(mgw_plan* p, int g, float scale, void* merge_buf, void* stream) {
   MGW_TRY {
     require(p != nullptr && merge_buf != nullptr && g >= 0 && g < p->G(), "bad pack arguments");
     mgw::set_device(p->comm);
     const uint32_t n = p->tile_first[g + 1] - p->tile_first[g];
     const int ctas = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(n, 4 * p->comm->num_sms)));
     ck(mgw::launch_pack(p->d_tiles + p->tile_first[g], n, p->d_grads, merge_buf,
-                        p->offs[p->heads[g]], scale, ctas, static_cast<cudaStream_t>(stream)),
+                        p->offs[p->heads[g]], scale, p->dtype, ctas, static_cast<cudaStream_t>(stream)),
        "pack launch");
     mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   }
   MGW_CATCH
 }
 
-int mgw_unpack_sgd(mgw_plan* p, int g, const float* merge_buf, float lr, int write_grad,
+int mgw_unpack_sgd(mgw_plan* p, int g, const void* merge_buf, float lr, int write_grad,
                    void* stream) {
   MGW_TRY {
     require(p != nullptr && merge_buf != nullptr && g >= 0 && g < p->G(), "bad unpack arguments");
@@ -537,7 +557,7 @@ int mgw_unpack_sgd(mgw_plan* p, int g, const float* merge_buf, float lr, int wri
     const int ctas = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(n, 4 * p->comm->num_sms)));
     const int epi = MGW_SGD | (write_grad ? MGW_WRITE_GRAD : 0);
     ck(mgw::launch_unpack_sgd(p->d_tiles + p->tile_first[g], n, p->d_grads, p->d_weights,
-                              merge_buf, p->offs[p->heads[g]], lr, epi, ctas,
+                              merge_buf, p->offs[p->heads[g]], lr, epi, p->dtype, ctas,
                               static_cast<cudaStream_t>(stream)),
        "unpack launch");
     mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
@@ -578,8 +598,9 @@ int mgw_allreduce(mgw_comm* c, float* buf, size_t n, int algo, void* stream) {
     L.scale = 1.0f;
     L.lr = 0.0f;
     L.epilogue = MGW_WRITE_GRAD;
-    L.slot_stride = c->arena_elems;
+    L.slot_stride = p->slot_stride;
     L.chunk = c->chunk_tiles;
+    L.dtype = MGW_DTYPE_F32;
     L.views[0] = mgw::make_view(c, 0, p->d_grads, p->d_weights);
     const bool two = mgw::use_two_shot(c, static_cast<uint64_t>(n) * 4, algo);
     ck(mgw::launch_group_allreduce(L, mgw::grid_for(c, L.n_tiles, two), two, false,
@@ -693,7 +714,7 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
   mgw_comm* c = p->comm;
   const int G = p->G();
   int occ = 1;
-  ck(engine_ctas_per_sm(c->nranks, &occ), "engine occupancy");
+  ck(engine_ctas_per_sm(c->nranks, p->dtype, &occ), "engine occupancy");
   // The engine runs concurrently with the compute stream, whose kernels must
   // still find SMs: measured on B200, a 1-thread replay kernel is NOT
   // scheduled next to engine CTAs when every SM holds one (the engine then
@@ -732,8 +753,9 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
   E.scale = 1.0f / static_cast<float>(c->nranks);
   E.lr = lr;
   E.epilogue = MGW_SGD;
-  E.slot_stride = c->arena_elems;
+  E.slot_stride = p->slot_stride;
   E.chunk = c->chunk_tiles;
+  E.dtype = p->dtype;
   E.pipe = pipe->d_pipe;
   E.ready = pipe->d_ready;
   E.group_done = timed ? pipe->d_group_done : nullptr;

@@ -26,9 +26,22 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
     return s.cuda_stream
 
 
-def padded_elems(counts: Sequence[int]) -> int:
-    """Merge-layout size: every layer starts on a 16-byte boundary."""
-    return sum((int(c) + 3) & ~3 for c in counts)
+F32, BF16 = 0, 1  # mgw_dtype (gradient / merge-arena element type)
+
+
+def padded_elems(counts: Sequence[int], dtype: int = F32) -> int:
+    """Merge-layout size in elements: every layer starts on a 16-byte
+    boundary (4 fp32 / 8 bf16 elements)."""
+    g = 8 if dtype == BF16 else 4
+    return sum((int(c) + g - 1) // g * g for c in counts)
+
+
+def dtype_of(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.bfloat16:
+        return BF16
+    raise TypeError(f"gradients must be float32 or bfloat16, got {t.dtype}")
 
 
 class Comm:
@@ -110,8 +123,9 @@ class Comm:
 class DevicePlan:
     """A merge plan bound to this rank's gradient / weight tensors.
 
-    grads / weights: one fp32 CUDA tensor per layer in forward order (for a
-    loopback comm: a list per emulated rank).
+    grads / weights: one CUDA tensor per layer in forward order (for a
+    loopback comm: a list per emulated rank). Gradients are fp32 or bf16
+    (all the same type); weights are fp32 master weights.
     """
 
     def __init__(self, comm: Comm, grads, weights, plan: MergePlan):
@@ -127,11 +141,16 @@ class DevicePlan:
         self._keep = (flat_g, flat_w)  # tensors must outlive the plan
         counts = [int(t.numel()) for t in flat_g[:L]]
         self.counts = counts
+        self.dtype = dtype_of(flat_g[0])
+        if any(dtype_of(t) != self.dtype for t in flat_g):
+            raise TypeError("all gradients of a plan must have the same dtype")
+        if flat_w is not None and any(t.dtype != torch.float32 for t in flat_w):
+            raise TypeError("weights must be float32 (master weights)")
         gp = arr(C.c_void_p, (t.data_ptr() for t in flat_g))
         wp = arr(C.c_void_p, (t.data_ptr() for t in flat_w)) if flat_w is not None else None
         h = C.c_void_p()
-        check(_lib.mgw_plan_create(comm.handle, L, gp, wp, arr(C.c_uint64, counts),
-                                   arr(C.c_uint8, (int(t) for t in plan.tags)), C.byref(h)))
+        check(_lib.mgw_plan_create_ex(comm.handle, L, gp, wp, arr(C.c_uint64, counts),
+                                      arr(C.c_uint8, (int(t) for t in plan.tags)), self.dtype, C.byref(h)))
         self.handle = h
         n = C.c_int()
         check(_lib.mgw_plan_num_groups(h, C.byref(n)))

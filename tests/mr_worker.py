@@ -64,6 +64,26 @@ def main():
                 failures.append(f"{algo} grads layer {l}")
         dp.close()
 
+    # bf16 gradients (fp32 master weights) over real NVLink: bit-exact vs the
+    # bf16 oracle, every algorithm
+    for algo in ("oneshot", "twoshot", "auto"):
+        g32, w_np = inputs(P)
+        g_np = [[pyoracle.f32_to_bf16(a) for a in per] for per in g32]
+        g_dev = [torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16) for a in g_np[rank]]
+        w_dev = [torch.from_numpy(a.copy()).cuda() for a in w_np[rank]]
+        dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+        for _ in range(2):
+            for g in reversed(range(dp.n_groups)):
+                dp.group_allreduce(g, LR, rt.SGD | rt.WRITE_GRAD, algo)
+            pyoracle.allreduce_sgd_bf16(g_np, w_np, tags, LR, write_grad=True)
+        torch.cuda.synchronize()
+        for l in range(len(COUNTS)):
+            if not np.array_equal(w_dev[l].cpu().numpy(), w_np[rank][l]):
+                failures.append(f"bf16 {algo} weights layer {l}")
+            if not np.array_equal(g_dev[l].view(torch.int16).cpu().numpy().view(np.uint16), g_np[rank][l]):
+                failures.append(f"bf16 {algo} grads layer {l}")
+        dp.close()
+
     # plain SUM all-reduce vs NCCL: bit-exact is not expected (NCCL's order
     # differs); bound |x - y| <= 1e-6 * sum_r |x_r| (SURVEY §7 vii)
     for n in (1 << 10, (1 << 20) + 3, 16 << 20):

@@ -111,3 +111,33 @@ def test_cpu_pipeline_runs_and_respects_replay_time():
     assert all(t >= 6e-3 for t in times)  # t_f + sum(t_b) replayed
     # 3 iterations of w -= 0.5 * 1 (P=1)
     assert np.all(weights[0][0] == -1.5)
+
+
+def test_oracle_bf16_rounding_is_round_to_nearest_even():
+    """The bf16 oracle's fp32 -> bf16 rounding (C and its numpy restatement)
+    against torch's conversion, on random values and on exact ties."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal(200000).astype(np.float32) * np.float32(1e3)
+    # exact ties: bf16 value + half an ulp, both parities of the kept bit
+    base = (rng.integers(0x0080, 0x7F00, 5000, dtype=np.uint32) << 16) | 0x8000
+    ties = base.view(np.float32)
+    x = np.concatenate([x, ties, -ties, np.float32([0.0, -0.0, 1e-40, -1e-40, 3.4e38])]).astype(np.float32)
+    want = torch.from_numpy(x.copy()).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    got = pyoracle.f32_to_bf16(x)
+    assert np.array_equal(got, want)
+    c = np.array([pyoracle.ORC.orc_f32_to_bf16(float(v)) for v in x[-6000:]], dtype=np.uint16)
+    assert np.array_equal(c, want[-6000:])
+    assert np.array_equal(pyoracle.bf16_to_f32(got), torch.from_numpy(want.view(np.int16)).view(torch.bfloat16).float().numpy())
+
+
+def test_oracle_bf16_allreduce_semantics():
+    """One rank-order bf16 reduction restated by hand on a tiny case."""
+    g = [[np.array([0x3F80, 0x4000, 0xC040], dtype=np.uint16)],   # 1, 2, -3
+         [np.array([0x3F80, 0x3F00, 0x4040], dtype=np.uint16)]]   # 1, 0.5, 3
+    w = [[np.zeros(3, dtype=np.float32)], [np.ones(3, dtype=np.float32)]]
+    pyoracle.allreduce_sgd_bf16(g, w, [0], 0.5, write_grad=True)
+    red = np.float32([1.0, 1.25, 0.0])
+    assert np.array_equal(pyoracle.bf16_to_f32(g[0][0]), red) and np.array_equal(g[0][0], g[1][0])
+    assert np.array_equal(w[0][0], -np.float32(0.5) * red) and np.array_equal(w[1][0], 1 - np.float32(0.5) * red)

@@ -240,3 +240,114 @@ def test_pipeline_step_io_copies_inputs_and_results():
         pipe.close()
     dp.close()
     comm.close()
+
+
+# ---- bf16 gradients: bit-exact vs the bf16 oracle ----------
+
+def _bf16_np(rng, counts, P):
+    return [[pyoracle.f32_to_bf16(rng.uniform(-1, 1, c).astype(np.float32)) for c in counts] for _ in range(P)]
+
+
+def _bf16_dev(arrays):
+    return [[torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16) for a in per] for per in arrays]
+
+
+def _bits(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+@pytest.mark.parametrize("algo", ["oneshot", "twoshot", "auto"])
+def test_bf16_fused_group_allreduce_bit_exact_vs_oracle(P, algo):
+    if P == 1 and algo != "auto":
+        pytest.skip("P=1 has no exchange")
+    rng = np.random.default_rng(300 + P)
+    counts = RAGGED
+    g_np, w_np = _bf16_np(rng, counts, P), _np(rng, counts, P)
+    g_dev, w_dev = _bf16_dev(g_np), _dev(w_np)
+    _, plan = _plan_for(counts, seed=P)
+    tags = [int(t) for t in plan.tags]
+    if P == 1:
+        comm = rt.Comm(0, 1, 0, 4 * rt.padded_elems(counts))
+        dp = rt.DevicePlan(comm, g_dev[0], w_dev[0], plan)
+    else:
+        comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
+        comm.set_oneshot_max(8 * 1024)
+        dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+    assert dp.dtype == rt.BF16
+    for it in range(3):
+        for g in reversed(range(dp.n_groups)):
+            dp.group_allreduce(g, LR, rt.SGD | rt.WRITE_GRAD, algo)
+        pyoracle.allreduce_sgd_bf16(g_np, w_np, tags, LR, write_grad=True)
+    torch.cuda.synchronize()
+    for r in range(P):
+        for l in range(len(counts)):
+            assert np.array_equal(_bits(g_dev[r][l]), g_np[r][l]), (r, l)
+            assert np.array_equal(w_dev[r][l].cpu().numpy(), w_np[r][l]), (r, l)
+    dp.close()
+    comm.close()
+
+
+def test_bf16_pack_unpack_bit_exact():
+    rng = np.random.default_rng(21)
+    counts = RAGGED
+    g_np = _bf16_np(rng, counts, 1)[0]
+    w_np = _np(rng, counts, 1)[0]
+    g_dev = _bf16_dev([g_np])[0]
+    w_dev = [torch.from_numpy(a.copy()).cuda() for a in w_np]
+    _, plan = _plan_for(counts)
+    comm = rt.Comm(0, 1, 0, 4 * rt.padded_elems(counts))
+    dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+    offs = pyoracle.merge_offsets_granule(counts, 8)
+    for g, members in enumerate(plan.groups()):
+        b, n, nbytes = dp.group_span(g)
+        assert b == offs[members[0]] and n == offs[members[-1] + 1] - b and nbytes == 2 * sum(counts[i] for i in members)
+        out = torch.zeros(max(n, 1), dtype=torch.bfloat16, device="cuda")
+        dp.pack(g, 0.5, out)
+        torch.cuda.synchronize()
+        want = pyoracle.pack_bf16(g_np, members[0], members[-1] + 1, 0.5)
+        got = _bits(out)[:n]
+        for l in members:  # compare the valid elements of every layer (padding is unspecified)
+            o = offs[l] - b
+            assert np.array_equal(got[o:o + counts[l]], want[o:o + counts[l]]), l
+        red = pyoracle.f32_to_bf16(rng.uniform(-1, 1, max(n, 1)).astype(np.float32))
+        red_dev = torch.from_numpy(red.view(np.int16).copy()).cuda().view(torch.bfloat16)
+        w_before = [w_dev[l].cpu().numpy().copy() for l in members]
+        dp.unpack_sgd(g, red_dev, LR, write_grad=True)
+        torch.cuda.synchronize()
+        for k, l in enumerate(members):
+            r = pyoracle.bf16_to_f32(red[offs[l] - b: offs[l] - b + counts[l]])
+            assert np.array_equal(w_dev[l].cpu().numpy(), (w_before[k] - (np.float32(LR) * r).astype(np.float32))), l
+            assert np.array_equal(_bits(g_dev[l]), red[offs[l] - b: offs[l] - b + counts[l]]), l
+    dp.close()
+    comm.close()
+
+
+@pytest.mark.parametrize("P,algo", [(4, "twoshot"), (2, "oneshot")])
+def test_bf16_large_message_matches_torch_rank_order(P, algo):
+    """32 Mi bf16 elements per rank: bit-exact against torch (fp32 widening,
+    rank-order fp32 sum, one bf16 rounding, fp32 SGD)."""
+    torch.manual_seed(10 + P)
+    counts = [32 * 1024 * 1024 - 3, 5, 1 << 20]
+    grads = [[(torch.rand(c, device="cuda") * 2 - 1).to(torch.bfloat16) for c in counts] for _ in range(P)]
+    weights = [[torch.rand(c, device="cuda") for c in counts] for _ in range(P)]
+    s = torch.tensor(1.0 / P, device="cuda")
+    lr = torch.tensor(LR, device="cuda")
+    want_w, want_g = [], []
+    for l in range(len(counts)):
+        acc = grads[0][l].float() * s
+        for r in range(1, P):
+            acc = acc + grads[r][l].float() * s
+        red = acc.to(torch.bfloat16)
+        want_g.append(red)
+        want_w.append([weights[r][l] - lr * red.float() for r in range(P)])
+    comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts, rt.BF16))
+    dp = rt.DevicePlan(comm, grads, weights, gs.MergePlan.all_merged(len(counts)))
+    dp.group_allreduce(0, LR, rt.SGD | rt.WRITE_GRAD, algo)
+    torch.cuda.synchronize()
+    for l in range(len(counts)):
+        for r in range(P):
+            assert torch.equal(weights[r][l], want_w[l][r]), (l, r)
+            assert torch.equal(grads[r][l], want_g[l]), (l, r)
+    dp.close()
+    comm.close()
