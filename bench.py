@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot"])
     ap.add_argument("--oneshot-max", type=int, default=0, help="0: the library default for N")
+    ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"],
+                    help="gradient / merge-arena type (bf16: fp32 accumulation, fp32 master weights)")
     ap.add_argument("--engine-ctas", type=int, default=-1,
                     help="-1: persistent comm engine, one CTA per SM; >0: that many CTAs; "
                          "0: one fused kernel launch per group")
@@ -249,19 +251,24 @@ def main():
     dev = torch.device("cuda", local)
     N = world
     trace = gs.load_trace(trace_path(args.trace))
+    bf16 = args.dtype == "bf16"
+    esz = 2 if bf16 else 4
+    gdt = torch.bfloat16 if bf16 else torch.float32
+    trace.bytes_per_element = esz  # the planner costs groups in gradient bytes (trace.hpp:50)
     counts = [l.params for l in trace.layers]
     L = len(counts)
-    total_bytes = 4 * sum(counts)
-    padded = rt.padded_elems(counts)
+    total_bytes = esz * sum(counts)
+    padded = rt.padded_elems(counts, rt.BF16 if bf16 else rt.F32)
+    granule = 16 // esz
 
-    # gradients: one flat fp32 buffer (16-byte aligned layer views, like a
-    # framework's flat grad buffer); weights: one allocation per layer
+    # gradients: one flat buffer (16-byte aligned layer views, like a
+    # framework's flat grad buffer); weights: fp32, one allocation per layer
     gen = torch.Generator(device=dev)
     gen.manual_seed(0x5EED0000 + rank)
-    flat_grad = torch.empty(padded, dtype=torch.float32, device=dev).uniform_(-1, 1, generator=gen)
+    flat_grad = torch.empty(padded, dtype=torch.float32, device=dev).uniform_(-1, 1, generator=gen).to(gdt)
     offs = [0]
     for c in counts:
-        offs.append(offs[-1] + ((c + 3) & ~3))
+        offs.append(offs[-1] + (c + granule - 1) // granule * granule)
     grads = [flat_grad[offs[i]:offs[i] + counts[i]] for i in range(L)]
     wgen = torch.Generator(device=dev)
     wgen.manual_seed(0xC0FFEE)
@@ -357,7 +364,7 @@ def main():
     # Each step: the step's gradients H2D from pinned host memory (captured in
     # the iteration graph on the comm branch, overlapping the forward replay;
     # every group kernel waits for it) and 16 result bytes D2H at the end.
-    host_grad = torch.empty(padded, dtype=torch.float32, pin_memory=True)
+    host_grad = torch.empty(padded, dtype=gdt, pin_memory=True)
     host_grad.copy_(flat_grad.cpu())
     host_out = torch.empty(4, dtype=torch.float32, pin_memory=True)
     out_src = weights[0][:4] if counts[0] >= 4 else flat_grad[:4]
@@ -376,8 +383,9 @@ def main():
     peaks = measured_peaks()
     gbytes = [dplans["mgwfbp"].group_span(g)[2] for g in range(dplans["mgwfbp"].n_groups)]
     kern_s = sum(group_ms) / 1e3
+    w_per_g = 4 / esz  # fp32 weight bytes per gradient byte
     if N == 1:
-        algo_bytes = sum(3 * b for b in gbytes)  # read grad, read W, write W
+        algo_bytes = sum((1 + 2 * w_per_g) * b for b in gbytes)  # read grad, read W, write W
         peak = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
         roof = {"bound": "hbm", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
     else:
@@ -392,7 +400,7 @@ def main():
             traffic = json.load(f).get("dram_bytes_per_launch")
     # asymptotic per-byte rate of the same fused kernel from the calibration
     # slope b (s/B): bytes that cross the bound per gradient byte / b
-    per_byte = 3.0 if N == 1 else 2 * (N - 1) / N
+    per_byte = (1 + 2 * w_per_g) if N == 1 else 2 * (N - 1) / N
     asym = per_byte / model.b / 1e9 if model.b > 0 else None
     roof.update({"kernel": ("engine_kernel/run_group (fused pack + push all-reduce + unpack/SGD), "
                             "per-group %globaltimer stamps" if args.engine_ctas
@@ -421,7 +429,7 @@ def main():
         big = [m for m in meas if m.size_bytes >= (1 << 20)]
         ncclt = []
         for m in big:
-            x = torch.ones(m.size_bytes // 4, dtype=torch.float32, device=dev)
+            x = torch.ones(m.size_bytes // esz, dtype=gdt, device=dev)
             for _ in range(3):
                 torch.distributed.all_reduce(x)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -446,14 +454,17 @@ def main():
         cpu = {"value": len(times) / sum(times), "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{len(times)} iterations of the CPU Algorithm-2 restatement (oracle/mgw_oracle.c, "
                          f"same trace/plan, P=1, {threads} threads)"
-                         + (f"; reference optimal_plan (oracle/_ref) {solver:.1f} us on 1 core" if solver else "")}
+                         + (f"; reference optimal_plan (oracle/_ref) {solver:.1f} us on 1 core" if solver else "")
+                         + ("; the CPU path reduces fp32 gradients (no bf16 CPU pipeline)" if bf16 else "")}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-            "data": "synthetic uniform[-1,1) fp32 gradients; backward replayed from B200-measured per-tensor t_b",
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "data": (f"synthetic uniform[-1,1) {args.dtype} gradients"
+                     + (" (fp32 accumulation, fp32 master weights)" if bf16 else "")
+                     + "; backward replayed from B200-measured per-tensor t_b"),
             "config": {"workload": args.trace, "trace": os.path.relpath(trace_path(args.trace), ROOT),
                        "layers": L, "params": sum(counts), "grad_bytes": total_bytes,
                        "plan": "optimal_plan on on-box calibrated (a, b)", "plan_sha256": digest[:16],
@@ -472,7 +483,7 @@ def main():
             "bus_gbs": bus,
             "roofline": roof,
             "cpu_baseline": cpu,
-            "e2e": {"value": N * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": padded * 4,
+            "e2e": {"value": N * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": padded * esz,
                     "d2h_bytes_per_step": 16},
             "gpu_launches": launches,
             "clocks": clocks,
