@@ -562,6 +562,111 @@ __device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, ui
   }
 }
 
+// ---- LL (flag-in-data) one-shot for small groups ----------------------------
+// Every 32-bit word of gradient data travels with a 32-bit epoch in ONE
+// naturally aligned 8-byte store (single-copy atomic), so a receiver that
+// sees the epoch sees the data: no barrier, no release/acquire round trip —
+// one NVLink trip per group. The epoch is the CTA's barrier count after the
+// launch's entry barrier (identical on every rank for CTA index b, strictly
+// increasing across launches; LL groups of one launch use disjoint packets).
+
+__device__ __forceinline__ uint64_t* ll_slot(const RankView& v, int q, int src) {
+  return reinterpret_cast<uint64_t*>(v.signal[q] + kSignalWords) + static_cast<uint64_t>(src) * kLLSlotPackets;
+}
+
+// The 4-element vector's raw gradient words: fp32 4 words, bf16 2.
+template <typename T>
+__device__ __forceinline__ void ll_send(uint64_t* dst, float4 x, uint32_t epoch) {
+  const uint64_t e = static_cast<uint64_t>(epoch) << 32;
+  if constexpr (sizeof(T) == 4) {
+    asm volatile("st.volatile.global.v2.b64 [%0], {%1, %2};" ::"l"(dst), "l"(e | __float_as_uint(x.x)),
+                 "l"(e | __float_as_uint(x.y))
+                 : "memory");
+    asm volatile("st.volatile.global.v2.b64 [%0], {%1, %2};" ::"l"(dst + 2), "l"(e | __float_as_uint(x.z)),
+                 "l"(e | __float_as_uint(x.w))
+                 : "memory");
+  } else {  // bf16 values are exact in fp32: repack the raw bits
+    const uint32_t w0 = (__float_as_uint(x.x) >> 16) | (__float_as_uint(x.y) & 0xffff0000u);
+    const uint32_t w1 = (__float_as_uint(x.z) >> 16) | (__float_as_uint(x.w) & 0xffff0000u);
+    asm volatile("st.volatile.global.v2.b64 [%0], {%1, %2};" ::"l"(dst), "l"(e | w0), "l"(e | w1) : "memory");
+  }
+}
+
+__device__ __forceinline__ bool ll_pair(const uint64_t* p, uint32_t epoch, uint32_t& w0, uint32_t& w1) {
+  uint64_t a, b;
+  asm volatile("ld.volatile.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+  w0 = static_cast<uint32_t>(a);
+  w1 = static_cast<uint32_t>(b);
+  return static_cast<uint32_t>(a >> 32) == epoch && static_cast<uint32_t>(b >> 32) == epoch;
+}
+
+// Spin until the vector's packets carry `epoch` (10 s timeout -> error flag).
+template <typename T>
+__device__ __forceinline__ float4 ll_recv(const uint64_t* src, uint32_t epoch, uint32_t* err) {
+  uint32_t w[4];
+  constexpr int kPairs = sizeof(T) == 4 ? 2 : 1;
+#pragma unroll
+  for (int k = 0; k < kPairs; ++k) {
+    if (!ll_pair(src + 2 * k, epoch, w[2 * k], w[2 * k + 1])) {
+      const uint64_t t0 = globaltimer_ns();
+      while (!ll_pair(src + 2 * k, epoch, w[2 * k], w[2 * k + 1])) {
+        if (globaltimer_ns() - t0 > kTimeoutNs) {
+          atomicExch(err, 1u);
+          break;
+        }
+      }
+    }
+  }
+  if constexpr (sizeof(T) == 4) {
+    return make_float4(__uint_as_float(w[0]), __uint_as_float(w[1]), __uint_as_float(w[2]), __uint_as_float(w[3]));
+  } else {
+    return unpack_bf16x4(w[0], w[1]);
+  }
+}
+
+// A small one-shot group over LL packets, all 16 warps. Work unit: one
+// kBlock-vector PART of a tile (one vector per thread), so even a 2-tile
+// group spreads over 8 CTAs — the group is latency-bound, not per-CTA
+// bandwidth-bound. Send the vector to every peer, then receive, rank-order
+// sum (own contribution in place), SGD. Tile t's packets start at
+// ll_pkt + (t.moff - mbase) * sizeof(T) / 4.
+constexpr uint32_t kLLParts = kTileElems / 4 / kBlock;  // parts per tile
+
+template <int P, typename T>
+__device__ __noinline__ void ll_group(const RankView& v, const Tile* tiles, uint32_t n_tiles, uint32_t ll_pkt,
+                                         uint32_t mbase, float scale, float lr, int epi, uint32_t cta,
+                                         uint32_t ncta, uint32_t epoch) {
+  constexpr uint32_t kW = sizeof(T);  // packets per 4-element vector
+  const int me = v.rank;
+  for (uint32_t u = cta; u < n_tiles * kLLParts; u += ncta) {
+    const Tile t = tiles[u / kLLParts];
+    const uint32_t i = (u % kLLParts) * kBlock + threadIdx.x;  // this thread's vector
+    const uint32_t nvec = (t.len + 3) >> 2;
+    if (i >= nvec) continue;
+    const uint32_t layer = t.layer & kLayerMask;
+    T* g = as<T>(v.grads[layer]);
+    const T* own = g + t.src;
+    float* w = v.weights[layer];
+    const uint32_t e = i * 4;
+    const uint64_t pkt = ll_pkt + static_cast<uint64_t>(t.moff - mbase) * sizeof(T) / 4 + static_cast<uint64_t>(i) * kW;
+    float4 x[1], wv[1];
+    x[0] = (!(t.layer & kGradUnaligned) && e + 4 <= t.len) ? ld4_stream<T>(own + e) : ld4_tail<T>(own + e, t.len - e);
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      if (q != me) ll_send<T>(ll_slot(v, q, me) + pkt, x[0], epoch);
+    }
+    load_w_batch<1>(t, i, kBlock, w, epi, wv);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+      const float4 xr = r == me ? x[0] : ll_recv<T>(ll_slot(v, me, r) + pkt, epoch, v.state + kStateError);
+      acc = r == 0 ? mul4(xr, scale) : add4(acc, mul4(xr, scale));
+    }
+    x[0] = round4<T>(acc);
+    apply_batch<1, T>(t, i, kBlock, x, wv, w, g, lr, epi);
+  }
+}
+
 // Everything a CTA needs to run groups: its barrier counter and, for the
 // producer warp, the TMA ring.
 struct CtaCtx {
@@ -683,7 +788,13 @@ template <int P, typename T>
 __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, const Tile* tiles,
                                           uint32_t n_tiles, uint64_t slot_stride, float scale,
                                           float lr, int epi, uint32_t cta, uint32_t ncta,
-                                          uint32_t chunk, CtaCtx& cx) {
+                                          uint32_t chunk, uint32_t ll_pkt, uint32_t mbase, CtaCtx& cx) {
+  if constexpr (P > 1) {
+    if (ll_pkt != kNoLL) {
+      ll_group<P, T>(v, tiles, n_tiles, ll_pkt, mbase, scale, lr, epi, cta, ncta, cx.count);
+      return;
+    }
+  }
   if constexpr (P == 1) {
     // Single rank: no exchange. grad x 1/P (= 1) straight into the epilogue;
     // all kB gradient and weight loads of a thread are in flight together.
@@ -742,7 +853,7 @@ __global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid
   CtaCtx cx;
   cta_ctx_init<P>(cx, v, dsmem, bars);
   run_group<P, T>(TWO_SHOT, v, L.tiles, L.n_tiles, L.slot_stride, L.scale, L.lr, L.epilogue,
-               blockIdx.x, gridDim.x, L.chunk, cx);
+                  blockIdx.x, gridDim.x, L.chunk, L.ll_pkt, L.mbase, cx);
   if constexpr (P > 1) store_cta_count(v, blockIdx.x, cx.count);
 }
 
@@ -762,7 +873,8 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
     const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
     const EngineGroup grp = E.groups[gi];
     const bool two = P > 1 && grp.two_shot != 0;
-    const uint32_t units = two ? (grp.n_tiles + P - 1) / P : grp.n_tiles;
+    const uint32_t units = two ? (grp.n_tiles + P - 1) / P
+                               : (grp.ll_pkt != kNoLL && P > 1 ? grp.n_tiles * kLLParts : grp.n_tiles);
     if (blockIdx.x >= units) continue;  // same on every rank: no barrier to skip
     if (threadIdx.x == 0) {
       // group gi is ready for iteration `iter` once its flag reached iter+1
@@ -783,7 +895,7 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
     }
     __syncthreads();
     run_group<P, T>(two, v, E.tiles + grp.tile_first, grp.n_tiles, E.slot_stride, E.scale, E.lr,
-                 E.epilogue, blockIdx.x, gridDim.x, E.chunk, cx);
+                    E.epilogue, blockIdx.x, gridDim.x, E.chunk, grp.ll_pkt, grp.mbase, cx);
     if (E.stamps != nullptr) {
       __syncthreads();
       if (threadIdx.x == 0) {

@@ -40,6 +40,13 @@ constexpr int kSignalWords = kMaxCtas * kMaxRanks;  // flag [cta][src rank]
 constexpr int kStateError = 2;
 constexpr int kStateCtaBase = 64;
 constexpr int kStateWords = kStateCtaBase + kMaxCtas;
+// LL (flag-in-data) area, right after the signal flags of every rank's
+// signal allocation: one slot per source rank of kLLSlotPackets 8-byte
+// packets {32-bit data word, 32-bit epoch}. Small one-shot groups travel as
+// packets (no barrier, no release/acquire round trip); LL doubles the bytes,
+// so a slot holds kLLSlotPackets * 4 bytes of gradient data per plan.
+constexpr uint64_t kLLSlotPackets = 1ull << 21;  // 16 MiB per source rank
+constexpr uint32_t kNoLL = 0xffffffffu;
 
 struct Tile {
   uint32_t layer;  // layer index | alignment flags
@@ -62,6 +69,8 @@ struct RankView {
 struct GroupLaunch {
   const Tile* tiles;     // this group's tiles
   uint32_t n_tiles;
+  uint32_t ll_pkt;       // first LL packet of the group (kNoLL: not an LL group)
+  uint32_t mbase;        // merge-layout element offset of the group's first element
   int nranks;
   float scale;           // 1/P, applied in the pack phase
   float lr;
@@ -77,7 +86,9 @@ struct EngineGroup {
   uint32_t tile_first;
   uint32_t n_tiles;
   uint32_t two_shot;
-  uint32_t pad;
+  uint32_t ll_pkt;       // kNoLL unless the group travels as LL packets (one-shot only)
+  uint32_t mbase;        // merge-layout element offset of the group's first element
+  uint32_t pad[3];
 };
 
 // The persistent comm engine (paper Algorithm 2's communication daemon, on

@@ -82,6 +82,7 @@ struct mgw_comm {
   uint64_t oneshot_max = 512 * 1024;
   int num_sms = 148;
   uint32_t chunk_tiles = 16;  // pipelined chunk per CTA (MGW_CHUNK_TILES overrides, for probing)
+  uint64_t ll_max = 64 << 10; // one-shot groups up to this many bytes use LL packets
   // own allocations (loopback: one per emulated rank)
   std::vector<float*> arenas;
   std::vector<uint32_t*> signals;
@@ -111,6 +112,7 @@ struct mgw_plan {
   std::vector<uint64_t> offs;       // L+1 padded element offsets
   std::vector<size_t> heads;        // G+1, ascending, heads[G] = L
   std::vector<uint32_t> tile_first; // G+1 tile ranges per group
+  std::vector<uint32_t> ll_pkt;     // G: first LL packet of a small group (kNoLL: too large / no room)
   mgw::Tile* d_tiles = nullptr;
   float** d_grads = nullptr;        // n_views * L
   float** d_weights = nullptr;      // n_views * L
@@ -206,6 +208,23 @@ uint64_t default_oneshot_max(int nranks) {
   return 1ull << 20;
 }
 
+// Signal allocation: the flags, then one LL slot per source rank.
+size_t signal_words(int nranks) {
+  return kSignalWords + static_cast<size_t>(nranks) * kLLSlotPackets * 2;
+}
+
+// Largest one-shot group that travels as LL packets (0 disables LL).
+// Measured on B200 (tools/probe_bw.py, engine, LL vs barrier one-shot): LL
+// wins up to 512 KiB at P = 2 (8.0 vs 10.7 us) and 128 KiB at P = 4 (8.5
+// vs 12.4 us); LL sends 2(P-1) x the bytes, so P = 8 gets 32 KiB.
+uint64_t default_ll_max(int nranks) {
+  const char* e = std::getenv("MGW_LL_MAX");
+  if (e != nullptr) return std::strtoull(e, nullptr, 10);
+  if (nranks <= 2) return 512ull << 10;
+  if (nranks <= 4) return 128ull << 10;
+  return 32ull << 10;
+}
+
 uint32_t default_chunk_tiles() {
   const char* e = std::getenv("MGW_CHUNK_TILES");
   const long v = e != nullptr ? std::strtol(e, nullptr, 10) : 0;
@@ -219,13 +238,14 @@ bool use_two_shot(const mgw_comm* c, uint64_t bytes, int algo) {
   return bytes > c->oneshot_max;
 }
 
-int grid_for(mgw_comm* c, uint32_t n_tiles, bool two_shot, int dtype = MGW_DTYPE_F32) {
+int grid_for(mgw_comm* c, uint32_t n_tiles, bool two_shot, int dtype = MGW_DTYPE_F32, bool ll = false) {
   int& occ = c->occ_cache[dtype == MGW_DTYPE_BF16 ? 1 : 0][two_shot ? 1 : 0];
   if (occ == 0) ck(max_ctas_per_sm(c->nranks, two_shot, c->loopback, dtype, &occ), "occupancy");
   int cap = std::max(1, occ) * c->num_sms;
   if (c->loopback) cap = std::max(1, cap / c->nranks);
   cap = std::min(cap, kMaxCtas);
-  const uint32_t units = two_shot ? (n_tiles + c->nranks - 1) / c->nranks : n_tiles;
+  const uint32_t units = two_shot ? (n_tiles + c->nranks - 1) / c->nranks
+                                  : (ll ? n_tiles * (kTileElems / 4 / kBlock) : n_tiles);
   return static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(units, cap)));
 }
 
@@ -256,7 +276,10 @@ void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStre
                            p->d_weights + static_cast<size_t>(r) * p->L);
   }
   const bool two = use_two_shot(c, group_bytes(p, g), algo);
-  ck(launch_group_allreduce(L, grid_for(c, L.n_tiles, two, p->dtype), two, c->loopback, stream),
+  L.ll_pkt = two ? kNoLL : p->ll_pkt[g];
+  L.mbase = static_cast<uint32_t>(p->offs[p->heads[g]]);
+  ck(launch_group_allreduce(L, grid_for(c, L.n_tiles, two, p->dtype, L.ll_pkt != kNoLL), two, c->loopback,
+                            stream),
      "group_allreduce launch");
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -336,6 +359,19 @@ mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* w
   }
   p->tile_first.push_back(static_cast<uint32_t>(tiles.size()));
   require(L <= kLayerMask, "too many layers");
+  // LL packets for the small groups, in backward (engine FIFO) order, while
+  // the LL slot has room; 4 data bytes per packet, padded layout
+  p->ll_pkt.assign(p->G(), kNoLL);
+  if (c->nranks > 1) {
+    uint64_t next = 0;
+    for (int g = p->G() - 1; g >= 0; --g) {
+      if (group_bytes(p, g) > c->ll_max) continue;
+      const uint64_t pk = (p->offs[p->heads[g + 1]] - p->offs[p->heads[g]]) * p->esize / 4;
+      if (next + pk > kLLSlotPackets) break;
+      p->ll_pkt[g] = static_cast<uint32_t>(next);
+      next += pk;
+    }
+  }
   ck(cudaMalloc(&p->d_tiles, std::max<size_t>(tiles.size(), 1) * sizeof(Tile)), "cudaMalloc(tiles)");
   if (!tiles.empty()) {
     ck(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice),
@@ -384,9 +420,10 @@ int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_co
     c->nranks = nranks;
     c->oneshot_max = mgw::default_oneshot_max(nranks);
     c->chunk_tiles = mgw::default_chunk_tiles();
+    c->ll_max = mgw::default_ll_max(nranks);
     mgw::init_common(c, device, arena_bytes);
     c->arenas.push_back(mgw::alloc_arena(c->arena_elems, nranks));
-    c->signals.push_back(mgw::alloc_zero_u32(mgw::kSignalWords));
+    c->signals.push_back(mgw::alloc_zero_u32(mgw::signal_words(nranks)));
     c->states.push_back(mgw::alloc_zero_u32(mgw::kStateWords));
     ck(cudaDeviceSynchronize(), "init sync");
     c->peer_arena[rank] = c->arenas[0];
@@ -405,11 +442,12 @@ int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_com
     c->nranks = nranks;
     c->oneshot_max = mgw::default_oneshot_max(nranks);
     c->chunk_tiles = mgw::default_chunk_tiles();
+    c->ll_max = mgw::default_ll_max(nranks);
     c->loopback = true;
     mgw::init_common(c, device, arena_bytes);
     for (int r = 0; r < nranks; ++r) {
       c->arenas.push_back(mgw::alloc_arena(c->arena_elems, nranks));
-      c->signals.push_back(mgw::alloc_zero_u32(mgw::kSignalWords));
+      c->signals.push_back(mgw::alloc_zero_u32(mgw::signal_words(nranks)));
       c->states.push_back(mgw::alloc_zero_u32(mgw::kStateWords));
     }
     ck(cudaDeviceSynchronize(), "init sync");
@@ -601,6 +639,8 @@ int mgw_allreduce(mgw_comm* c, float* buf, size_t n, int algo, void* stream) {
     L.slot_stride = p->slot_stride;
     L.chunk = c->chunk_tiles;
     L.dtype = MGW_DTYPE_F32;
+    L.ll_pkt = mgw::kNoLL;
+    L.mbase = 0;
     L.views[0] = mgw::make_view(c, 0, p->d_grads, p->d_weights);
     const bool two = mgw::use_two_shot(c, static_cast<uint64_t>(n) * 4, algo);
     ck(mgw::launch_group_allreduce(L, mgw::grid_for(c, L.n_tiles, two), two, false,
@@ -738,7 +778,8 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
     groups[g].tile_first = p->tile_first[g];
     groups[g].n_tiles = p->tile_first[g + 1] - p->tile_first[g];
     groups[g].two_shot = use_two_shot(c, group_bytes(p, g), algo) ? 1u : 0u;
-    groups[g].pad = 0;
+    groups[g].ll_pkt = groups[g].two_shot ? kNoLL : p->ll_pkt[g];
+    groups[g].mbase = static_cast<uint32_t>(p->offs[p->heads[g]]);
   }
   ck(cudaMalloc(&pipe->d_groups, g1 * sizeof(EngineGroup)), "cudaMalloc(groups)");
   ck(cudaMemcpy(pipe->d_groups, groups.data(), G * sizeof(EngineGroup), cudaMemcpyHostToDevice),
