@@ -200,8 +200,7 @@ static void reduce_layer(int P, float* const* grads, float* const* weights, size
     for (int r = 0; r < P; ++r) {
       float* w = weights[(size_t)r * L + l];
       if (w) {
-        const volatile float step = lr * acc; /* no contraction into an FMA */
-        w[j] = w[j] - step;
+        w[j] = w[j] - lr * acc; /* two roundings: -ffp-contract=off, no FMA */
       }
     }
     if (write_grad) {
@@ -265,8 +264,7 @@ void orc_allreduce_sgd_bf16(int P, uint16_t* const* grads, float* const* weights
       for (int r = 0; r < P; ++r) {
         float* w = weights[(size_t)r * L + l];
         if (w) {
-          const volatile float step = lr * red; /* no contraction into an FMA */
-          w[j] = w[j] - step;
+          w[j] = w[j] - lr * red; /* two roundings: -ffp-contract=off, no FMA */
         }
       }
       if (write_grad) {
@@ -313,7 +311,9 @@ static void cpu_group(pipe_ctx* c, size_t g) {
     for (size_t l = first; l < last; ++l) {
       float* dst = m + (c->offs[l] - base);
       const uint64_t padded = c->offs[l + 1] - c->offs[l];
-      for (uint64_t j = 0; j < padded; ++j) dst[j] = j < c->counts[l] ? gr[l][j] * scale : 0.0f;
+      const uint64_t cnt = c->counts[l];
+      for (uint64_t j = 0; j < cnt; ++j) dst[j] = gr[l][j] * scale;
+      for (uint64_t j = cnt; j < padded; ++j) dst[j] = 0.0f;
     }
   }
   const long long n = (long long)span;
@@ -329,10 +329,7 @@ static void cpu_group(pipe_ctx* c, size_t g) {
     for (int r = 0; r < c->P; ++r) {
       float* w = c->weights[(size_t)r * c->L + l];
 #pragma omp parallel for num_threads(c->threads) schedule(static) if (cnt > 65536)
-      for (long long j = 0; j < cnt; ++j) {
-        const volatile float step = c->lr * red[j];
-        w[j] = w[j] - step;
-      }
+      for (long long j = 0; j < cnt; ++j) w[j] = w[j] - c->lr * red[j]; /* -ffp-contract=off */
     }
   }
 }
@@ -362,7 +359,8 @@ int orc_pipeline_run(int P, float* const* grads, float* const* weights, const ui
   pipe_ctx c;
   memset(&c, 0, sizeof c);
   c.P = P;
-  c.threads = threads < 1 ? 1 : threads;
+  /* the calling thread spins on the replay clock: leave it a core */
+  c.threads = threads > 1 ? threads - 1 : 1;
   c.lr = lr;
   c.grads = grads;
   c.weights = weights;
