@@ -243,7 +243,7 @@ int mgw_pipeline_stamps(mgw_pipeline* pipe, uint64_t* stamps_2g);
  * replay, the framework marks each group ready on its compute stream after
  * the backward of the group's layers (e.g. from autograd post-accumulate
  * hooks). Per iteration: mgw_engine_begin (launch the engine after the work
- * queued on after_stream), mgw_engine_mark_ready per group (1-thread kernel
+ * queued on after_stream; NULL = the legacy default stream), mgw_engine_mark_ready per group (1-thread kernel
  * on the compute stream; groups may complete in any order, they are reduced
  * FIFO in backward order), mgw_engine_join (stream waits until every group's
  * SGD is done). engine_ctas > 0 should be small so the backward keeps SMs.
@@ -254,6 +254,11 @@ int mgw_engine_create(mgw_plan* plan, float lr, int algo, int engine_ctas, int r
 int mgw_engine_begin(mgw_pipeline* engine, void* after_stream);
 int mgw_engine_mark_ready(mgw_pipeline* engine, int group, void* stream);
 int mgw_engine_join(mgw_pipeline* engine, void* stream);
+/* Leave groups [0, n_tail) — the last ones the backward makes ready — to
+ * the caller: the engine reduces groups [n_tail, G) only, and after
+ * mgw_engine_join the caller runs mgw_group_allreduce for the tail groups at
+ * full width (the backward no longer needs the SMs then). */
+int mgw_engine_set_tail(mgw_pipeline* engine, int n_tail);
 /* Synchronise the engine and report a barrier / ready timeout as an error. */
 int mgw_engine_check(mgw_pipeline* engine);
 

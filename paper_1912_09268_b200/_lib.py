@@ -116,6 +116,7 @@ mgw_engine_create = _proto("mgw_engine_create", [vp, C.c_float, C.c_int, C.c_int
 mgw_engine_begin = _proto("mgw_engine_begin", [vp, vp])
 mgw_engine_mark_ready = _proto("mgw_engine_mark_ready", [vp, C.c_int, vp])
 mgw_engine_join = _proto("mgw_engine_join", [vp, vp])
+mgw_engine_set_tail = _proto("mgw_engine_set_tail", [vp, C.c_int])
 mgw_engine_check = _proto("mgw_engine_check", [vp])
 mgw_kernel_launches = _proto("mgw_kernel_launches", [], C.c_uint64)
 

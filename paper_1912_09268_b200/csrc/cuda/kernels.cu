@@ -869,7 +869,7 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
   CtaCtx cx;
   cta_ctx_init<P>(cx, v, dsmem, bars);
   const uint32_t iter = s_iter;
-  for (uint32_t k = 0; k < E.G; ++k) {
+  for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
     const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
     const EngineGroup grp = E.groups[gi];
     const bool two = P > 1 && grp.two_shot != 0;

@@ -99,6 +99,7 @@ struct EngineLaunch {
   const Tile* tiles;
   const EngineGroup* groups;     // ascending group index
   uint32_t G;
+  uint32_t g_lo;                 // the engine runs groups [g_lo, G) (the rest: caller's tail launches)
   int nranks;
   float scale;
   float lr;

@@ -1133,10 +1133,9 @@ int mgw_engine_begin(mgw_pipeline* pipe, void* after_stream) {
   MGW_TRY {
     require(pipe != nullptr && pipe->manual, "not a host-driven engine");
     mgw::set_device(pipe->plan->comm);
-    if (after_stream != nullptr) {
-      ck(cudaEventRecord(pipe->fork, static_cast<cudaStream_t>(after_stream)), "fork");
-      ck(cudaStreamWaitEvent(pipe->comm, pipe->fork, 0), "fork wait");
-    }
+    // NULL is the legacy default stream (torch's default), not "no stream"
+    ck(cudaEventRecord(pipe->fork, static_cast<cudaStream_t>(after_stream)), "fork");
+    ck(cudaStreamWaitEvent(pipe->comm, pipe->fork, 0), "fork wait");
     ck(mgw::launch_engine(pipe->args, pipe->engine_ctas, pipe->comm), "engine launch");
     mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   }
@@ -1162,6 +1161,15 @@ int mgw_engine_join(mgw_pipeline* pipe, void* stream) {
     mgw::set_device(pipe->plan->comm);
     ck(cudaEventRecord(pipe->join, pipe->comm), "join");
     ck(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pipe->join, 0), "join wait");
+  }
+  MGW_CATCH
+}
+
+int mgw_engine_set_tail(mgw_pipeline* pipe, int n_tail) {
+  MGW_TRY {
+    require(pipe != nullptr && pipe->manual, "not a host-driven engine");
+    require(n_tail >= 0 && n_tail <= pipe->plan->G(), "tail group count out of range");
+    pipe->args.g_lo = static_cast<uint32_t>(n_tail);
   }
   MGW_CATCH
 }

@@ -37,9 +37,12 @@ from .runtime import ALGO, Comm, DevicePlan, padded_elems
 class MGWFBP:
     def __init__(self, model: torch.nn.Module, comm: Comm, lr: float, plan: Optional[MergePlan] = None,
                  algo: str = "auto", engine_ctas: int = 8, record_group_times: bool = False,
-                 params: Optional[List[torch.nn.Parameter]] = None):
+                 params: Optional[List[torch.nn.Parameter]] = None, tail_groups: int = 1):
         """params: the layer order of the plan / trace (forward order; the
-        backward visits it last to first). Default: model.parameters()."""
+        backward visits it last to first). Default: model.parameters().
+        tail_groups: the last groups the backward makes ready (groups
+        0..tail_groups-1) are reduced after the backward by a full-width
+        fused kernel instead of the few-CTA engine — the SMs are free then."""
         self.params: List[torch.nn.Parameter] = (list(params) if params is not None else
                                                  [p for p in model.parameters() if p.requires_grad])
         for p in self.params:
@@ -65,7 +68,10 @@ class MGWFBP:
         check(_lib.mgw_engine_create(self.dplan.handle, lr, ALGO[algo], engine_ctas,
                                      int(record_group_times), C.byref(h)))
         self.handle = h
+        self.lr, self.algo = lr, algo
         self.groups = self.plan.groups()
+        self.tail = max(0, min(int(tail_groups), len(self.groups)))
+        check(_lib.mgw_engine_set_tail(h, self.tail))
         self.group_of = [0] * L
         for g, members in enumerate(self.groups):
             for i in members:
@@ -80,12 +86,16 @@ class MGWFBP:
         def hook(_p):
             g = self.group_of[i]
             self.remaining[g] -= 1
-            if self.remaining[g] == 0:
+            if self.remaining[g] == 0 and g >= self.tail:
                 stream = torch.cuda.current_stream().cuda_stream
                 if self._lazy_launch and not self._launched:
                     # start the engine with the first finished group: the
-                    # forward pass keeps every SM
-                    check(_lib.mgw_engine_begin(self.handle, None))
+                    # forward pass keeps every SM. Ordered after the compute
+                    # stream's queued work — in particular the previous
+                    # iteration's full-width tail launches, whose CTAs must
+                    # all be resident (an engine holding SMs while waiting
+                    # for marks queued behind them would deadlock).
+                    check(_lib.mgw_engine_begin(self.handle, stream))
                     self._launched = True
                 check(_lib.mgw_engine_mark_ready(self.handle, g, stream))
         return hook
@@ -112,12 +122,14 @@ class MGWFBP:
     def end(self) -> None:
         """Make the current stream wait until every group's SGD is applied."""
         stream = torch.cuda.current_stream().cuda_stream
-        missing = [g for g, r in enumerate(self.remaining) if r != 0]
+        missing = [g for g, r in enumerate(self.remaining) if r != 0 and g >= self.tail]
         for g in missing:  # parameters that got no gradient this iteration
             check(_lib.mgw_engine_mark_ready(self.handle, g, stream))
         if not self._launched:
             check(_lib.mgw_engine_begin(self.handle, stream))
         check(_lib.mgw_engine_join(self.handle, stream))
+        for g in reversed(range(self.tail)):  # backward order, full width
+            check(_lib.mgw_group_allreduce(self.dplan.handle, g, self.lr, 1, ALGO[self.algo], stream))
         self._iters += 1
 
     def check(self) -> None:

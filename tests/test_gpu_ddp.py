@@ -56,6 +56,7 @@ def test_real_backward_sgd_matches_pytorch_p1(plan_kind):
     sync.check()
     for a, b in zip(model.parameters(), ref.parameters()):
         assert torch.equal(a, b)
-    assert all(t > 0 for t in sync.group_times_ms())
+    times = sync.group_times_ms()
+    assert all(t > 0 for t in times[sync.tail:])  # engine groups (the tail runs full width after join)
     sync.close()
     comm.close()

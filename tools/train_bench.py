@@ -1,5 +1,5 @@
 """Real-training comparison (paper §6 "real experiments"):
-a torchvision model trained with synthetic data on N GPUs (torchrun, one
+a torchvision model (or BERT-large pre-training) trained with synthetic data on N GPUs (torchrun, one
 process per GPU), gradients synchronised by
   ddp        torch DistributedDataParallel (NCCL, 25 MB buckets) + torch SGD
   mgwfbp     this repo's persistent comm engine, optimal merge plan from the
@@ -30,10 +30,8 @@ from paper_1912_09268_b200 import runtime as rt  # noqa: E402
 from paper_1912_09268_b200.ddp import MGWFBP  # noqa: E402
 
 
-def build(name):
-    import torchvision
-
-    return getattr(torchvision.models, name)(weights=None)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from extract_traces import build, loss_of, make_batch  # noqa: E402  (same models / inputs as the traces)
 
 
 def time_loop(step, iters, warmup):
@@ -60,19 +58,20 @@ def main():
     ap.add_argument("--engine-ctas", type=int, default=8)
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--strategies", default="ddp,mgwfbp,wfbp,single")
+    ap.add_argument("--tail-groups", type=int, default=1)
+    ap.add_argument("--debug", action="store_true")
     args = ap.parse_args()
     rank, N, local = D.init("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     torch.backends.cudnn.benchmark = True
-    x = torch.randn(args.batch, 3, 224, 224, device=dev)
-    y = torch.randint(0, 1000, (args.batch,), device=dev)
+    batch = make_batch(args.model, args.batch, dev)
     trace = gs.load_trace(os.path.join(ROOT, "traces", f"{args.model}.json"))
     results = {}
 
     def fwd_bwd(model):
         with torch.autocast("cuda", dtype=torch.bfloat16):
-            loss = torch.nn.functional.cross_entropy(model(x), y)
+            loss = loss_of(args.model, model, batch)
         loss.backward()
 
     for strat in args.strategies.split(","):
@@ -112,7 +111,18 @@ def main():
                 plan, extra = gs.MergePlan.all_normal(len(params)), {}
             else:
                 plan, extra = gs.MergePlan.all_merged(len(params)), {}
-            sync = MGWFBP(model, comm, args.lr, plan=plan, engine_ctas=args.engine_ctas, params=params)
+            sync = MGWFBP(model, comm, args.lr, plan=plan, engine_ctas=args.engine_ctas, params=params,
+                          tail_groups=args.tail_groups)
+            if args.debug:
+                import time
+                for k in range(4):
+                    t0 = time.time()
+                    sync.begin()
+                    fwd_bwd(model)
+                    sync.end()
+                    torch.cuda.synchronize()
+                    print(f"[rank {rank}] {strat} debug step {k} {time.time() - t0:.3f}s", flush=True)
+                sync.check()
 
             def step():
                 sync.begin()
@@ -124,7 +134,7 @@ def main():
             results[strat] = {"iter_ms": ms, "groups": len(plan.groups()), **extra}
             sync.close()
             comm.close()
-        results[strat]["images_per_s"] = N * args.batch / (results[strat]["iter_ms"] / 1e3)
+        results[strat]["samples_per_s"] = N * args.batch / (results[strat]["iter_ms"] / 1e3)
         del model
         torch.cuda.empty_cache()
     if rank == 0:
