@@ -191,6 +191,10 @@ int mgw_group_allreduce(mgw_plan* plan, int group, float lr, int epilogue, int a
  * B200-measured crossover for the communicator's rank count). */
 int mgw_comm_set_oneshot_max(mgw_comm* comm, uint64_t bytes);
 int mgw_comm_get_oneshot_max(const mgw_comm* comm, uint64_t* bytes);
+/* Cap on the CTAs per rank of a standalone fused launch (mgw_group_allreduce,
+ * mgw_allreduce); 0 = one per SM (default). A real backward that launches
+ * groups while it runs leaves the other SMs to the compute kernels. */
+int mgw_comm_set_max_ctas(mgw_comm* comm, int max_ctas);
 
 /* Backward-replay pipeline (paper Algorithm 2): a compute stream spins
  * until each group head's ready time (t_f + backward of the layers above,

@@ -76,6 +76,7 @@ mgw_comm_open_peers = _proto("mgw_comm_open_peers", [vp, vp])
 mgw_comm_destroy = _proto("mgw_comm_destroy", [vp])
 mgw_comm_set_oneshot_max = _proto("mgw_comm_set_oneshot_max", [vp, C.c_uint64])
 mgw_comm_get_oneshot_max = _proto("mgw_comm_get_oneshot_max", [vp, u64p])
+mgw_comm_set_max_ctas = _proto("mgw_comm_set_max_ctas", [vp, C.c_int])
 mgw_plan_create = _proto(
     "mgw_plan_create", [vp, C.c_size_t, C.POINTER(vp), C.POINTER(vp), u64p, u8p, C.POINTER(vp)]
 )

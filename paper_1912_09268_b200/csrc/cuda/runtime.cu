@@ -83,6 +83,7 @@ struct mgw_comm {
   int num_sms = 148;
   uint32_t chunk_tiles = 16;  // pipelined chunk per CTA (MGW_CHUNK_TILES overrides, for probing)
   uint64_t ll_max = 64 << 10; // one-shot groups up to this many bytes use LL packets
+  int max_ctas = 0;           // cap on the CTAs of a standalone group launch (0: one per SM)
   // own allocations (loopback: one per emulated rank)
   std::vector<float*> arenas;
   std::vector<uint32_t*> signals;
@@ -244,6 +245,7 @@ int grid_for(mgw_comm* c, uint32_t n_tiles, bool two_shot, int dtype = MGW_DTYPE
   int cap = std::max(1, occ) * c->num_sms;
   if (c->loopback) cap = std::max(1, cap / c->nranks);
   cap = std::min(cap, kMaxCtas);
+  if (c->max_ctas > 0) cap = std::min(cap, c->max_ctas);
   const uint32_t units = two_shot ? (n_tiles + c->nranks - 1) / c->nranks
                                   : (ll ? n_tiles * (kTileElems / 4 / kBlock) : n_tiles);
   return static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(units, cap)));
@@ -496,6 +498,14 @@ int mgw_comm_set_oneshot_max(mgw_comm* c, uint64_t bytes) {
   MGW_TRY {
     require(c != nullptr, "comm is NULL");
     c->oneshot_max = bytes;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_set_max_ctas(mgw_comm* c, int max_ctas) {
+  MGW_TRY {
+    require(c != nullptr && max_ctas >= 0, "bad communicator / CTA cap");
+    c->max_ctas = max_ctas;
   }
   MGW_CATCH
 }

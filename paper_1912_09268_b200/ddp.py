@@ -37,12 +37,20 @@ from .runtime import ALGO, Comm, DevicePlan, padded_elems
 class MGWFBP:
     def __init__(self, model: torch.nn.Module, comm: Comm, lr: float, plan: Optional[MergePlan] = None,
                  algo: str = "auto", engine_ctas: int = 8, record_group_times: bool = False,
-                 params: Optional[List[torch.nn.Parameter]] = None, tail_groups: int = 1):
+                 params: Optional[List[torch.nn.Parameter]] = None, tail_groups: int = 1,
+                 mode: str = "engine", launch_ctas: int = 16):
         """params: the layer order of the plan / trace (forward order; the
         backward visits it last to first). Default: model.parameters().
         tail_groups: the last groups the backward makes ready (groups
         0..tail_groups-1) are reduced after the backward by a full-width
-        fused kernel instead of the few-CTA engine — the SMs are free then."""
+        fused kernel instead of the few-CTA engine — the SMs are free then.
+        mode: "engine" — the persistent comm engine (engine_ctas CTAs for the
+        whole backward); "launch" — one fused launch per group on a comm
+        stream the moment the group is complete (launch_ctas CTAs, SMs held
+        only while a group is in flight)."""
+        if mode not in ("engine", "launch"):
+            raise ValueError("mode must be 'engine' or 'launch'")
+        self.mode, self.launch_ctas, self.comm = mode, int(launch_ctas), comm
         self.params: List[torch.nn.Parameter] = (list(params) if params is not None else
                                                  [p for p in model.parameters() if p.requires_grad])
         for p in self.params:
@@ -81,12 +89,26 @@ class MGWFBP:
         self._launched = False
         self._lazy_launch = False
         self._hooks = [p.register_post_accumulate_grad_hook(self._hook(i)) for i, p in enumerate(self.params)]
+        if mode == "launch":
+            self.comm_stream = torch.cuda.Stream(device=dev)
+            self._events = [torch.cuda.Event() for _ in range(len(self.groups) + 1)]
+
+    def _launch(self, g: int, stream) -> None:
+        """launch mode: group g on the comm stream after the work queued on `stream`."""
+        ev = self._events[g]
+        ev.record(torch.cuda.ExternalStream(stream) if isinstance(stream, int) else stream)
+        self.comm_stream.wait_event(ev)
+        self.comm.set_max_ctas(self.launch_ctas)
+        check(_lib.mgw_group_allreduce(self.dplan.handle, g, self.lr, 1, ALGO[self.algo],
+                                       self.comm_stream.cuda_stream))
 
     def _hook(self, i: int):
         def hook(_p):
             g = self.group_of[i]
             self.remaining[g] -= 1
-            if self.remaining[g] == 0 and g >= self.tail:
+            if self.remaining[g] == 0 and g >= self.tail and self.mode == "launch":
+                self._launch(g, torch.cuda.current_stream())
+            elif self.remaining[g] == 0 and g >= self.tail:
                 stream = torch.cuda.current_stream().cuda_stream
                 if self._lazy_launch and not self._launched:
                     # start the engine with the first finished group: the
@@ -123,11 +145,19 @@ class MGWFBP:
         """Make the current stream wait until every group's SGD is applied."""
         stream = torch.cuda.current_stream().cuda_stream
         missing = [g for g, r in enumerate(self.remaining) if r != 0 and g >= self.tail]
-        for g in missing:  # parameters that got no gradient this iteration
-            check(_lib.mgw_engine_mark_ready(self.handle, g, stream))
-        if not self._launched:
-            check(_lib.mgw_engine_begin(self.handle, stream))
-        check(_lib.mgw_engine_join(self.handle, stream))
+        if self.mode == "launch":
+            for g in reversed(missing):  # parameters that got no gradient this iteration
+                self._launch(g, torch.cuda.current_stream())
+            done = self._events[-1]
+            done.record(self.comm_stream)
+            torch.cuda.current_stream().wait_event(done)
+            self.comm.set_max_ctas(0)
+        else:
+            for g in missing:  # parameters that got no gradient this iteration
+                check(_lib.mgw_engine_mark_ready(self.handle, g, stream))
+            if not self._launched:
+                check(_lib.mgw_engine_begin(self.handle, stream))
+            check(_lib.mgw_engine_join(self.handle, stream))
         for g in reversed(range(self.tail)):  # backward order, full width
             check(_lib.mgw_group_allreduce(self.dplan.handle, g, self.lr, 1, ALGO[self.algo], stream))
         self._iters += 1

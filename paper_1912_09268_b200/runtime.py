@@ -79,6 +79,10 @@ class Comm:
     def set_oneshot_max(self, nbytes: int) -> None:
         check(_lib.mgw_comm_set_oneshot_max(self.handle, int(nbytes)))
 
+    def set_max_ctas(self, n: int) -> None:
+        """Cap the CTAs of standalone fused launches (0: one per SM)."""
+        check(_lib.mgw_comm_set_max_ctas(self.handle, int(n)))
+
     @property
     def oneshot_max(self) -> int:
         v = C.c_uint64()

@@ -128,9 +128,14 @@ def main():
     model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.ReLU(), torch.nn.Linear(256, 10)).cuda()
     L = len(list(model.parameters()))
     mplan = gs.MergePlan([gs.LayerTag(0 if i % 2 == 0 else 1) for i in range(L)])
-    sync = MGWFBP(model, comm, LR, plan=mplan, engine_ctas=8)
     gen = torch.Generator(device="cuda").manual_seed(100 + rank)
-    for step in range(3):
+    for step in range(6):
+        if step % 3 == 0:  # steps 0-2: persistent engine; 3-5: one launch per group
+            if step:
+                sync.check()
+                sync.close()
+            sync = MGWFBP(model, comm, LR, plan=mplan, engine_ctas=8, mode="engine" if step == 0 else "launch",
+                          launch_ctas=4)
         w_before = [p.detach().cpu().numpy().copy() for p in model.parameters()]
         x = torch.randn(16, 64, device="cuda", generator=gen)
         y = torch.randint(0, 10, (16,), device="cuda", generator=gen)

@@ -59,6 +59,8 @@ def main():
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--strategies", default="ddp,mgwfbp,wfbp,single")
     ap.add_argument("--tail-groups", type=int, default=1)
+    ap.add_argument("--mode", default="engine", choices=["engine", "launch"])
+    ap.add_argument("--launch-ctas", type=int, default=16)
     ap.add_argument("--debug", action="store_true")
     args = ap.parse_args()
     rank, N, local = D.init("nccl")
@@ -99,7 +101,12 @@ def main():
             comm = rt.Comm(rank, N, local, 4 * rt.padded_elems(counts))
             if strat == "mgwfbp":
                 sizes = [4096 << k for k in range(0, 20, 2) if (4096 << k) <= 4 * rt.padded_elems(counts)]
-                meas = comm.calibrate_engine(sizes, warmup=1, reps=3, engine_ctas=args.engine_ctas)
+                if args.mode == "launch":  # the cost of one fused launch with launch_ctas CTAs
+                    comm.set_max_ctas(args.launch_ctas)
+                    meas = comm.calibrate(sizes, warmup=1, reps=3)
+                    comm.set_max_ctas(0)
+                else:
+                    meas = comm.calibrate_engine(sizes, warmup=1, reps=3, engine_ctas=args.engine_ctas)
                 t = torch.tensor([m.time_sec for m in meas], dtype=torch.float64, device=dev)
                 if N > 1:
                     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -112,7 +119,7 @@ def main():
             else:
                 plan, extra = gs.MergePlan.all_merged(len(params)), {}
             sync = MGWFBP(model, comm, args.lr, plan=plan, engine_ctas=args.engine_ctas, params=params,
-                          tail_groups=args.tail_groups)
+                          tail_groups=args.tail_groups, mode=args.mode, launch_ctas=args.launch_ctas)
             if args.debug:
                 import time
                 for k in range(4):
@@ -139,7 +146,8 @@ def main():
         torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps({"model": args.model, "batch_per_gpu": args.batch, "n_gpus": N,
-                          "engine_ctas": args.engine_ctas, "results": results}), flush=True)
+                          "mode": args.mode, "engine_ctas": args.engine_ctas, "launch_ctas": args.launch_ctas,
+                          "tail_groups": args.tail_groups, "results": results}), flush=True)
     dist.destroy_process_group() if dist.is_initialized() else None
 
 
