@@ -1,26 +1,31 @@
 // mgwfbp-b200 sm_100a kernels.
 //
-//  run_group<P>  — THE hot op, shared by both launch styles: for one merge
-//      group, pack (gather layer grads x 1/P) fused with a push over NVLink
-//      into the peers' merge arenas -> rank-order reduction from local HBM ->
-//      unpack + SGD into the layer weights.
+//  run_group<P, T>  — THE hot op, shared by both launch styles: for one
+//      merge group, the gradient push over NVLink into the peers' merge
+//      arenas -> rank-order reduction (x 1/P per source, fp32) from local HBM
+//      -> unpack + SGD into the fp32 layer weights. T = float or bf16
+//      gradients. Warp roles: a producer warp pushes gradients with TMA bulk
+//      copies (global -> smem -> peer), 15 data warps reduce / apply / push
+//      all-gather results.
 //        one-shot: every rank pushes its tiles to every rank; 1 barrier per
-//          chunk.
-//        two-shot: tile t is owned by rank t % P; ranks push each tile to its
+//          chunk of 16 tiles per CTA.
+//        two-shot: tile s*P+q is owned by rank q; ranks push each tile to its
 //          owner (reduce-scatter), owners reduce + push the result to every
-//          peer (all-gather) fused with SGD; 2 barriers per chunk.
-//      A CTA walks its tiles in 256 KiB CHUNKS, software-pipelined: chunk
-//      c+1's posted NVLink stores are issued before chunk c's local work.
-//  engine_kernel<P> — the persistent comm engine: one launch per iteration
-//      runs every group in backward order as soon as the compute side marks
-//      its head ready (paper Algorithm 2's daemon thread, on the GPU; no
-//      per-group launch latency).
-//  group_allreduce_kernel<P, TWO_SHOT, LOOPBACK> — one launch per group
-//      (standalone C-ABI op, calibration of that op, and the single-GPU
-//      loopback emulation of P ranks in one cooperative launch).
+//          peer (all-gather) fused with SGD; pipelined RS(c) | RA(c-1) |
+//          AP(c-2), one barrier per chunk.
+//        LL: small one-shot groups as flag-in-data packets, no barrier.
+//  engine_kernel<P, T> — the persistent comm engine: one launch per
+//      iteration runs every group in backward order as soon as the compute
+//      side marks it ready (paper Algorithm 2's daemon thread, on the GPU;
+//      no per-group launch latency).
+//  group_allreduce_kernel<P, TWO_SHOT, LOOPBACK, T> — one launch per group
+//      (standalone C-ABI op, calibration of that op, the full-width tail of
+//      a real backward, and the single-GPU loopback emulation of P ranks in
+//      one cooperative launch).
 //  pack_kernel / unpack_sgd_kernel — the standalone pack and unpack+SGD
 //      ops of the C ABI (rank-local, HBM-bound).
-//  replay_all_kernel / replay_kernel — backward-pass replay on %globaltimer.
+//  replay_all_kernel / replay_kernel / mark_ready_kernel — backward replay
+//      on %globaltimer and ready marks for the engine.
 //
 // Cross-rank synchronisation is per CTA index: CTA b of every rank handles
 // the same tiles, so CTA b only waits for CTA b of the peers. Each CTA index
