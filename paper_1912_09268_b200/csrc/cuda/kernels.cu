@@ -50,7 +50,11 @@ namespace mgw {
 namespace {
 
 constexpr uint64_t kTimeoutNs = 10ull * 1000 * 1000 * 1000;  // 10 s: error, never a hang
-constexpr int kStages = 4;                           // TMA ring depth (32 KiB stages)
+constexpr int kStages = 3;                           // TMA ring depth (32 KiB stages)
+// Per-data-thread staging slots (16 B each) for the reduction's inputs,
+// filled with cp.async so a whole batch (P sources + weights of up to 5
+// vectors) is in flight without holding registers: 480 x 15 x 16 B.
+constexpr uint32_t kStageSlots = 15;
 constexpr uint32_t kStageBytes = kTileElems * 4;
 // Software pipelining: a CTA walks its tiles in CHUNKS; while the producer
 // warp pushes chunk c over NVLink the data warps reduce / apply chunk c-1
@@ -510,6 +514,80 @@ __device__ __forceinline__ void apply_batch(const Tile& t, uint32_t i0, uint32_t
   }
 }
 
+// cp.async (LDGSTS, L2-only .cg) of 16 bytes into this thread's staging slot.
+__device__ __forceinline__ void cp_async16(float4* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+
+// fp32 reduction with staged inputs: for a batch of B vectors per thread,
+// every source slot, the own gradient and the weight vector are copied
+// global -> shared with cp.async (one memory latency per batch, B * (P + 1)
+// <= kStageSlots 16-byte slots per thread, conflict-free: slot k of thread t
+// at stage[k * kThreads + t]); then each vector is summed in rank order from
+// shared memory, pushed to the peers (all-gather) and applied. Bit-identical
+// to reduce_tile: the same operands, the same operation order.
+template <int P>
+struct StagedBatch {
+  static constexpr uint32_t raw = kStageSlots / (P + 1);
+  static constexpr uint32_t value = raw < kVecPerThread ? raw : kVecPerThread;
+};
+
+template <int P>
+__device__ __forceinline__ void reduce_tile_staged(const RankView& v, const Tile& t, uint64_t slot_stride,
+                                                   bool push_to_peers, uint64_t my_slot, float scale, float lr,
+                                                   int epi, float4* stage) {
+  constexpr uint32_t B = StagedBatch<P>::value;
+  static_assert(B >= 1, "staging slots too few for P");
+  const float* base = v.arena[v.rank] + t.moff;
+  const uint32_t nvec = (t.len + 3) >> 2;
+  const uint32_t layer = t.layer & kLayerMask;
+  float* w = v.weights[layer];
+  float* g = v.grads[layer];
+  const float* own = g + t.src;
+  const bool own_aligned = !(t.layer & kGradUnaligned);
+  const bool vec_w = (epi & MGW_SGD) && w != nullptr && !(t.layer & kWeightUnaligned);
+  float4* my = stage + threadIdx.x;
+  auto slot = [&](uint32_t k) { return my + k * kThreads; };
+#pragma unroll 1
+  for (uint32_t k0 = 0; k0 < kVecPerThread; k0 += B) {
+    const uint32_t i0 = threadIdx.x + k0 * kThreads;
+    if (i0 >= nvec) break;
+#pragma unroll
+    for (uint32_t j = 0; j < B; ++j) {
+      const uint32_t i = i0 + j * kThreads;
+      if (i >= nvec) continue;
+      const uint32_t e = i * 4;
+      const bool full = e + 4 <= t.len;
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        if (r != v.rank) cp_async16(slot(j * (P + 1) + r), base + r * slot_stride + e);
+      }
+      if (own_aligned && full) cp_async16(slot(j * (P + 1) + v.rank), own + e);
+      else *slot(j * (P + 1) + v.rank) = ld4_tail<float>(own + e, t.len - e);
+      if (vec_w && full) cp_async16(slot(j * (P + 1) + P), w + t.src + e);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll 1
+    for (uint32_t j = 0; j < B; ++j) {
+      const uint32_t i = i0 + j * kThreads;
+      if (i >= nvec) break;
+      float4 s[1], wv[1];
+      s[0] = mul4(*slot(j * (P + 1)), scale);
+#pragma unroll
+      for (int r = 1; r < P; ++r) s[0] = add4(s[0], mul4(*slot(j * (P + 1) + r), scale));
+      wv[0] = *slot(j * (P + 1) + P);  // (unused by the scalar epilogue paths)
+      if (push_to_peers) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          if (q != v.rank) st_v4(v.arena[q] + my_slot + t.moff + i * 4, s[0]);
+        }
+      }
+      apply_batch<1, float>(t, i, kThreads, s, wv, w, g, lr, epi);
+    }
+  }
+}
+
 // Rank-order sum of tile t: x_r from slot r of the local arena (.cg loads:
 // peers wrote them) and this rank's own gradients, each times 1/P, summed
 // x0 + x1 + ... + x_{P-1}; B vectors per batch; optionally push each sum
@@ -678,6 +756,7 @@ struct CtaCtx {
   uint32_t count;
   PushRing ring;
   uint8_t* stages;
+  float4* staging;  // data warps' cp.async slots (after the TMA ring)
   uint64_t* bars;
   bool producer;
 };
@@ -710,7 +789,11 @@ __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* ti
     } else if (t >= 1) {
 #pragma unroll 1
       for (uint32_t j = (t - 1) * C; j < mine && j < t * C; ++j) {
-        reduce_tile<P, T>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, scale, lr, epi);
+        if constexpr (sizeof(T) == 4) {
+          reduce_tile_staged<P>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, scale, lr, epi, cx.staging);
+        } else {
+          reduce_tile<P, T>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, scale, lr, epi);
+        }
       }
     }
     if (t < n_chunks) cta_barrier(v, P, cta, cx.count);
@@ -756,7 +839,13 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
 #pragma unroll 1
         for (uint32_t j = (t - 1) * C; j < mine && j < t * C; ++j) {
           const uint32_t ti = (cta + j * ncta) * P + me;
-          if (ti < n_tiles) reduce_tile<P, T>(v, tiles[ti], slot_stride, true, my_slot, scale, lr, epi);
+          if (ti < n_tiles) {
+            if constexpr (sizeof(T) == 4) {
+              reduce_tile_staged<P>(v, tiles[ti], slot_stride, true, my_slot, scale, lr, epi, cx.staging);
+            } else {
+              reduce_tile<P, T>(v, tiles[ti], slot_stride, true, my_slot, scale, lr, epi);
+            }
+          }
         }
       }
       if (t >= 2) {  // AP(t-2)
@@ -836,6 +925,7 @@ template <int P>
 __device__ __forceinline__ void cta_ctx_init(CtaCtx& cx, const RankView& v, uint8_t* dsmem, uint64_t* bars) {
   cx.producer = threadIdx.x >= kThreads;
   cx.stages = dsmem;
+  cx.staging = reinterpret_cast<float4*>(dsmem + static_cast<size_t>(kStages) * kStageBytes);
   cx.bars = bars;
   cx.ring.head = 0;
   cx.ring.phase = 0;
@@ -1023,7 +1113,8 @@ __global__ void __launch_bounds__(512) l2_flush_kernel(float4* buf, size_t n_vec
   }
 }
 
-constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes;
+constexpr size_t kSmemBytes =
+    static_cast<size_t>(kStages) * kStageBytes + static_cast<size_t>(kThreads) * kStageSlots * 16;
 
 constexpr size_t smem_for(int P) { return P > 1 ? kSmemBytes : 0; }
 
