@@ -285,7 +285,8 @@ def main():
         a_us, b_ps = (float(x) for x in args.model.split(","))
         sizes = sizes[:2]  # (a short sweep still exercises the calibration kernels)
     if args.engine_ctas != 0:
-        meas = comm.calibrate_engine(sizes, warmup=3, reps=15, algo=args.algo, engine_ctas=args.engine_ctas)
+        meas = comm.calibrate_engine(sizes, warmup=3, reps=15, algo=args.algo, engine_ctas=args.engine_ctas,
+                                     dtype=rt.BF16 if bf16 else rt.F32)
     else:
         meas = comm.calibrate(sizes, warmup=3, reps=15, algo=args.algo)
     tvec = torch.tensor([m.time_sec for m in meas], dtype=torch.float64, device=dev)

@@ -278,6 +278,9 @@ int mgw_calibrate(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int war
  * sample. This is the T(M) the planner sees in engine pipelines. */
 int mgw_calibrate_engine(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int warmup,
                          int reps, int algo, int engine_ctas, mgw_meas* out);
+/* The same with the gradient type of the groups (sizes stay in bytes). */
+int mgw_calibrate_engine_ex(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int warmup,
+                            int reps, int algo, int engine_ctas, int dtype, mgw_meas* out);
 
 /* Plain in-place sum all-reduce of a contiguous fp32 device buffer in rank
  * order (no scale, no SGD), through the same kernel. Collective. */

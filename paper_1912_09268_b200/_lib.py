@@ -101,6 +101,10 @@ mgw_calibrate_engine = _proto(
     "mgw_calibrate_engine",
     [vp, u64p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Meas)],
 )
+mgw_calibrate_engine_ex = _proto(
+    "mgw_calibrate_engine_ex",
+    [vp, u64p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Meas)],
+)
 mgw_pipeline_create_io = _proto(
     "mgw_pipeline_create_io",
     [vp, f64p, C.c_double, C.c_float, C.c_int, C.c_int, C.c_size_t, C.c_int, vp, vp, C.c_size_t, vp, vp,

@@ -1041,13 +1041,20 @@ int mgw_pipeline_group_times(mgw_pipeline* pipe, float* group_ms) {
 
 int mgw_calibrate_engine(mgw_comm* c, const uint64_t* sizes, size_t n, int warmup, int reps,
                          int algo, int engine_ctas, mgw_meas* out) {
+  return mgw_calibrate_engine_ex(c, sizes, n, warmup, reps, algo, engine_ctas, MGW_DTYPE_F32, out);
+}
+
+int mgw_calibrate_engine_ex(mgw_comm* c, const uint64_t* sizes, size_t n, int warmup, int reps,
+                            int algo, int engine_ctas, int dtype, mgw_meas* out) {
   MGW_TRY {
+    require(dtype == MGW_DTYPE_F32 || dtype == MGW_DTYPE_BF16, "bad dtype");
+    const uint64_t esize = dtype == MGW_DTYPE_BF16 ? 2 : 4;
     require(c != nullptr && sizes != nullptr && out != nullptr && reps >= 1, "bad calibrate args");
     require(!c->loopback, "calibration runs on a real communicator");
     mgw::set_device(c);
     uint64_t max_bytes = 16;
     for (size_t i = 0; i < n; ++i) max_bytes = std::max(max_bytes, sizes[i]);
-    const size_t max_elems = (max_bytes + 3) / 4;
+    const size_t max_elems = (max_bytes + esize - 1) / esize;  // gradient elements
     // ONE group per iteration, ready at t = 0: the planner's cost T(M) is a
     // group's time on an idle engine (back-to-back groups overlap at CTA
     // granularity, which made per-group stamps of a multi-group iteration
@@ -1055,24 +1062,22 @@ int mgw_calibrate_engine(mgw_comm* c, const uint64_t* sizes, size_t n, int warmu
     constexpr int kGroups = 1;
     float* grad = nullptr;
     float* w = nullptr;
-    ck(cudaMalloc(&grad, max_elems * sizeof(float)), "cudaMalloc(calib grad)");
+    ck(cudaMalloc(&grad, max_elems * esize + 16), "cudaMalloc(calib grad)");
     ck(cudaMalloc(&w, max_elems * sizeof(float)), "cudaMalloc(calib w)");
-    ck(cudaMemset(grad, 0, max_elems * sizeof(float)), "memset");
+    ck(cudaMemset(grad, 0, max_elems * esize + 16), "memset");
     ck(cudaMemset(w, 0, max_elems * sizeof(float)), "memset");
     try {
       for (size_t i = 0; i < n; ++i) {
         // R layers of `cnt` elements that all alias the same buffers (the
         // kernel reads grads / updates weights; aliasing is harmless for
         // timing), one group each, every group ready at iteration start.
-        const uint64_t cnt = std::max<uint64_t>(1, (sizes[i] + 3) / 4);
-        const uint64_t padded = (cnt + 3) & ~uint64_t{3};
-        const int R = static_cast<int>(std::max<uint64_t>(
-            1, std::min<uint64_t>(kGroups, c->arena_elems / std::max<uint64_t>(padded, 1))));
+        const uint64_t cnt = std::max<uint64_t>(1, (sizes[i] + esize - 1) / esize);
+        const int R = kGroups;
         std::vector<float*> gp(R, grad), wp(R, w);
         std::vector<uint64_t> counts(R, cnt);
         std::vector<uint8_t> tags(R, 0);
         std::vector<double> tb(R, 0.0);
-        mgw_plan* p = mgw::build_plan(c, R, gp.data(), wp.data(), counts.data(), tags.data());
+        mgw_plan* p = mgw::build_plan(c, R, gp.data(), wp.data(), counts.data(), tags.data(), dtype);
         mgw_pipeline* pipe = nullptr;
         try {
           pipe = mgw::build_pipeline(p, tb.data(), 0.0, 0.0f, algo, true, 0, engine_ctas);

@@ -104,12 +104,13 @@ class Comm:
         return [CommMeasurement(out[i].size_bytes, out[i].time_sec) for i in range(len(sizes))]
 
     def calibrate_engine(self, sizes: Sequence[int], warmup: int = 2, reps: int = 5,
-                         algo: str = "auto", engine_ctas: int = -1) -> List[CommMeasurement]:
+                         algo: str = "auto", engine_ctas: int = -1, dtype: int = 0) -> List[CommMeasurement]:
         """N1 for engine pipelines: median per-group device time in the
-        persistent comm engine (one group per iteration, ready at once)."""
+        persistent comm engine (one group per iteration, ready at once);
+        dtype: gradient type of the group (sizes in bytes)."""
         out = (_lib.Meas * len(sizes))()
-        check(_lib.mgw_calibrate_engine(self.handle, arr(C.c_uint64, sizes), len(sizes), warmup, reps,
-                                        ALGO[algo], engine_ctas, out))
+        check(_lib.mgw_calibrate_engine_ex(self.handle, arr(C.c_uint64, sizes), len(sizes), warmup, reps,
+                                           ALGO[algo], engine_ctas, int(dtype), out))
         return [CommMeasurement(out[i].size_bytes, out[i].time_sec) for i in range(len(sizes))]
 
     def close(self) -> None:

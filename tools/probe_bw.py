@@ -19,7 +19,8 @@ f = 2 * (P - 1) / P
 out = []
 for algo in os.environ.get("ALGOS", "oneshot,twoshot").split(","):
     for ctas in [int(c) for c in os.environ.get("CTAS", "64,140").split(",")]:
-        m = comm.calibrate_engine(sizes, warmup=2, reps=int(os.environ.get("REPS", "10")), algo=algo, engine_ctas=ctas)
+        m = comm.calibrate_engine(sizes, warmup=2, reps=int(os.environ.get("REPS", "10")), algo=algo, engine_ctas=ctas,
+                                  dtype=1 if os.environ.get("DTYPE") == "bf16" else 0)
         t = torch.tensor([x.time_sec for x in m], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         out.append((f"engine {algo} ctas={ctas}", [f * s / tt / 1e9 for s, tt in zip(sizes, t.tolist())],
