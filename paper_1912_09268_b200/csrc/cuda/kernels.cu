@@ -115,23 +115,6 @@ __device__ __forceinline__ float4 ld4_cg<bf16>(const bf16* p) {
   return unpack_bf16x4(a, b);
 }
 
-// ld4_cg(p) when `pred`, else `other` (predicated: no branch, no dynamically
-// indexed register array)
-template <typename T>
-__device__ __forceinline__ float4 ld4_cg_or(const T* p, bool pred, float4 other);
-template <>
-__device__ __forceinline__ float4 ld4_cg_or<float>(const float* p, bool pred, float4 other) {
-  return ld_cg_v4_or(p, pred, other);
-}
-template <>
-__device__ __forceinline__ float4 ld4_cg_or<bf16>(const bf16* p, bool pred, float4 other) {
-  uint32_t a = 0, b = 0;
-  asm volatile("{ .reg .pred q; setp.ne.u32 q, %3, 0; @q ld.global.cg.v2.u32 {%0,%1}, [%2]; }"
-               : "+r"(a), "+r"(b)
-               : "l"(p), "r"(static_cast<uint32_t>(pred)));
-  return pred ? unpack_bf16x4(a, b) : other;
-}
-
 // 4 elements -> float4: streaming read-once gradients
 template <typename T>
 __device__ __forceinline__ float4 ld4_stream(const T* p);
@@ -464,15 +447,6 @@ __device__ __forceinline__ void push_drain() {
   __syncwarp();
 }
 
-// Vectors of a thread reduced per batch: all slot, own-gradient and weight
-// loads of a batch are in flight together (one memory latency per batch);
-// B = 2 at P = 2, else 1, keeps the engine within 128 registers, no spills.
-template <int P>
-struct RedBatch {
-  static constexpr uint32_t raw = P == 2 ? 2 : 1;
-  static constexpr uint32_t value = raw < kVecPerThread ? raw : kVecPerThread;
-};
-
 // Weight vectors of B vectors of tile t (thread vector indices i0, i0 +
 // stride, ...), loaded up front so their latency overlaps the gradient loads.
 template <uint32_t B>
@@ -519,7 +493,45 @@ __device__ __forceinline__ void cp_async16(float4* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 
-// fp32 reduction with staged inputs: for a batch of B vectors per thread,
+// 8-byte cp.async (a bf16 vector). .ca (the only 8-byte form) may allocate
+// in L1; safe here: within a launch every arena address is read at most once
+// per CTA (groups and phases use disjoint bytes), and kernel boundaries
+// invalidate L1.
+__device__ __forceinline__ void cp_async8(float4* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ void cp_async_vec(float4* smem, const T* gmem) {
+  if constexpr (sizeof(T) == 4) {
+    cp_async16(smem, gmem);
+  } else {
+    cp_async8(smem, gmem);
+  }
+}
+
+// A staged vector: fp32 as is; bf16 as its raw 8 bytes in the slot's first half.
+template <typename T>
+__device__ __forceinline__ float4 slot_load(const float4* slot) {
+  if constexpr (sizeof(T) == 4) {
+    return *slot;
+  } else {
+    const uint2 u = *reinterpret_cast<const uint2*>(slot);
+    return unpack_bf16x4(u.x, u.y);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void slot_store(float4* slot, float4 v) {  // v exact in T
+  if constexpr (sizeof(T) == 4) {
+    *slot = v;
+  } else {
+    *reinterpret_cast<uint2*>(slot) = make_uint2((__float_as_uint(v.x) >> 16) | (__float_as_uint(v.y) & 0xffff0000u),
+                                                 (__float_as_uint(v.z) >> 16) | (__float_as_uint(v.w) & 0xffff0000u));
+  }
+}
+
+// Reduction with staged inputs: for a batch of B vectors per thread,
 // every source slot, the own gradient and the weight vector are copied
 // global -> shared with cp.async (one memory latency per batch, B * (P + 1)
 // <= kStageSlots 16-byte slots per thread, conflict-free: slot k of thread t
@@ -532,18 +544,18 @@ struct StagedBatch {
   static constexpr uint32_t value = raw < kVecPerThread ? raw : kVecPerThread;
 };
 
-template <int P>
+template <int P, typename T>
 __device__ __forceinline__ void reduce_tile_staged(const RankView& v, const Tile& t, uint64_t slot_stride,
                                                    bool push_to_peers, uint64_t my_slot, float scale, float lr,
                                                    int epi, float4* stage) {
   constexpr uint32_t B = StagedBatch<P>::value;
   static_assert(B >= 1, "staging slots too few for P");
-  const float* base = v.arena[v.rank] + t.moff;
+  const T* base = as<T>(v.arena[v.rank]) + t.moff;
   const uint32_t nvec = (t.len + 3) >> 2;
   const uint32_t layer = t.layer & kLayerMask;
   float* w = v.weights[layer];
-  float* g = v.grads[layer];
-  const float* own = g + t.src;
+  T* g = as<T>(v.grads[layer]);
+  const T* own = g + t.src;
   const bool own_aligned = !(t.layer & kGradUnaligned);
   const bool vec_w = (epi & MGW_SGD) && w != nullptr && !(t.layer & kWeightUnaligned);
   float4* my = stage + threadIdx.x;
@@ -560,10 +572,10 @@ __device__ __forceinline__ void reduce_tile_staged(const RankView& v, const Tile
       const bool full = e + 4 <= t.len;
 #pragma unroll
       for (int r = 0; r < P; ++r) {
-        if (r != v.rank) cp_async16(slot(j * (P + 1) + r), base + r * slot_stride + e);
+        if (r != v.rank) cp_async_vec<T>(slot(j * (P + 1) + r), base + r * slot_stride + e);
       }
-      if (own_aligned && full) cp_async16(slot(j * (P + 1) + v.rank), own + e);
-      else *slot(j * (P + 1) + v.rank) = ld4_tail<float>(own + e, t.len - e);
+      if (own_aligned && full) cp_async_vec<T>(slot(j * (P + 1) + v.rank), own + e);
+      else slot_store<T>(slot(j * (P + 1) + v.rank), ld4_tail<T>(own + e, t.len - e));
       if (vec_w && full) cp_async16(slot(j * (P + 1) + P), w + t.src + e);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -573,75 +585,19 @@ __device__ __forceinline__ void reduce_tile_staged(const RankView& v, const Tile
       const uint32_t i = i0 + j * kThreads;
       if (i >= nvec) break;
       float4 s[1], wv[1];
-      s[0] = mul4(*slot(j * (P + 1)), scale);
+      s[0] = mul4(slot_load<T>(slot(j * (P + 1))), scale);
 #pragma unroll
-      for (int r = 1; r < P; ++r) s[0] = add4(s[0], mul4(*slot(j * (P + 1) + r), scale));
+      for (int r = 1; r < P; ++r) s[0] = add4(s[0], mul4(slot_load<T>(slot(j * (P + 1) + r)), scale));
+      s[0] = round4<T>(s[0]);
       wv[0] = *slot(j * (P + 1) + P);  // (unused by the scalar epilogue paths)
       if (push_to_peers) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
-          if (q != v.rank) st_v4(v.arena[q] + my_slot + t.moff + i * 4, s[0]);
+          if (q != v.rank) st4<T>(as<T>(v.arena[q]) + my_slot + t.moff + i * 4, s[0]);
         }
       }
-      apply_batch<1, float>(t, i, kThreads, s, wv, w, g, lr, epi);
+      apply_batch<1, T>(t, i, kThreads, s, wv, w, g, lr, epi);
     }
-  }
-}
-
-// Rank-order sum of tile t: x_r from slot r of the local arena (.cg loads:
-// peers wrote them) and this rank's own gradients, each times 1/P, summed
-// x0 + x1 + ... + x_{P-1}; B vectors per batch; optionally push each sum
-// into slot `my_slot` of every peer (the two-shot owner's all-gather), then
-// SGD. Data warps only.
-template <int P, typename T>
-__device__ __forceinline__ void reduce_tile(const RankView& v, const Tile& t, uint64_t slot_stride,
-                                            bool push_to_peers, uint64_t my_slot, float scale, float lr,
-                                            int epi) {
-  constexpr uint32_t B = RedBatch<P>::value;
-  const T* base = as<T>(v.arena[v.rank]) + t.moff;
-  const uint32_t nvec = (t.len + 3) >> 2;
-  const uint32_t layer = t.layer & kLayerMask;
-  float* w = v.weights[layer];
-  T* g = as<T>(v.grads[layer]);
-  const T* own = g + t.src;
-  const bool own_aligned = !(t.layer & kGradUnaligned);
-#pragma unroll 1
-  for (uint32_t k0 = 0; k0 < kVecPerThread; k0 += B) {
-    const uint32_t i0 = threadIdx.x + k0 * kThreads;
-    if (i0 >= nvec) break;
-    float4 x[B][P];
-    float4 wv[B];
-#pragma unroll
-    for (uint32_t j = 0; j < B; ++j) {
-      const uint32_t i = i0 + j * kThreads;
-      if (i < nvec) {
-        const uint32_t e = i * 4;
-        const float4 o = (own_aligned && e + 4 <= t.len) ? ld4_stream<T>(own + e) : ld4_tail<T>(own + e, t.len - e);
-#pragma unroll
-        for (int r = 0; r < P; ++r) x[j][r] = ld4_cg_or<T>(base + r * slot_stride + e, r != v.rank, o);
-      }
-    }
-    load_w_batch<B>(t, i0, kThreads, w, epi, wv);
-    float4 s[B];
-#pragma unroll
-    for (uint32_t j = 0; j < B; ++j) {
-      s[j] = mul4(x[j][0], scale);
-#pragma unroll
-      for (int r = 1; r < P; ++r) s[j] = add4(s[j], mul4(x[j][r], scale));
-      s[j] = round4<T>(s[j]);
-    }
-    if (push_to_peers) {
-#pragma unroll
-      for (uint32_t j = 0; j < B; ++j) {
-        const uint32_t i = i0 + j * kThreads;
-        if (i >= nvec) continue;
-#pragma unroll
-        for (int q = 0; q < P; ++q) {
-          if (q != v.rank) st4<T>(as<T>(v.arena[q]) + my_slot + t.moff + i * 4, s[j]);
-        }
-      }
-    }
-    apply_batch<B, T>(t, i0, kThreads, s, wv, w, g, lr, epi);
   }
 }
 
@@ -789,11 +745,7 @@ __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* ti
     } else if (t >= 1) {
 #pragma unroll 1
       for (uint32_t j = (t - 1) * C; j < mine && j < t * C; ++j) {
-        if constexpr (sizeof(T) == 4) {
-          reduce_tile_staged<P>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, scale, lr, epi, cx.staging);
-        } else {
-          reduce_tile<P, T>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, scale, lr, epi);
-        }
+        reduce_tile_staged<P, T>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, scale, lr, epi, cx.staging);
       }
     }
     if (t < n_chunks) cta_barrier(v, P, cta, cx.count);
@@ -839,13 +791,7 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
 #pragma unroll 1
         for (uint32_t j = (t - 1) * C; j < mine && j < t * C; ++j) {
           const uint32_t ti = (cta + j * ncta) * P + me;
-          if (ti < n_tiles) {
-            if constexpr (sizeof(T) == 4) {
-              reduce_tile_staged<P>(v, tiles[ti], slot_stride, true, my_slot, scale, lr, epi, cx.staging);
-            } else {
-              reduce_tile<P, T>(v, tiles[ti], slot_stride, true, my_slot, scale, lr, epi);
-            }
-          }
+          if (ti < n_tiles) reduce_tile_staged<P, T>(v, tiles[ti], slot_stride, true, my_slot, scale, lr, epi, cx.staging);
         }
       }
       if (t >= 2) {  // AP(t-2)

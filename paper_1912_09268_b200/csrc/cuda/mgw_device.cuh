@@ -157,17 +157,6 @@ __device__ __forceinline__ float4 ld_cg_v4(const float* p) {
   return v;
 }
 
-// ld_cg_v4(p) when `pred`, else `other` (a predicated load: no branch, no
-// dynamically indexed register array).
-__device__ __forceinline__ float4 ld_cg_v4_or(const float* p, bool pred, float4 other) {
-  float4 v = other;
-  asm volatile(
-      "{ .reg .pred q; setp.ne.u32 q, %5, 0; @q ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4]; }"
-      : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
-      : "l"(p), "r"(static_cast<uint32_t>(pred)));
-  return v;
-}
-
 // Streaming gradient reads: read once per iteration, keep L1 clean.
 __device__ __forceinline__ float4 ld_stream_v4(const float* p) {
   float4 v;
