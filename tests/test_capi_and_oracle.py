@@ -141,3 +141,32 @@ def test_oracle_bf16_allreduce_semantics():
     red = np.float32([1.0, 1.25, 0.0])
     assert np.array_equal(pyoracle.bf16_to_f32(g[0][0]), red) and np.array_equal(g[0][0], g[1][0])
     assert np.array_equal(w[0][0], -np.float32(0.5) * red) and np.array_equal(w[1][0], 1 - np.float32(0.5) * red)
+
+
+def test_bf16_merge_layout_pads_layers_to_16_bytes():
+    """bf16 plans pad every layer to 8 elements (16 bytes): the Python
+    mirror, the oracle and the TMA / LL granule agree."""
+    from paper_1912_09268_b200 import runtime as rt
+
+    counts = [1, 7, 8, 9, 0, 4097, 3]
+    offs = pyoracle.merge_offsets_granule(counts, 8)
+    assert all(o % 8 == 0 for o in offs)
+    assert offs[-1] == rt.padded_elems(counts, rt.BF16)
+    assert pyoracle.merge_offsets(counts)[-1] == rt.padded_elems(counts, rt.F32)
+
+
+def test_scaling_projection_runs_on_committed_calibrations():
+    """§8f row 3: the measured-coefficient projection (ring alpha/beta fitted
+    to the on-box N=2,4 calibrations, then the reference sweep via the CLI)."""
+    import subprocess
+    import sys
+
+    calib = os.path.join(ROOT, "profiles", "calib")
+    if not os.path.exists(os.path.join(calib, "calib_resnet50_P2.csv")):
+        pytest.skip("no committed calibrations")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "project_scaling.py"), "resnet50", calib,
+                          "2,4,8,64"], capture_output=True, text=True, check=True).stdout
+    rows = [l.split() for l in out.splitlines() if l and not l.startswith("#") and l.split()[0].isdigit()]
+    eff = {(int(r[0]), r[1]): float(r[5]) for r in rows}
+    assert eff[(64, "mgwfbp")] >= eff[(64, "wfbp")]  # merging never loses under the reference model
+    assert 0 < eff[(8, "mgwfbp")] <= 1.0
