@@ -168,6 +168,60 @@ def ref_solver_us(trace, model, reps=200):
     return statistics.median(ts) * 1e6
 
 
+def cpu_path_detail(trace, model, budget_s=3.0):
+    """SURVEY §8d "CPU path timed beside it": the reference's own solver and
+    predictor on 1 core (oracle/_ref, the unmodified headers) and the CPU
+    restatement of the merged all-reduce + SGD for config 1 (ResNet-50-sized,
+    2 ranks as host buffers) on 1 core."""
+    import ctypes
+    import platform
+
+    import numpy as np
+
+    from oracle import pyoracle
+
+    out = {"host": platform.processor() or platform.machine(), "nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            out["host"] = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except (OSError, StopIteration):
+        pass
+    params = [l.params for l in trace.layers]
+    t_b = [l.backward_time for l in trace.layers]
+    L = len(params)
+    p = (ctypes.c_uint64 * L)(*params)
+    tb = (ctypes.c_double * L)(*t_b)
+    tags = (ctypes.c_uint8 * L)()
+    if pyoracle.REF is not None:
+        def med(fn, reps=100):
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                fn()
+                ts.append(time.perf_counter() - t0)
+            return statistics.median(ts) * 1e6
+        args = (p, tb, L, trace.forward_time, trace.bytes_per_element, model.a, model.b)
+        out["ref_optimal_plan_us_1core"] = med(lambda: pyoracle.REF.ref_optimal_plan(*args, tags))
+        out["ref_greedy_plan_us_1core"] = med(lambda: pyoracle.REF.ref_greedy_plan(*args, tags))
+        it, nonov = ctypes.c_double(), ctypes.c_double()
+        out["ref_iteration_time_us_1core"] = med(
+            lambda: pyoracle.REF.ref_iteration_time(*args, tags, ctypes.byref(it), ctypes.byref(nonov)))
+    # config 1: ResNet-50-sized merged all-reduce + SGD, 2 ranks, 1 core
+    rng = np.random.default_rng(1)
+    counts = [25_557_032]
+    g = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(2)]
+    w = [[np.full(c, 0.5, np.float32) for c in counts] for _ in range(2)]
+    ts = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or not ts:
+        t0 = time.perf_counter()
+        pyoracle.allreduce_sgd(g, w, [0], 0.01)
+        ts.append(time.perf_counter() - t0)
+    out["allreduce_sgd_r50_2ranks_ms_1core"] = statistics.median(ts) * 1e3
+    out["allreduce_sgd_r50_2ranks_GBps_1core"] = 2 * 4 * counts[0] * 3 / statistics.median(ts) / 1e9
+    return out
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle port of Algorithm 2
     + the reference's own optimal_plan from oracle/_ref) on host cores."""
@@ -452,11 +506,13 @@ def main():
         times = cpu_pipeline_sample(trace, [int(t) for t in plans["mgwfbp"].tags], 1, args.lr, threads,
                                     args.cpu_budget_s)
         solver = ref_solver_us(trace, model)
+        detail = cpu_path_detail(trace, model)
         cpu = {"value": len(times) / sum(times), "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{len(times)} iterations of the CPU Algorithm-2 restatement (oracle/mgw_oracle.c, "
                          f"same trace/plan, P=1, {threads} threads)"
                          + (f"; reference optimal_plan (oracle/_ref) {solver:.1f} us on 1 core" if solver else "")
-                         + ("; the CPU path reduces fp32 gradients (no bf16 CPU pipeline)" if bf16 else "")}
+                         + ("; the CPU path reduces fp32 gradients (no bf16 CPU pipeline)" if bf16 else ""),
+               "detail": detail}
 
     if rank == 0:
         line = {
