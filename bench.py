@@ -51,6 +51,9 @@ def parse_args():
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot"])
     ap.add_argument("--oneshot-max", type=int, default=0, help="0: the library default for N")
+    ap.add_argument("--tb-scale", type=float, default=1.0,
+                    help="scale the trace's forward/backward times (emulates faster compute / smaller batches: "
+                         "the comm-bound regime of the paper); 1.0 = the B200-measured trace")
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"],
                     help="gradient / merge-arena type (bf16: fp32 accumulation, fp32 master weights)")
     ap.add_argument("--engine-ctas", type=int, default=-1,
@@ -233,6 +236,10 @@ def run_reference(args):
         return 0
     N = max(world, args.gpus)
     trace = gs.load_trace(trace_path(args.trace))
+    if args.tb_scale != 1.0:
+        trace.forward_time *= args.tb_scale
+        for l in trace.layers:
+            l.backward_time *= args.tb_scale
     # paper cluster-independent model: a NVLink-class guess; the plan only
     # decides grouping, the CPU work is the same bytes either way
     model = gs.AllReduceModel(20e-6, 1.0 / 600e9)
@@ -305,6 +312,10 @@ def main():
     dev = torch.device("cuda", local)
     N = world
     trace = gs.load_trace(trace_path(args.trace))
+    if args.tb_scale != 1.0:
+        trace.forward_time *= args.tb_scale
+        for l in trace.layers:
+            l.backward_time *= args.tb_scale
     bf16 = args.dtype == "bf16"
     esz = 2 if bf16 else 4
     gdt = torch.bfloat16 if bf16 else torch.float32
@@ -530,7 +541,7 @@ def main():
                                if args.engine_ctas else "one fused kernel launch per group",
                        "parallelism": f"dp{N}", "l2": f"flushed every iteration ({args.l2_flush_mib} MiB memset "
                                                      "on the comm stream during the forward replay)",
-                       "compute_ms": compute_ms},
+                       "compute_ms": compute_ms, "tb_scale": args.tb_scale},
             "calibration": {"a_us": model.a * 1e6, "b_ps_per_byte": model.b * 1e12, "how": fit_how,
                             "sizes": len(meas), "largest_bytes": meas[-1].size_bytes,
                             "largest_us": meas[-1].time_sec * 1e6},
