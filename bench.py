@@ -51,6 +51,9 @@ def parse_args():
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot"])
     ap.add_argument("--oneshot-max", type=int, default=0, help="0: the library default for N")
+    ap.add_argument("--cost", default="linear", choices=["linear", "table"],
+                    help="linear: the reference's a + b*M (bit-exact optimal_plan); table: B200 extension, the same "
+                         "DP on the calibration's piecewise measured curve")
     ap.add_argument("--tb-scale", type=float, default=1.0,
                     help="scale the trace's forward/backward times (emulates faster compute / smaller batches: "
                          "the comm-bound regime of the paper); 1.0 = the B200-measured trace")
@@ -371,7 +374,7 @@ def main():
 
     # ---- plans (host solver, replicated; verified identical across ranks)
     plans = {
-        "mgwfbp": gs.optimal_plan(trace, model),
+        "mgwfbp": gs.optimal_plan(trace, model) if args.cost == "linear" else gs.optimal_plan_table(trace, meas),
         "wfbp": gs.MergePlan.all_normal(L),
         "single_buffer": gs.MergePlan.all_merged(L),
         "greedy": gs.greedy_plan(trace, model),
@@ -416,7 +419,8 @@ def main():
         med = D.max_over_ranks(statistics.median(per), dev)
         p10 = D.max_over_ranks(per[max(0, int(0.1 * len(per)) - 0)], dev)
         p90 = D.max_over_ranks(per[min(len(per) - 1, int(0.9 * len(per)))], dev)
-        pred = gs.iteration_time(trace, plans[name], model).iteration_time
+        pred = (gs.iteration_time(trace, plans[name], model).iteration_time if args.cost == "linear"
+                else gs.iteration_time_table(trace, plans[name], meas))
         strat[name] = {"iter_ms_median": med, "iter_ms_p10": p10, "iter_ms_p90": p90,
                        "predicted_ms": pred * 1e3, "groups": dplans[name].n_groups}
         if args.engine_ctas != 0:
@@ -535,7 +539,9 @@ def main():
                      + "; backward replayed from B200-measured per-tensor t_b"),
             "config": {"workload": args.trace, "trace": os.path.relpath(trace_path(args.trace), ROOT),
                        "layers": L, "params": sum(counts), "grad_bytes": total_bytes,
-                       "plan": "optimal_plan on on-box calibrated (a, b)", "plan_sha256": digest[:16],
+                       "plan": ("optimal_plan on on-box calibrated (a, b)" if args.cost == "linear" else
+                                "optimal_plan_table on the on-box calibration curve (B200 extension)"),
+                       "plan_sha256": digest[:16],
                        "groups": dplans["mgwfbp"].n_groups, "algo": args.algo, "oneshot_max": comm.oneshot_max,
                        "comm": ("persistent engine, %s CTAs" % ("1/SM" if args.engine_ctas < 0 else args.engine_ctas))
                                if args.engine_ctas else "one fused kernel launch per group",

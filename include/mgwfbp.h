@@ -104,6 +104,16 @@ int mgw_predict(const uint64_t* params, const double* t_b, size_t L, double t_f,
                 double* comm_nonoverlap_out, double* tau_b_out, double* tau_c_out,
                 double* t_c_out);
 
+/* B200 extension (no reference counterpart): optimal_plan's exact DP and
+ * iteration_time's FIFO timeline with T(M) interpolated from measured
+ * (size, time) pairs — piecewise linear, non-decreasing, flat below the
+ * smallest size, last slope above the largest — instead of a + b*M. The
+ * fused kernel's cost is piecewise (LL / one-shot / two-shot). */
+int mgw_plan_optimal_table(const uint64_t* params, const double* t_b, size_t L, double t_f, int bpe,
+                           const mgw_meas* meas, size_t n_meas, uint8_t* tags_out);
+int mgw_predict_table(const uint64_t* params, const double* t_b, size_t L, double t_f, int bpe,
+                      const mgw_meas* meas, size_t n_meas, const uint8_t* tags, double* iter_time_out);
+
 /* gradsched::synceasgd_time / naive_time (timeline.hpp:196-221). */
 int mgw_baseline_times(const uint64_t* params, const double* t_b, size_t L, double t_f,
                        int bpe, double a, double b, double* synceasgd_out, double* naive_out);

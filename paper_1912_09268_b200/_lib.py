@@ -58,6 +58,9 @@ mgw_plan_optimal = _proto("mgw_plan_optimal", _plan_args + [u8p])
 mgw_plan_greedy = _proto("mgw_plan_greedy", _plan_args + [u8p])
 mgw_plan_brute_force = _proto("mgw_plan_brute_force", _plan_args + [C.c_size_t, u8p, f64p])
 mgw_predict = _proto("mgw_predict", _plan_args + [u8p, f64p, f64p, f64p, f64p, f64p])
+_table_args = [u64p, f64p, C.c_size_t, C.c_double, C.c_int, C.POINTER(Meas), C.c_size_t]
+mgw_plan_optimal_table = _proto("mgw_plan_optimal_table", _table_args + [u8p])
+mgw_predict_table = _proto("mgw_predict_table", _table_args + [u8p, f64p])
 mgw_baseline_times = _proto("mgw_baseline_times", _plan_args + [f64p, f64p])
 mgw_synth_trace_json = _proto(
     "mgw_synth_trace_json",

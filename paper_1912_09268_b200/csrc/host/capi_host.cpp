@@ -10,6 +10,7 @@
 #include "capi_common.hpp"
 #include "gradsched/gradsched.hpp"
 #include "mgwfbp.h"
+#include "planner_table.hpp"
 
 namespace mgw {
 
@@ -108,6 +109,37 @@ const char* mgw_last_error(void) { return mgw::g_last_error.c_str(); }
 const char* mgw_last_error_kind(void) { return mgw::g_last_kind; }
 
 const char* mgw_version(void) { return "mgwfbp-b200 0.1 (sm_100a)"; }
+
+namespace {
+mgw_host::CostTable make_table(const mgw_meas* meas, size_t n) {
+  if (meas == nullptr && n != 0) throw gradsched::ValidationError("measurements are NULL");
+  std::vector<double> m(n), t(n);
+  for (size_t i = 0; i < n; ++i) {
+    m[i] = static_cast<double>(meas[i].size_bytes);
+    t[i] = meas[i].time_sec;
+  }
+  return mgw_host::CostTable(std::move(m), std::move(t));
+}
+}  // namespace
+
+int mgw_plan_optimal_table(const uint64_t* params, const double* t_b, size_t L, double t_f, int bpe,
+                           const mgw_meas* meas, size_t n_meas, uint8_t* tags_out) {
+  MGW_TRY {
+    const auto trace = make_trace(params, t_b, L, t_f, bpe);
+    write_tags(mgw_host::optimal_plan_table(trace, make_table(meas, n_meas)), tags_out);
+  }
+  MGW_CATCH
+}
+
+int mgw_predict_table(const uint64_t* params, const double* t_b, size_t L, double t_f, int bpe,
+                      const mgw_meas* meas, size_t n_meas, const uint8_t* tags, double* iter_time_out) {
+  MGW_TRY {
+    const auto trace = make_trace(params, t_b, L, t_f, bpe);
+    const double t = mgw_host::iteration_time_table(trace, make_plan(tags, L), make_table(meas, n_meas));
+    if (iter_time_out) *iter_time_out = t;
+  }
+  MGW_CATCH
+}
 
 int mgw_fit(const mgw_meas* samples, size_t n, double* a_out, double* b_out) {
   MGW_TRY {

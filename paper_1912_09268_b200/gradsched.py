@@ -277,6 +277,31 @@ def iteration_time(trace: ModelTrace, plan: MergePlan, model: AllReduceModel) ->
     return Timeline(list(tau_b)[:L], list(tau_c)[:L], list(t_c)[:L], it.value, no.value)
 
 
+def _meas_arr(meas: Sequence[CommMeasurement]):
+    out = (_lib.Meas * max(1, len(meas)))()
+    for i, m in enumerate(meas):
+        out[i].size_bytes, out[i].time_sec = int(m.size_bytes), float(m.time_sec)
+    return out
+
+
+def optimal_plan_table(trace: ModelTrace, meas: Sequence[CommMeasurement]) -> MergePlan:
+    """B200 extension: optimal_plan's exact DP with T(M) interpolated from the
+    measured calibration instead of a + b*M (mgw_plan_optimal_table)."""
+    p, tb, L, tf, bpe = trace._c()
+    out = (C.c_uint8 * max(1, L))()
+    check(_lib.mgw_plan_optimal_table(p, tb, L, tf, bpe, _meas_arr(meas), len(meas), out))
+    return _tags_from(out, L)
+
+
+def iteration_time_table(trace: ModelTrace, plan: MergePlan, meas: Sequence[CommMeasurement]) -> float:
+    """The serialised FIFO iteration time with the interpolated measured cost."""
+    p, tb, L, tf, bpe = trace._c()
+    tags = arr(C.c_uint8, (int(t) for t in plan.tags))
+    it = C.c_double()
+    check(_lib.mgw_predict_table(p, tb, L, tf, bpe, _meas_arr(meas), len(meas), tags, C.byref(it)))
+    return it.value
+
+
 def synceasgd_time(trace: ModelTrace, model: AllReduceModel) -> float:
     p, tb, L, tf, bpe = trace._c()
     s, n = C.c_double(), C.c_double()
