@@ -880,8 +880,12 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
       }
       if (pipe->flush_bytes > 0) {
         // The comm stream is idle until the first group is ready: evict L2
-        // there while the compute stream replays the forward pass.
-        ck(launch_l2_flush(pipe->flush_buf, pipe->flush_bytes, 16, pipe->comm), "l2 flush");
+        // there while the compute stream replays the forward pass — on all
+        // but 8 SMs (a full-grid flush kept the 1-thread replay kernel from
+        // being scheduled; 16 CTAs took ~170 us, longer than a short
+        // forward, and delayed the engine).
+        const int flush_ctas = std::max(16, p->comm->num_sms - 8);
+        ck(launch_l2_flush(pipe->flush_buf, pipe->flush_bytes, flush_ctas, pipe->comm), "l2 flush");
       }
       if (pipe->engine) {
         ck(launch_engine(pipe->args, pipe->engine_ctas, pipe->comm), "engine launch");
