@@ -285,7 +285,8 @@ int mgw_calibrate(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int war
 /* Calibration of the persistent comm engine: per size, `reps` iterations of
  * an engine running ONE group of that size, ready at once; the median group
  * device duration (%globaltimer, first CTA start -> last CTA end) is the
- * sample. This is the T(M) the planner sees in engine pipelines. */
+ * sample (L2 evicted before every rep). This is the T(M) the planner sees in
+ * engine pipelines. */
 int mgw_calibrate_engine(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int warmup,
                          int reps, int algo, int engine_ctas, mgw_meas* out);
 /* The same with the gradient type of the groups (sizes stay in bytes). */

@@ -1084,7 +1084,11 @@ int mgw_calibrate_engine_ex(mgw_comm* c, const uint64_t* sizes, size_t n, int wa
         mgw_plan* p = mgw::build_plan(c, R, gp.data(), wp.data(), counts.data(), tags.data(), dtype);
         mgw_pipeline* pipe = nullptr;
         try {
-          pipe = mgw::build_pipeline(p, tb.data(), 0.0, 0.0f, algo, true, 0, engine_ctas);
+          // L2 evicted before every rep (256 MiB > the 126 MB L2, on the comm
+          // branch before the engine; the group's stamps start after it):
+          // cold-HBM group times, as in a pipeline iteration — a warm L2 made
+          // the P = 1 slope look faster than HBM
+          pipe = mgw::build_pipeline(p, tb.data(), 0.0, 0.0f, algo, true, size_t{256} << 20, engine_ctas);
           std::vector<float> ms;
           std::vector<float> gm(R);
           for (int k = 0; k < warmup + reps; ++k) {
