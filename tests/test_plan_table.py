@@ -44,3 +44,16 @@ def test_table_plan_is_optimal_by_exhaustive_search():
             for tags in itertools.product([0, 1], repeat=L - 1))
         plan = gs.optimal_plan_table(tr, meas)
         assert gs.iteration_time_table(tr, plan, meas) <= best * (1 + 1e-12)
+
+
+def test_table_api_rejects_bad_measurements():
+    tr = gs.trace_from_arrays([100, 200], [1e-4, 1e-4], 1e-3)
+    import pytest
+
+    with pytest.raises(gs.ValidationError):
+        gs.optimal_plan_table(tr, [])
+    with pytest.raises(gs.ValidationError):
+        gs.optimal_plan_table(tr, [gs.CommMeasurement(1024, 0.0)])
+    # a single point is a flat (latency-only) curve: merging everything is optimal
+    plan = gs.optimal_plan_table(tr, [gs.CommMeasurement(1024, 1e-3)])
+    assert [int(t) for t in plan.tags] == [0, 1]
