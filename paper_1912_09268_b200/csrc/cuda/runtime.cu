@@ -84,6 +84,7 @@ struct mgw_comm {
   uint32_t chunk_tiles = 16;  // pipelined chunk per CTA (MGW_CHUNK_TILES overrides, for probing)
   uint64_t ll_max = 64 << 10; // one-shot groups up to this many bytes use LL packets
   int max_ctas = 0;           // cap on the CTAs of a standalone group launch (0: one per SM)
+  uint64_t small_tile_max = 0; // groups below this many bytes use kTileElems / 4 tiles (more CTAs)
   // own allocations (loopback: one per emulated rank)
   std::vector<float*> arenas;
   std::vector<uint32_t*> signals;
@@ -226,6 +227,15 @@ uint64_t default_ll_max(int nranks) {
   return 32ull << 10;
 }
 
+// Groups below this many bytes are cut into kTileElems / 4 tiles so they
+// spread over more CTAs. Measured on B200 (tools/probe_bw.py, engine): 1 MiB
+// P = 2 one-shot 11.0 -> 9.9 us, 2 MiB P = 4 two-shot 23.4 -> 21.2 us; from
+// 4 MiB on the 32 KiB tiles are as fast or faster (P = 2 8 MiB 24.2 vs 28.1).
+uint64_t default_small_tile_max() {
+  const char* e = std::getenv("MGW_SMALL_TILE_MAX");
+  return e != nullptr ? std::strtoull(e, nullptr, 10) : (3ull << 20);
+}
+
 uint32_t default_chunk_tiles() {
   const char* e = std::getenv("MGW_CHUNK_TILES");
   const long v = e != nullptr ? std::strtol(e, nullptr, 10) : 0;
@@ -342,6 +352,10 @@ mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* w
   std::vector<Tile> tiles;
   for (int g = 0; g + 1 < static_cast<int>(p->heads.size()); ++g) {
     p->tile_first.push_back(static_cast<uint32_t>(tiles.size()));
+    // medium groups: smaller tiles spread the group over more CTAs
+    uint64_t gbytes = 0;
+    for (size_t l = p->heads[g]; l < p->heads[g + 1]; ++l) gbytes += counts[l] * p->esize;
+    const uint64_t tile_elems = (c->nranks > 1 && gbytes < c->small_tile_max) ? kTileElems / 4 : kTileElems;
     for (size_t l = p->heads[g]; l < p->heads[g + 1]; ++l) {
       uint32_t flags = 0;
       for (size_t r = 0; r < nv; ++r) {
@@ -349,10 +363,10 @@ mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* w
         if (reinterpret_cast<uintptr_t>(p->h_weights[r * L + l]) % 16) flags |= kWeightUnaligned;
         require(counts[l] == 0 || p->h_grads[r * L + l] != nullptr, "NULL gradient pointer");
       }
-      for (uint64_t s = 0; s < counts[l]; s += kTileElems) {
+      for (uint64_t s = 0; s < counts[l]; s += tile_elems) {
         Tile t;
         t.layer = static_cast<uint32_t>(l) | flags;
-        t.len = static_cast<uint32_t>(std::min<uint64_t>(kTileElems, counts[l] - s));
+        t.len = static_cast<uint32_t>(std::min<uint64_t>(tile_elems, counts[l] - s));
         t.src = static_cast<uint32_t>(s);
         t.moff = static_cast<uint32_t>(p->offs[l] + s);
         tiles.push_back(t);
@@ -423,6 +437,7 @@ int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_co
     c->oneshot_max = mgw::default_oneshot_max(nranks);
     c->chunk_tiles = mgw::default_chunk_tiles();
     c->ll_max = mgw::default_ll_max(nranks);
+    c->small_tile_max = mgw::default_small_tile_max();
     mgw::init_common(c, device, arena_bytes);
     c->arenas.push_back(mgw::alloc_arena(c->arena_elems, nranks));
     c->signals.push_back(mgw::alloc_zero_u32(mgw::signal_words(nranks)));
@@ -445,6 +460,7 @@ int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_com
     c->oneshot_max = mgw::default_oneshot_max(nranks);
     c->chunk_tiles = mgw::default_chunk_tiles();
     c->ll_max = mgw::default_ll_max(nranks);
+    c->small_tile_max = mgw::default_small_tile_max();
     c->loopback = true;
     mgw::init_common(c, device, arena_bytes);
     for (int r = 0; r < nranks; ++r) {
