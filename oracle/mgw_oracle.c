@@ -7,6 +7,14 @@
  * Each function is a deliberately literal restatement of the reference
  * (O(L^2) DP with no pruning, greedy with full tau_c recomputation) so it
  * checks the optimised product code through a different path.
+ *
+ * Pinning: the solver / predictor / fit restatements are pinned to the
+ * reference itself (oracle/_ref, built from the unmodified headers, and the
+ * golden vectors in tests/golden). The reduction part (pack, rank-order
+ * all-reduce + SGD, the CPU Algorithm-2 pipeline) has NO reference code —
+ * the reference only models it — so its parity is UNPINNED by the
+ * reference: it restates PAPER.md:117-120 (Eq. 2) and PAPER.md:562-563,
+ * and only its bf16 rounding is pinned (to torch's conversion).
  */
 #define _GNU_SOURCE
 #include "mgw_oracle.h"
