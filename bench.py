@@ -388,6 +388,10 @@ def main():
         pipes[name] = rt.Pipeline(dplans[name], trace, args.lr, args.algo,
                                   record_group_times=True, l2_flush_bytes=flush,
                                   engine_ctas=args.engine_ctas)
+    # the headline pipeline: the same plan without the per-group timing
+    # stamps (an instrumented twin above supplies group times / the tail)
+    pipes["headline"] = rt.Pipeline(dplans["mgwfbp"], trace, args.lr, args.algo, record_group_times=False,
+                                    l2_flush_bytes=flush, engine_ctas=args.engine_ctas)
 
     def timed(name, iters):
         D.barrier()
@@ -404,17 +408,16 @@ def main():
     # ---- the timed region: K MG-WFBP iterations
     launches0 = rt.kernel_launches()
     with ClockSampler(local) as clk:
-        ms = timed("mgwfbp", args.steps)
+        ms = timed("headline", args.steps)
     launches = rt.kernel_launches() - launches0
     clocks = clk.summary()
     t_total = D.max_over_ranks(sum(ms) / 1e3, dev)
     value = N * args.steps / t_total
-    group_ms = pipes["mgwfbp"].group_times_ms()
 
     # ---- comparison strategies on the same box / pipeline
     strat = {}
     for name in ("mgwfbp", "wfbp", "single_buffer", "greedy"):
-        m = ms if name == "mgwfbp" else timed(name, args.steps)
+        m = timed(name, args.steps)  # instrumented pipelines, alike for every strategy
         per = sorted(m)
         med = D.max_over_ranks(statistics.median(per), dev)
         p10 = D.max_over_ranks(per[max(0, int(0.1 * len(per)) - 0)], dev)
@@ -428,6 +431,8 @@ def main():
             tl = pipes[name].device_timeline()
             strat[name]["device_tail_us"] = D.max_over_ranks(tl["tail_us"], dev)
             strat[name]["device_replay_ms"] = tl["replay_us"] / 1e3
+        if name == "mgwfbp":
+            group_ms = pipes["mgwfbp"].group_times_ms()
     compute_ms = (trace.forward_time + sum(l.backward_time for l in trace.layers)) * 1e3
 
     # ---- e2e through the public API with host buffers
@@ -438,7 +443,7 @@ def main():
     host_grad.copy_(flat_grad.cpu())
     host_out = torch.empty(4, dtype=torch.float32, pin_memory=True)
     out_src = weights[0][:4] if counts[0] >= 4 else flat_grad[:4]
-    pipe = rt.Pipeline(dplans["mgwfbp"], trace, args.lr, args.algo, record_group_times=True,
+    pipe = rt.Pipeline(dplans["mgwfbp"], trace, args.lr, args.algo, record_group_times=False,
                        l2_flush_bytes=flush, engine_ctas=args.engine_ctas,
                        h2d=(host_grad, flat_grad), d2h=(host_out, out_src))
     pipe.run(max(1, args.warmup))
