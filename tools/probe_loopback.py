@@ -14,7 +14,8 @@ n = (int(os.environ.get("SIZE_MB", "64")) << 20) // 4
 algo = os.environ.get("ALGO", "twoshot")
 iters = int(os.environ.get("ITERS", "5"))
 torch.cuda.set_device(0)
-grads = [[torch.rand(n, device="cuda")] for _ in range(P)]
+gdt = torch.bfloat16 if os.environ.get("DTYPE") == "bf16" else torch.float32
+grads = [[torch.rand(n, device="cuda").to(gdt)] for _ in range(P)]
 weights = [[torch.rand(n, device="cuda")] for _ in range(P)]
 comm = rt.Comm.create_loopback(P, 0, 4 * n)
 dp = rt.DevicePlan(comm, grads, weights, gs.MergePlan.all_merged(1))
