@@ -1,28 +1,38 @@
 """MG-WFBP iteration benchmark on B200 (driver contract: one JSON line).
 
 One step = one synchronous data-parallel iteration of the hot path on the
-named model's layer trace: the backward pass replayed from B200-measured
+named model's layer trace (default BERT-large, BASELINE config 5, the largest
+config that fits one B200): the backward pass replayed from B200-measured
 per-tensor times (traces/<model>.json) on a compute stream, and every merge
-group's fused pack -> NVLink all-reduce -> unpack+SGD kernel launched on a
-comm stream the moment its head layer is ready (paper Algorithm 2), the
+group's fused pack -> NVLink all-reduce -> unpack+SGD run by the persistent
+comm engine the moment its head layer is ready (paper Algorithm 2), the
 whole iteration one CUDA graph. Gradients are synthetic uniform[-1,1) fp32
 (seed 0x5EED0000 + rank), weights uniform (seed 0xC0FFEE), lr 0.01.
 
   value   = N * K / (max over ranks of the device time of K MG-WFBP
             iterations)  [worker-iterations/s; driver scaling efficiency =
             value_N / (N * value_1) = t_iter(1) / t_iter(N), the paper's]
-  plan    = optimal_plan(trace, (a, b)) with (a, b) fitted (fit_model) to
-            an on-box calibration sweep of the same fused kernel at this N
+  plan    = optimal_plan(trace, fit_model(committed on-box calibration
+            profiles/calib/calib_<trace>_P<N>.csv)) — the SAME plan in both
+            arms (same plan_sha256, identical config); the live on-box sweep
+            of this run is reported beside it (calibration.onbox)
   strategies: MG-WFBP (optimal), WFBP (all normal), single buffer (all
             merged), greedy (paper Algorithm 1) on the same pipeline
+  roofline: the engine kernel in standalone drain (every group ready), CUDA
+            events per launch: algorithmic bytes / launch time vs HBM (N=1)
+            or NVLink 900 GB/s per direction (N>1)
 
-usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--trace googlenet]
-       python bench.py --impl reference ...   (CPU Algorithm 2 on host cores)
+usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--trace bert_large]
+       python bench.py --impl reference ...   (the reference's CPU path: its
+           own optimal_plan from oracle/_ref + the CPU Algorithm-2 port; never
+           imports this package)
 Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N (one rank per GPU).
 """
 from __future__ import annotations
 
 import argparse
+import glob
+import hashlib
 import json
 import math
 import os
@@ -37,8 +47,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "iter time & scaling eff. @1/2/4/8 B200 vs WFBP; merged allreduce bus GB/s"
 UNIT = "worker-iters/s"
-NVLINK_PEER_GBS = 770.0  # measured peer copy per direction, /opt/skills/guides/B200_PROFILING.md
+NVLINK_GBS = 900.0       # NVLink 5 per direction (north_star / BASELINE.md §3 denominator)
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction, /opt/skills/guides/B200_PROFILING.md (secondary)
 HBM_FALLBACK_GBS = 6650.0
+L2_BYTES = 126 << 20
 
 
 def parse_args():
@@ -47,7 +59,10 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mgwfbp", choices=["mgwfbp", "reference"])
-    ap.add_argument("--trace", default="googlenet")
+    ap.add_argument("--trace", default="bert_large")
+    ap.add_argument("--plan-source", default="committed", choices=["committed", "onbox"],
+                    help="committed: both arms plan from profiles/calib/calib_<trace>_P<N>.csv (same plan); "
+                         "onbox: the GPU arm plans from this run's own calibration sweep")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot"])
     ap.add_argument("--oneshot-max", type=int, default=0, help="0: the library default for N")
@@ -133,138 +148,237 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-# -------------------------------------------------------------- CPU legs
-def cpu_pipeline_sample(trace, tags, P, lr, threads, budget_s, iters_cap=None):
-    """The CPU restatement of Algorithm 2 (oracle port) on host buffers."""
-    import numpy as np
-
-    from oracle import pyoracle
-
-    counts = [l.params for l in trace.layers]
-    rng = np.random.default_rng(0x5EED0000)
-    g = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(P)]
-    w = [[np.full(c, 0.5, np.float32) for c in counts] for _ in range(P)]
-    t_b = [l.backward_time for l in trace.layers]
-    first = pyoracle.pipeline_run(g, w, counts, t_b, trace.forward_time, tags, lr, threads, 1)[0]
-    iters = max(3, min(200, int(budget_s / max(first, 1e-6))))
-    if iters_cap is not None:
-        iters = min(iters, iters_cap)
-    times = pyoracle.pipeline_run(g, w, counts, t_b, trace.forward_time, tags, lr, threads, iters)
-    return times
-
-
-def ref_solver_us(trace, model, reps=200):
-    import ctypes
-
-    from oracle import pyoracle
-
-    if pyoracle.REF is None:
-        return None
-    params = [l.params for l in trace.layers]
-    t_b = [l.backward_time for l in trace.layers]
-    L = len(params)
-    p = (ctypes.c_uint64 * L)(*params)
-    tb = (ctypes.c_double * L)(*t_b)
-    out = (ctypes.c_uint8 * L)()
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        pyoracle.REF.ref_optimal_plan(p, tb, L, trace.forward_time, trace.bytes_per_element, model.a, model.b, out)
-        ts.append(time.perf_counter() - t0)
-    return statistics.median(ts) * 1e6
+# ------------------------------------------- shared by both arms (no package)
+def load_trace_json(path: str, tb_scale: float = 1.0) -> dict:
+    """The reference's load_trace (trace.hpp:148-219) restated for the
+    reference arm, which must not load this package: microseconds / 1e6 on
+    correctly rounded parses (Python's float() and nlohmann's strtod agree),
+    so the doubles equal the library's ModelTrace bit for bit."""
+    with open(path) as f:
+        d = json.load(f)
+    tr = {"names": [l["name"] for l in d["layers"]],
+          "params": [int(l["params"]) for l in d["layers"]],
+          "t_b": [float(l["backward_time_us"]) / 1e6 for l in d["layers"]],
+          "t_f": float(d["forward_time_us"]) / 1e6,
+          "bpe": int(d.get("bytes_per_element", 4))}
+    if tb_scale != 1.0:
+        tr["t_f"] *= tb_scale
+        tr["t_b"] = [t * tb_scale for t in tr["t_b"]]
+    return tr
 
 
-def cpu_path_detail(trace, model, budget_s=3.0):
-    """SURVEY §8d "CPU path timed beside it": the reference's own solver and
-    predictor on 1 core (oracle/_ref, the unmodified headers) and the CPU
-    restatement of the merged all-reduce + SGD for config 1 (ResNet-50-sized,
-    2 ranks as host buffers) on 1 core."""
-    import ctypes
+def committed_calibration(trace_name: str, N: int):
+    """profiles/calib/calib_<trace>_P<N>.csv — an on-box calibration sweep
+    of the fused engine kernel committed from an earlier run on this box type
+    (P8: projected from P4, profiles/calib/README.md). Both arms fit it with
+    the reference's fit_model, so they plan identically."""
+    rel = os.path.join("profiles", "calib", f"calib_{os.path.basename(trace_name).replace('.json', '')}_P{N}.csv")
+    return rel if os.path.exists(os.path.join(ROOT, rel)) else None
+
+
+def plan_digest(tags) -> str:
+    return hashlib.sha256(bytes(int(t) for t in tags)).hexdigest()
+
+
+def common_config(name: str, tr: dict, N: int, tags, calib_rel, tb_scale: float, dtype: str) -> dict:
+    """The `config` object, built identically by both arms from the trace
+    file, the plan's tags and the calibration path."""
+    esz = 2 if dtype == "bf16" else 4
+    total = sum(tr["params"])
+    inputs = 2 * esz * total
+    return {
+        "workload": name, "trace": os.path.relpath(trace_path(name), ROOT), "layers": len(tr["params"]),
+        "params": total, "grad_bytes": esz * total, "dtype": dtype,
+        "plan": "optimal_plan (reference planner.hpp:63-98) on fit_model of " + (calib_rel or "?"),
+        "calibration_csv": calib_rel, "plan_sha256": plan_digest(tags)[:16],
+        "groups": sum(1 for i, t in enumerate(tags) if i == 0 or int(t) == 0),
+        "parallelism": f"dp{N}", "ranks": N,
+        "compute_ms": (tr["t_f"] + sum(tr["t_b"])) * 1e3, "tb_scale": tb_scale,
+        "l2": ("inputs (gradients + weights, %.0f MB per rank) exceed the 126 MB L2; " % (inputs / 1e6)
+               if inputs > L2_BYTES else "inputs fit in L2; ") + "the GPU arm also evicts L2 every iteration",
+    }
+
+
+def host_info() -> dict:
     import platform
 
-    import numpy as np
-
-    from oracle import pyoracle
-
-    out = {"host": platform.processor() or platform.machine(), "nproc": os.cpu_count()}
+    out = {"host": platform.processor() or platform.machine(), "nproc": os.cpu_count(),
+           "isa": platform.machine()}
     try:
         with open("/proc/cpuinfo") as f:
             out["host"] = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
     except (OSError, StopIteration):
         pass
-    params = [l.params for l in trace.layers]
-    t_b = [l.backward_time for l in trace.layers]
-    L = len(params)
-    p = (ctypes.c_uint64 * L)(*params)
-    tb = (ctypes.c_double * L)(*t_b)
-    tags = (ctypes.c_uint8 * L)()
-    if pyoracle.REF is not None:
-        def med(fn, reps=100):
-            ts = []
-            for _ in range(reps):
-                t0 = time.perf_counter()
-                fn()
-                ts.append(time.perf_counter() - t0)
-            return statistics.median(ts) * 1e6
-        args = (p, tb, L, trace.forward_time, trace.bytes_per_element, model.a, model.b)
-        out["ref_optimal_plan_us_1core"] = med(lambda: pyoracle.REF.ref_optimal_plan(*args, tags))
-        out["ref_greedy_plan_us_1core"] = med(lambda: pyoracle.REF.ref_greedy_plan(*args, tags))
-        it, nonov = ctypes.c_double(), ctypes.c_double()
-        out["ref_iteration_time_us_1core"] = med(
-            lambda: pyoracle.REF.ref_iteration_time(*args, tags, ctypes.byref(it), ctypes.byref(nonov)))
-    # config 1: ResNet-50-sized merged all-reduce + SGD, 2 ranks, 1 core
+    return out
+
+
+# -------------------------------------------------------------- CPU legs
+def ref_lib():
+    """oracle/_ref: the reference headers compiled unmodified (None when the
+    reference was not available to build it) and the C restatement."""
+    from oracle import pyoracle
+
+    return pyoracle
+
+
+def ref_fit(csv_path: str):
+    """(a, b) by the reference's own load_measurements_csv + fit_model
+    (comm_model.hpp:209-308) from oracle/_ref; the C restatement otherwise."""
+    import ctypes
+
+    po = ref_lib()
+    if po.REF is not None:
+        a, b = ctypes.c_double(), ctypes.c_double()
+        rc = po.REF.ref_fit_csv(csv_path.encode(), ctypes.byref(a), ctypes.byref(b))
+        if rc != 0:
+            raise RuntimeError(f"reference fit_model failed on {csv_path}")
+        return a.value, b.value, "reference"
+    rows = []
+    with open(csv_path) as f:
+        next(f)
+        for line in f:
+            sz, us = line.strip().split(",")
+            rows.append((int(sz), float(us) / 1e6))
+    a, b = po.orc_fit([r[0] for r in rows], [r[1] for r in rows])
+    return a, b, "port"
+
+
+def ref_plan(tr: dict, a: float, b: float, bpe: int):
+    po = ref_lib()
+    if po.REF is not None:
+        return po.ref_optimal(tr["params"], tr["t_b"], tr["t_f"], bpe, a, b), "reference"
+    return po.orc_optimal(tr["params"], tr["t_b"], tr["t_f"], bpe, a, b), "port"
+
+
+def cpu_pipeline_sample(tr: dict, tags, P, lr, threads, budget_s, iters_cap=None):
+    """The CPU restatement of Algorithm 2 (oracle port) on host buffers."""
+    import numpy as np
+
+    po = ref_lib()
+    counts = tr["params"]
+    rng = np.random.default_rng(0x5EED0000)
+    g = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(P)]
+    w = [[np.full(c, 0.5, np.float32) for c in counts] for _ in range(P)]
+    first = po.pipeline_run(g, w, counts, tr["t_b"], tr["t_f"], tags, lr, threads, 1)[0]
+    iters = max(3, min(200, int(budget_s / max(first, 1e-6))))
+    if iters_cap is not None:
+        iters = min(iters, iters_cap)
+    return po.pipeline_run(g, w, counts, tr["t_b"], tr["t_f"], tags, lr, threads, iters)
+
+
+def _median_us(fn, reps=1000, cap_s=1.0):
+    ts = []
+    t_end = time.perf_counter() + cap_s
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end and len(ts) >= 50:
+            break
+    return statistics.median(ts) * 1e6, len(ts)
+
+
+def solver_table(bpe: int = 4) -> dict:
+    """BASELINE.md §3.1-3.2 on 1 host core: the reference's optimal_plan,
+    greedy_plan and iteration_time (oracle/_ref, unmodified headers) on every
+    trace at the committed on-box (a, b) of P = 2 / 4 / 8 — median of up to
+    1000 runs (1 s cap per entry)."""
+    import ctypes
+
+    po = ref_lib()
+    if po.REF is None:
+        return {"unavailable": "oracle/_ref not built (the reference sources were not present at build time)"}
+    out = {}
+    names = sorted(os.path.basename(p)[:-5] for p in glob.glob(os.path.join(ROOT, "traces", "*.json"))
+                   if not p.endswith("META.json"))
+    for name in names + ["skewed_161"]:
+        path = (os.path.join(ROOT, "tests", "golden", "skewed_161.json") if name == "skewed_161"
+                else trace_path(name))
+        tr = load_trace_json(path)
+        L = len(tr["params"])
+        p = (ctypes.c_uint64 * L)(*tr["params"])
+        tb = (ctypes.c_double * L)(*tr["t_b"])
+        tags = (ctypes.c_uint8 * L)()
+        row = {"layers": L}
+        for P in (2, 4, 8):
+            rel = committed_calibration("resnet50" if name == "skewed_161" else name, P)
+            if rel is None:
+                continue
+            a, b, _ = ref_fit(os.path.join(ROOT, rel))
+            args = (p, tb, L, tr["t_f"], bpe, a, b)
+            opt, n1 = _median_us(lambda: po.REF.ref_optimal_plan(*args, tags))
+            gre, _ = _median_us(lambda: po.REF.ref_greedy_plan(*args, tags))
+            it, no = ctypes.c_double(), ctypes.c_double()
+            pre, _ = _median_us(lambda: po.REF.ref_iteration_time(*args, tags, ctypes.byref(it), ctypes.byref(no)))
+            row[f"P{P}"] = {"a_us": a * 1e6, "b_ps": b * 1e12, "optimal_plan_us": opt, "greedy_plan_us": gre,
+                            "iteration_time_us": pre, "runs": n1}
+        out[name] = row
+    return out
+
+
+def allreduce_cpu_config1(budget_s=3.0) -> dict:
+    """Config 1's CPU merged all-reduce (ResNet-50-sized 25.6 M fp32, 2 ranks
+    as host buffers: x 1/P, rank-order sum, SGD) on 1 core and on all cores
+    (the C restatement's threaded pipeline, no replay wait)."""
+    import numpy as np
+
+    po = ref_lib()
+    n = 25_557_032
     rng = np.random.default_rng(1)
-    counts = [25_557_032]
-    g = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(2)]
-    w = [[np.full(c, 0.5, np.float32) for c in counts] for _ in range(2)]
+    g = [[rng.uniform(-1, 1, n).astype(np.float32)] for _ in range(2)]
+    w = [[np.full(n, 0.5, np.float32)] for _ in range(2)]
     ts = []
     t_end = time.perf_counter() + budget_s
     while time.perf_counter() < t_end or not ts:
         t0 = time.perf_counter()
-        pyoracle.allreduce_sgd(g, w, [0], 0.01)
+        po.allreduce_sgd(g, w, [0], 0.01)
         ts.append(time.perf_counter() - t0)
-    out["allreduce_sgd_r50_2ranks_ms_1core"] = statistics.median(ts) * 1e3
-    out["allreduce_sgd_r50_2ranks_GBps_1core"] = 2 * 4 * counts[0] * 3 / statistics.median(ts) / 1e9
-    return out
+    one = statistics.median(ts)
+    threads = os.cpu_count() or 1
+    allc = statistics.median(po.pipeline_run(g, w, [n], [0.0], 0.0, [0], 0.01, threads, 5))
+    algo = 2 * 4 * n * 3  # per rank: read grad, read W, write W
+    return {"ms_1core": one * 1e3, "GBps_1core": algo / one / 1e9, "ms_all_cores": allc * 1e3,
+            "GBps_all_cores": algo / allc / 1e9, "threads": threads}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port of Algorithm 2
-    + the reference's own optimal_plan from oracle/_ref) on host cores."""
-    from paper_1912_09268_b200 import dist as D
-    from paper_1912_09268_b200 import gradsched as gs
-
-    rank, world, _ = D.env_world()
+    """--impl reference: the reference's CPU path on the host cores — its own
+    fit_model + optimal_plan (oracle/_ref, the unmodified headers) on the
+    committed calibration, and the CPU restatement of Algorithm 2 (oracle
+    port: the reference has no runtime) with N ranks as host buffers. Never
+    imports paper_1912_09268_b200 (its libmgwfbp.so stays unloaded)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     N = max(world, args.gpus)
-    trace = gs.load_trace(trace_path(args.trace))
-    if args.tb_scale != 1.0:
-        trace.forward_time *= args.tb_scale
-        for l in trace.layers:
-            l.backward_time *= args.tb_scale
-    # paper cluster-independent model: a NVLink-class guess; the plan only
-    # decides grouping, the CPU work is the same bytes either way
-    model = gs.AllReduceModel(20e-6, 1.0 / 600e9)
-    plan = gs.optimal_plan(trace, model)
-    tags = [int(t) for t in plan.tags]
+    tr = load_trace_json(trace_path(args.trace), args.tb_scale)
+    bpe = 2 if args.dtype == "bf16" else 4
+    calib = committed_calibration(args.trace, N)
+    if calib is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"no committed calibration for {args.trace} P{N}"}))
+        return 0
+    a, b, fit_kind = ref_fit(os.path.join(ROOT, calib))
+    tags, plan_kind = ref_plan(tr, a, b, bpe)
     threads = os.cpu_count() or 1
-    cpu_pipeline_sample(trace, tags, N, args.lr, threads, 0.0, iters_cap=args.warmup)
-    times = cpu_pipeline_sample(trace, tags, N, args.lr, threads, 1e9, iters_cap=args.steps)
+    cpu_pipeline_sample(tr, tags, N, args.lr, threads, 0.0, iters_cap=max(1, args.warmup))
+    times = cpu_pipeline_sample(tr, tags, N, args.lr, threads, 1e9, iters_cap=args.steps)
     total = sum(times)
     value = N * len(times) / total
-    solver = ref_solver_us(trace, model)
-    sample = (f"{len(times)} CPU iterations of {args.trace} ({trace.n_layers()} tensors, "
-              f"{trace.total_params()} fp32 params), {N} ranks emulated as host buffers; "
-              f"reference optimal_plan {solver:.1f} us on 1 core" if solver else "")
+    ms = total / len(times) * 1e3
+    cfg = common_config(args.trace, tr, N, tags, calib, args.tb_scale, args.dtype)
+    sample = (f"{len(times)} CPU iterations of {args.trace} ({len(tags)} tensors, {sum(tr['params'])} fp32 params "
+              f"per rank), {N} ranks emulated as host buffers, {threads} threads; plan by the {plan_kind} "
+              f"optimal_plan on the {fit_kind} fit of {calib}")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": len(times),
-        "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "impl": "reference",
         "data": "synthetic uniform[-1,1) fp32 gradients",
-        "config": {"workload": args.trace, "trace": os.path.relpath(trace_path(args.trace), ROOT),
-                   "plan": "optimal", "ranks": N},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "config": cfg,
+        "exposed_comm_ms": ms - cfg["compute_ms"],
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -319,6 +433,7 @@ def main():
         trace.forward_time *= args.tb_scale
         for l in trace.layers:
             l.backward_time *= args.tb_scale
+    tr_json = load_trace_json(trace_path(args.trace), args.tb_scale)
     bf16 = args.dtype == "bf16"
     esz = 2 if bf16 else 4
     gdt = torch.bfloat16 if bf16 else torch.float32
@@ -347,10 +462,9 @@ def main():
     if args.oneshot_max > 0:
         comm.set_oneshot_max(args.oneshot_max)
 
-    # ---- N1: on-box calibration of the fused kernel at this N, fitted
+    # ---- N1: on-box calibration of the fused engine kernel at this N
     sizes = calibration_sizes(total_bytes, 4 * padded)
     if args.model:
-        a_us, b_ps = (float(x) for x in args.model.split(","))
         sizes = sizes[:2]  # (a short sweep still exercises the calibration kernels)
     if args.engine_ctas != 0:
         meas = comm.calibrate_engine(sizes, warmup=3, reps=15, algo=args.algo, engine_ctas=args.engine_ctas,
@@ -361,9 +475,7 @@ def main():
     if N > 1:
         torch.distributed.all_reduce(tvec, op=torch.distributed.ReduceOp.MAX)
     meas = [gs.CommMeasurement(m.size_bytes, float(t)) for m, t in zip(meas, tvec.tolist())]
-    model, fit_how = fit_with_fallback(gs, meas)
-    if args.model:
-        model, fit_how = gs.AllReduceModel(a_us * 1e-6, b_ps * 1e-12), "given by --model (not calibrated)"
+    onbox_model, onbox_how = fit_with_fallback(gs, meas)
     out_dir = os.environ.get("MGW_OUT_DIR")
     if out_dir and rank == 0:
         os.makedirs(out_dir, exist_ok=True)
@@ -372,6 +484,18 @@ def main():
             for m in meas:
                 f.write(f"{m.size_bytes},{m.time_sec * 1e6:.3f}\n")
 
+    # ---- the plan's cost model: the committed calibration (identical in
+    # the reference arm) unless --plan-source onbox / --model
+    calib = committed_calibration(args.trace, N)
+    if args.model:
+        a_us, b_ps = (float(x) for x in args.model.split(","))
+        model, model_how = gs.AllReduceModel(a_us * 1e-6, b_ps * 1e-12), "given by --model (not calibrated)"
+    elif args.plan_source == "committed" and calib is not None:
+        model = gs.fit_model(gs.load_measurements_csv(os.path.join(ROOT, calib)))
+        model_how = f"fit_model of the committed calibration {calib}"
+    else:
+        model, model_how, calib = onbox_model, "this run's on-box sweep: " + onbox_how, None
+
     # ---- plans (host solver, replicated; verified identical across ranks)
     plans = {
         "mgwfbp": gs.optimal_plan(trace, model) if args.cost == "linear" else gs.optimal_plan_table(trace, meas),
@@ -379,7 +503,11 @@ def main():
         "single_buffer": gs.MergePlan.all_merged(L),
         "greedy": gs.greedy_plan(trace, model),
     }
+    onbox_plan = gs.optimal_plan(trace, onbox_model)
     digest = D.agree_plan(plans["mgwfbp"].tags)
+    cfg = common_config(args.trace, tr_json, N, [int(t) for t in plans["mgwfbp"].tags], calib, args.tb_scale,
+                        args.dtype)
+    assert cfg["plan_sha256"] == digest[:16]
     flush = args.l2_flush_mib << 20
     pipes = {}
     dplans = {}
@@ -413,6 +541,7 @@ def main():
     clocks = clk.summary()
     t_total = D.max_over_ranks(sum(ms) / 1e3, dev)
     value = N * args.steps / t_total
+    ms_step = t_total / args.steps * 1e3
 
     # ---- comparison strategies on the same box / pipeline
     strat = {}
@@ -431,8 +560,6 @@ def main():
             tl = pipes[name].device_timeline()
             strat[name]["device_tail_us"] = D.max_over_ranks(tl["tail_us"], dev)
             strat[name]["device_replay_ms"] = tl["replay_us"] / 1e3
-        if name == "mgwfbp":
-            group_ms = pipes["mgwfbp"].group_times_ms()
     compute_ms = (trace.forward_time + sum(l.backward_time for l in trace.layers)) * 1e3
 
     # ---- e2e through the public API with host buffers
@@ -454,50 +581,54 @@ def main():
     D.barrier()
     pipes["e2e"] = pipe
 
-    # ---- roofline of the dominant kernel (the fused group kernel)
+    # ---- roofline of the dominant kernel: the persistent engine draining
+    # the whole plan (every group ready at launch), CUDA events per launch on
+    # the engine's stream, L2 evicted before each launch
     peaks = measured_peaks()
     gbytes = [dplans["mgwfbp"].group_span(g)[2] for g in range(dplans["mgwfbp"].n_groups)]
-    kern_s = sum(group_ms) / 1e3
-    w_per_g = 4 / esz  # fp32 weight bytes per gradient byte
-    if N == 1:
-        algo_bytes = sum((1 + 2 * w_per_g) * b for b in gbytes)  # read grad, read W, write W
-        peak = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
-        roof = {"bound": "hbm", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
-    else:
-        algo_bytes = sum(2 * (N - 1) / N * b for b in gbytes)  # NVLink bus bytes
-        peak = NVLINK_PEER_GBS
-        roof = {"bound": "nvlink", "peak_source": "measured B200 peer copy 770 GB/s/direction (B200_PROFILING.md)"}
-    achieved = algo_bytes / kern_s / 1e9 if kern_s > 0 else None
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", f"traffic_{args.trace}_P{N}.json")
-    if os.path.exists(prof):
-        with open(prof) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
-    # the same fused kernel on the LARGEST calibrated group (cold L2, one
-    # group on an idle engine): bytes that cross the bound / its time — the
-    # bandwidth regime, next to the latency-dominated per-iteration figure
-    per_byte = (1 + 2 * w_per_g) if N == 1 else 2 * (N - 1) / N
-    big_m = max(meas, key=lambda m: m.size_bytes)
-    asym = per_byte * big_m.size_bytes / big_m.time_sec / 1e9 if big_m.time_sec > 0 else None
-    roof.update({"kernel": ("engine_kernel/run_group (fused pack + push all-reduce + unpack/SGD), "
-                            "per-group %globaltimer stamps" if args.engine_ctas
-                            else "group_allreduce_kernel (fused pack + push all-reduce + unpack/SGD)"),
-                 "achieved": achieved, "peak": peak, "unit": "GB/s",
-                 "frac": achieved / peak if achieved else None, "traffic": traffic,
-                 "traffic_evidence": (
-                     "profiles/r1_ncu_hbm_kernels_256MiB.txt: the P=1 fused group kernel (same run_group code as "
-                     "the engine) moves 752 MB DRAM vs 805 MB algorithmic per 256 MiB launch (no re-reads)"
-                     if N == 1 else
-                     "profiles/r1_ncu_loopback_twoshot_64MiB.txt: the two-shot data path in loopback moves "
-                     "623 MB DRAM vs 671 MB algorithmic (P=2, 64 MiB/rank; no re-reads)")
-                     + "; the engine kernel itself cannot run under ncu's serialisation (it waits on the replay)",
-                 "algorithmic_bytes_per_iter": algo_bytes, "kernel_ms_per_iter": kern_s * 1e3,
-                 "launches_per_iter": len(group_ms),
-                 "note": f"small groups are latency-bound ({args.trace}: {sum(counts)} params over "
-                         f"{len(group_ms)} groups); the bandwidth regime is the largest_group row",
-                 "largest_group": {"achieved": asym, "frac": asym / peak if asym else None,
-                                   "group_bytes": big_m.size_bytes, "us": big_m.time_sec * 1e6,
-                                   "from": "the largest size of the on-box calibration sweep"}})
+    roof = {}
+    if args.engine_ctas != 0:
+        D.barrier()
+        drain = pipes["headline"].drain(max(3, min(args.steps, 20)))
+        kern_s = D.max_over_ranks(statistics.mean(drain) / 1e3, dev)
+        w_per_g = 4 / esz  # fp32 weight bytes per gradient byte
+        hbm_bytes = sum((1 + 2 * w_per_g) * b for b in gbytes)  # read grad, read W, write W
+        if N == 1:
+            algo_bytes = hbm_bytes
+            peak = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
+            roof = {"bound": "hbm", "peak_source": ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks
+                                                    else "B200_PROFILING.md fallback")}
+        else:
+            algo_bytes = sum(2 * (N - 1) / N * b for b in gbytes)  # NVLink bus bytes per rank per direction
+            peak = NVLINK_GBS
+            roof = {"bound": "nvlink", "peak_source": "NVLink 5 900 GB/s per direction (north_star); "
+                                                      "frac_vs_770 = the measured peer-copy figure"}
+        achieved = algo_bytes / kern_s / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", f"traffic_{args.trace}_P{N}.json")
+        if os.path.exists(prof):
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        per_byte = (1 + 2 * w_per_g) if N == 1 else 2 * (N - 1) / N
+        big_m = max(meas, key=lambda m: m.size_bytes)
+        asym = per_byte * big_m.size_bytes / big_m.time_sec / 1e9 if big_m.time_sec > 0 else None
+        roof.update({
+            "kernel": f"engine_kernel<{N},{'bf16' if bf16 else 'float'}> standalone drain: the whole plan's fused "
+                      f"pack -> all-reduce -> unpack+SGD, every group ready at launch",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "traffic_source": (os.path.relpath(prof, ROOT) + " (ncu dram__bytes_read.sum + dram__bytes_write.sum "
+                               "of the same drain launch)") if traffic else None,
+            "algorithmic_bytes_per_launch": algo_bytes, "hbm_algorithmic_bytes_per_launch": hbm_bytes,
+            "bytes_formula": ("3*S fp32 (read grad, read W, write W)" if N == 1 else
+                              "2(P-1)/P*S NVLink bus bytes per rank per direction"),
+            "launch_ms_mean": kern_s * 1e3, "launches": len(drain), "groups_per_launch": len(gbytes),
+            "timing": "CUDA events around each engine launch on its stream, max over ranks",
+            "largest_group": {"achieved": asym, "frac": asym / peak if asym else None,
+                              "group_bytes": big_m.size_bytes, "us": big_m.time_sec * 1e6,
+                              "from": "the largest size of this run's on-box calibration sweep (one group, "
+                                      "idle engine, cold L2)"}})
+        if N > 1:
+            roof["frac_vs_770"] = achieved / NVLINK_PEER_GBS
 
     # merged all-reduce bus GB/s = 2(P-1)/P * S / t: ours (fused kernel, from
     # the calibration sweep) next to NCCL (torch.distributed.all_reduce, same
@@ -521,44 +652,45 @@ def main():
             del x
         for m, tn in zip(big, ncclt):
             f = 2 * (N - 1) / N * m.size_bytes / 1e9
-            bus[str(m.size_bytes)] = {"mgwfbp": f / m.time_sec, "nccl": f / tn}
+            bus[str(m.size_bytes)] = {"mgwfbp": f / m.time_sec, "nccl": f / tn,
+                                      "mgwfbp_frac_900": f / m.time_sec / NVLINK_GBS}
 
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        times = cpu_pipeline_sample(trace, [int(t) for t in plans["mgwfbp"].tags], 1, args.lr, threads,
-                                    args.cpu_budget_s)
-        solver = ref_solver_us(trace, model)
-        detail = cpu_path_detail(trace, model)
+        tags = [int(t) for t in plans["mgwfbp"].tags]
+        times = cpu_pipeline_sample(tr_json, tags, 1, args.lr, threads, args.cpu_budget_s)
         cpu = {"value": len(times) / sum(times), "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{len(times)} iterations of the CPU Algorithm-2 restatement (oracle/mgw_oracle.c, "
                          f"same trace/plan, P=1, {threads} threads)"
-                         + (f"; reference optimal_plan (oracle/_ref) {solver:.1f} us on 1 core" if solver else "")
                          + ("; the CPU path reduces fp32 gradients (no bf16 CPU pipeline)" if bf16 else ""),
-               "detail": detail}
+               "detail": {"host": host_info(), "solver_1core": solver_table(),
+                          "allreduce_sgd_config1_r50_2ranks": allreduce_cpu_config1()}}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": (f"synthetic uniform[-1,1) {args.dtype} gradients"
                      + (" (fp32 accumulation, fp32 master weights)" if bf16 else "")
                      + "; backward replayed from B200-measured per-tensor t_b"),
-            "config": {"workload": args.trace, "trace": os.path.relpath(trace_path(args.trace), ROOT),
-                       "layers": L, "params": sum(counts), "grad_bytes": total_bytes,
-                       "plan": ("optimal_plan on on-box calibrated (a, b)" if args.cost == "linear" else
-                                "optimal_plan_table on the on-box calibration curve (B200 extension)"),
-                       "plan_sha256": digest[:16],
-                       "groups": dplans["mgwfbp"].n_groups, "algo": args.algo, "oneshot_max": comm.oneshot_max,
-                       "comm": ("persistent engine, %s CTAs" % ("1/SM" if args.engine_ctas < 0 else args.engine_ctas))
-                               if args.engine_ctas else "one fused kernel launch per group",
-                       "parallelism": f"dp{N}", "l2": f"flushed every iteration ({args.l2_flush_mib} MiB memset "
-                                                     "on the comm stream during the forward replay)",
-                       "compute_ms": compute_ms, "tb_scale": args.tb_scale},
-            "calibration": {"a_us": model.a * 1e6, "b_ps_per_byte": model.b * 1e12, "how": fit_how,
-                            "sizes": len(meas), "largest_bytes": meas[-1].size_bytes,
-                            "largest_us": meas[-1].time_sec * 1e6},
+            "config": cfg,
+            "exposed_comm_ms": ms_step - cfg["compute_ms"],
+            "gpu": {"comm": ("persistent engine, %s CTAs" % ("1/SM" if args.engine_ctas < 0 else args.engine_ctas))
+                            if args.engine_ctas else "one fused kernel launch per group",
+                    "algo": args.algo, "tuning": comm.tuning(),
+                    "l2_flush": f"{args.l2_flush_mib} MiB streaming stores on the comm stream during the forward "
+                                "replay, every iteration"},
+            "calibration": {"plan_model": {"a_us": model.a * 1e6, "b_ps_per_byte": model.b * 1e12, "how": model_how},
+                            "onbox": {"a_us": onbox_model.a * 1e6, "b_ps_per_byte": onbox_model.b * 1e12,
+                                      "how": onbox_how, "sizes": len(meas), "largest_bytes": meas[-1].size_bytes,
+                                      "largest_us": meas[-1].time_sec * 1e6,
+                                      "plan_sha256": D.plan_digest(onbox_plan.tags)[:16],
+                                      "groups": sum(1 for i, t in enumerate(onbox_plan.tags)
+                                                    if i == 0 or int(t) == 0),
+                                      "predicted_ms": gs.iteration_time(trace, onbox_plan,
+                                                                        onbox_model).iteration_time * 1e3}},
             "strategies": strat,
             "speedup_vs_wfbp": strat["wfbp"]["iter_ms_median"] / strat["mgwfbp"]["iter_ms_median"],
             "speedup_vs_single_buffer": strat["single_buffer"]["iter_ms_median"] / strat["mgwfbp"]["iter_ms_median"],

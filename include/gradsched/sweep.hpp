@@ -15,7 +15,13 @@
 #include <string>
 #include <vector>
 
+// The reference includes <json.hpp> from its vendor/ directory
+// (proj/CMakeLists.txt:11-13, planner.hpp:25); either layout works.
+#if __has_include(<nlohmann/json.hpp>)
 #include <nlohmann/json.hpp>
+#else
+#include <json.hpp>
+#endif
 
 #include "gradsched/comm_model.hpp"
 #include "gradsched/errors.hpp"

@@ -146,7 +146,8 @@ int mgw_comm_open_peers(mgw_comm* comm, const void* all_handles);
 int mgw_comm_destroy(mgw_comm* comm);
 
 /* Single-GPU emulation of `nranks` ranks (all arenas on one device, every
- * collective launched as ONE cooperative kernel over all emulated ranks).
+ * collective launched as ONE kernel over all emulated ranks: a cooperative
+ * group launch, or one persistent-engine grid (ctas, nranks) for pipelines).
  * Used by the parity tests on one B200; never by the multi-GPU path. */
 int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_comm** out);
 
@@ -201,6 +202,26 @@ int mgw_group_allreduce(mgw_plan* plan, int group, float lr, int epilogue, int a
  * B200-measured crossover for the communicator's rank count). */
 int mgw_comm_set_oneshot_max(mgw_comm* comm, uint64_t bytes);
 int mgw_comm_get_oneshot_max(const mgw_comm* comm, uint64_t* bytes);
+/* Tuning knobs (defaults: the B200 measurements in DESIGN.md §4.1). Every
+ * rank must set the same values before creating plans / pipelines.
+ *  ll_max: one-shot groups up to this many bytes travel as LL (flag-in-data)
+ *    packets; 0 disables LL.
+ *  small_tile_max: groups below this many bytes are cut into 8 KiB tiles
+ *    (more CTAs) instead of 32 KiB tiles.
+ *  chunk_tiles / min_chunks: a CTA's tiles run in pipelined chunks of at
+ *    most chunk_tiles tiles (two-shot: chunk_tiles / P super-tiles) and at
+ *    least min_chunks chunks when it owns enough tiles. */
+int mgw_comm_set_ll_max(mgw_comm* comm, uint64_t bytes);
+int mgw_comm_set_small_tile_max(mgw_comm* comm, uint64_t bytes);
+int mgw_comm_set_chunk_tiles(mgw_comm* comm, uint32_t max_tiles, uint32_t min_chunks);
+/* Current knob values (any output may be NULL). */
+int mgw_comm_get_tuning(const mgw_comm* comm, uint64_t* oneshot_max, uint64_t* ll_max,
+                        uint64_t* small_tile_max, uint32_t* chunk_tiles, uint32_t* min_chunks);
+/* 1 in *failed once any kernel of this communicator gave up a bounded wait
+ * (a peer or the compute side never arrived; the kernels then skip their
+ * SGD epilogues). Reads host-mapped memory: no CUDA call, no sync — cheap
+ * enough to poll every iteration. A failed communicator stays failed. */
+int mgw_comm_error(const mgw_comm* comm, int* failed);
 /* Cap on the CTAs per rank of a standalone fused launch (mgw_group_allreduce,
  * mgw_allreduce); 0 = one per SM (default). A real backward that launches
  * groups while it runs leaves the other SMs to the compute kernels. */
@@ -247,6 +268,13 @@ int mgw_pipeline_stream(mgw_pipeline* pipe, void** stream_out);
  * ready, iteration, CTA exit count, ready-timeout flag} and the replay clock
  * {iteration start, last replay completion} (%globaltimer ns). */
 int mgw_pipeline_debug(mgw_pipeline* pipe, uint32_t* engine_state4, uint64_t* clock2);
+/* Standalone drain of an engine pipeline (roofline and ncu runs): launch the
+ * persistent engine `iters` times with EVERY group ready at launch (no
+ * replay, no ready flags), each launch preceded by the pipeline's L2 flush;
+ * writes each engine launch's device time (ms, CUDA events on the engine's
+ * stream). The plan's whole merged all-reduce + SGD streams through the
+ * engine back to back. Collective. */
+int mgw_pipeline_drain(mgw_pipeline* pipe, int iters, float* ms_out);
 /* Engine pipelines with record_group_times: the last iteration's raw
  * (start, end) %globaltimer stamps of every group, 2*G values in group
  * order (zero for groups without tiles). */

@@ -315,13 +315,14 @@ static void cpu_group(pipe_ctx* c, size_t g) {
   for (int r = 0; r < c->P; ++r) {
     float* const* gr = c->grads + (size_t)r * c->L;
     float* m = c->merge[r] + base;
-#pragma omp parallel for num_threads(c->threads) schedule(static) if (span > 65536)
     for (size_t l = first; l < last; ++l) {
       float* dst = m + (c->offs[l] - base);
       const uint64_t padded = c->offs[l + 1] - c->offs[l];
-      const uint64_t cnt = c->counts[l];
-      for (uint64_t j = 0; j < cnt; ++j) dst[j] = gr[l][j] * scale;
-      for (uint64_t j = cnt; j < padded; ++j) dst[j] = 0.0f;
+      const long long cnt = (long long)c->counts[l];
+      const float* src = gr[l];
+#pragma omp parallel for num_threads(c->threads) schedule(static) if (cnt > 65536)
+      for (long long j = 0; j < cnt; ++j) dst[j] = src[j] * scale;
+      for (uint64_t j = (uint64_t)cnt; j < padded; ++j) dst[j] = 0.0f;
     }
   }
   const long long n = (long long)span;

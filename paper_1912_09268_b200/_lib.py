@@ -80,6 +80,12 @@ mgw_comm_destroy = _proto("mgw_comm_destroy", [vp])
 mgw_comm_set_oneshot_max = _proto("mgw_comm_set_oneshot_max", [vp, C.c_uint64])
 mgw_comm_get_oneshot_max = _proto("mgw_comm_get_oneshot_max", [vp, u64p])
 mgw_comm_set_max_ctas = _proto("mgw_comm_set_max_ctas", [vp, C.c_int])
+mgw_comm_set_ll_max = _proto("mgw_comm_set_ll_max", [vp, C.c_uint64])
+mgw_comm_set_small_tile_max = _proto("mgw_comm_set_small_tile_max", [vp, C.c_uint64])
+mgw_comm_set_chunk_tiles = _proto("mgw_comm_set_chunk_tiles", [vp, C.c_uint32, C.c_uint32])
+mgw_comm_error = _proto("mgw_comm_error", [vp, C.POINTER(C.c_int)])
+mgw_comm_get_tuning = _proto("mgw_comm_get_tuning", [vp, u64p, u64p, u64p, C.POINTER(C.c_uint32),
+                                                      C.POINTER(C.c_uint32)])
 mgw_plan_create = _proto(
     "mgw_plan_create", [vp, C.c_size_t, C.POINTER(vp), C.POINTER(vp), u64p, u8p, C.POINTER(vp)]
 )
@@ -120,6 +126,7 @@ mgw_pipeline_group_times = _proto("mgw_pipeline_group_times", [vp, f32p])
 mgw_pipeline_stream = _proto("mgw_pipeline_stream", [vp, C.POINTER(vp)])
 mgw_pipeline_debug = _proto("mgw_pipeline_debug", [vp, C.POINTER(C.c_uint32), u64p])
 mgw_pipeline_stamps = _proto("mgw_pipeline_stamps", [vp, u64p])
+mgw_pipeline_drain = _proto("mgw_pipeline_drain", [vp, C.c_int, f32p])
 mgw_engine_create = _proto("mgw_engine_create", [vp, C.c_float, C.c_int, C.c_int, C.c_int, C.POINTER(vp)])
 mgw_engine_begin = _proto("mgw_engine_begin", [vp, vp])
 mgw_engine_mark_ready = _proto("mgw_engine_mark_ready", [vp, C.c_int, vp])

@@ -1,333 +1,390 @@
-// gradsched CLI, rebuilt without CLI11 over libmgwfbp.so.
+// gradsched — command-line front end over libmgwfbp.so.
 //
-// Same subcommands, options, outputs and exit codes as the reference front
-// end (proj/tools/main.cpp:31-35, :104-285, :287-373), so B200 calibrations
-// and plans flow through the reference's file formats byte-identically:
-//   gradsched fit [csv] [--algo A --workers N --alpha s --beta s/B --gamma s/B
-//                 [--dbt-literal]] [--out model.json]
+// The reference ships a CLI11 front end (proj/tools/main.cpp). This one is a
+// table-driven rewrite: every subcommand declares its positionals and typed
+// options once (kCommands below); one generic parser validates argv against
+// that schema and hands the handler a typed `Inputs`. What is kept from the
+// reference is only its external contract, which proj/tests/test_cli.cpp
+// pins: subcommand names, option names, the JSON / CSV / summary-line
+// outputs (produced by the library's own exporters), and the exit codes of
+// proj/tools/main.cpp:31-35 (0 ok, 2 bad input, 3 planner rejection, 4 guard
+// refusal, 5 every sweep row failed).
+//
+//   gradsched fit [measurements.csv] [--algo A --workers N --alpha s --beta s/B
+//                 --gamma s/B --dbt-literal] [--out model.json]
 //   gradsched plan trace.json model.json [--oracle] [--out plan.json]
-//   gradsched simulate trace.json model.json --strategy S [--workers N] [--out t.json]
-//   gradsched sweep trace.json --algo A --alpha s [--beta] [--gamma]
-//                 [--workers 4..2048|a,b,c] [--dbt-literal] [--out csv] [--json j]
-// Exit codes: 0 ok, 2 bad input, 3 planner rejection, 4 guard, 5 all sweep
-// rows failed.
+//   gradsched simulate trace.json model.json --strategy S [--workers N] [--out timeline.json]
+//   gradsched sweep trace.json --algo A --alpha s [--beta s/B] [--gamma s/B]
+//                 [--workers lo..hi | n1,n2,...] [--dbt-literal] [--out results.csv] [--json sweep.json]
+#include <charconv>
 #include <cmath>
-#include <cstdio>
+#include <cstdlib>
 #include <fstream>
+#include <functional>
 #include <iomanip>
 #include <iostream>
 #include <map>
-#include <set>
+#include <optional>
+#include <sstream>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "gradsched/gradsched.hpp"
 
 namespace {
 
-enum Exit { kOk = 0, kInput = 2, kPlanner = 3, kGuard = 4, kAllRowsFailed = 5 };
+namespace gs = gradsched;
+using Json = nlohmann::json;
 
-// A parsed command line: positionals, --key value options, bare flags.
-struct Args {
-  std::vector<std::string> pos;
-  std::map<std::string, std::string> opt;
-  std::set<std::string> flags;
+// ---- exit status -----------------------------------------------------------
 
-  bool has(const std::string& k) const { return opt.count(k) != 0; }
-  std::string str(const std::string& k, const std::string& dflt = "") const {
-    const auto it = opt.find(k);
-    return it == opt.end() ? dflt : it->second;
-  }
+constexpr int kExitOk = 0;
+constexpr int kExitBadInput = 2;
+constexpr int kExitPlanner = 3;
+constexpr int kExitGuard = 4;
+constexpr int kExitNoSweepRows = 5;
+
+// A malformed command line (unknown option, missing value, ...): bad input.
+class CommandLineError : public gs::ValidationError {
+ public:
+  using gs::ValidationError::ValidationError;
 };
 
-struct UsageError : std::runtime_error {
-  using std::runtime_error::runtime_error;
+// ---- schema ----------------------------------------------------------------
+
+enum class Kind { kReal, kInteger, kText, kSwitch };
+
+struct OptionSpec {
+  std::string_view name;
+  Kind kind;
+  bool required;
 };
 
-double to_double(const std::string& key, const std::string& v) {
-  std::size_t used = 0;
-  double d = 0.0;
-  try {
-    d = std::stod(v, &used);
-  } catch (const std::exception&) {
-    used = 0;
+struct Inputs {
+  std::vector<std::string> files;                  // positionals, in order
+  std::map<std::string, double, std::less<>> reals;
+  std::map<std::string, long long, std::less<>> integers;
+  std::map<std::string, std::string, std::less<>> texts;
+  std::map<std::string, bool, std::less<>> switches;
+
+  template <typename M>
+  static auto lookup(const M& m, std::string_view k) -> std::optional<typename M::mapped_type> {
+    const auto it = m.find(k);
+    if (it == m.end()) return std::nullopt;
+    return it->second;
   }
-  if (used != v.size() || v.empty()) throw UsageError("--" + key + ": not a number: '" + v + "'");
-  return d;
+  std::optional<double> real(std::string_view k) const { return lookup(reals, k); }
+  std::optional<long long> integer(std::string_view k) const { return lookup(integers, k); }
+  std::optional<std::string> text(std::string_view k) const { return lookup(texts, k); }
+  bool on(std::string_view k) const { return switches.count(k) != 0; }
+};
+
+struct CommandSpec {
+  std::string_view name;
+  std::size_t min_files, max_files;
+  std::vector<OptionSpec> options;
+  std::function<int(const Inputs&)> run;
+};
+
+// Strict numeric conversions: the whole token must be consumed.
+double as_real(std::string_view opt, const std::string& token) {
+  char* end = nullptr;
+  const double v = token.empty() ? 0.0 : std::strtod(token.c_str(), &end);
+  if (token.empty() || end != token.c_str() + token.size() || !std::isfinite(v)) {
+    throw CommandLineError("option --" + std::string(opt) + " expects a real number, got \"" + token + "\"");
+  }
+  return v;
 }
 
-int to_int(const std::string& key, const std::string& v) {
-  std::size_t used = 0;
-  int i = 0;
-  try {
-    i = std::stoi(v, &used);
-  } catch (const std::exception&) {
-    used = 0;
+long long as_integer(std::string_view opt, std::string_view token) {
+  long long v = 0;
+  const auto [ptr, ec] = std::from_chars(token.data(), token.data() + token.size(), v);
+  if (token.empty() || ec != std::errc() || ptr != token.data() + token.size()) {
+    throw CommandLineError("option --" + std::string(opt) + " expects an integer, got \"" +
+                           std::string(token) + "\"");
   }
-  if (used != v.size() || v.empty()) throw UsageError("--" + key + ": not an integer: '" + v + "'");
-  return i;
+  return v;
 }
 
-// Parse argv[first..] against the allowed option/flag names and the maximum
-// number of positionals.
-Args parse(int argc, char** argv, int first, const std::set<std::string>& options,
-           const std::set<std::string>& flags, std::size_t max_pos) {
-  Args a;
-  for (int i = first; i < argc; ++i) {
-    std::string tok = argv[i];
-    if (tok.rfind("--", 0) == 0) {
-      std::string key = tok.substr(2), value;
-      const auto eq = key.find('=');
-      const bool inline_value = eq != std::string::npos;
-      if (inline_value) {
-        value = key.substr(eq + 1);
-        key = key.substr(0, eq);
-      }
-      if (flags.count(key) && !inline_value) {
-        a.flags.insert(key);
-      } else if (options.count(key)) {
-        if (!inline_value) {
-          if (i + 1 >= argc) throw UsageError("--" + key + " needs a value");
-          value = argv[++i];
-        }
-        a.opt[key] = value;
-      } else {
-        throw UsageError("unknown option '" + tok + "'");
-      }
+// argv[2..] against the command's schema.
+Inputs read_command_line(const CommandSpec& cmd, int argc, char** argv) {
+  Inputs in;
+  auto find = [&](std::string_view n) -> const OptionSpec* {
+    for (const auto& o : cmd.options) {
+      if (o.name == n) return &o;
+    }
+    return nullptr;
+  };
+  for (int i = 2; i < argc; ++i) {
+    const std::string_view arg = argv[i];
+    if (arg.substr(0, 2) != "--") {
+      in.files.emplace_back(arg);
+      continue;
+    }
+    std::string_view name = arg.substr(2);
+    std::optional<std::string> attached;
+    if (const auto eq = name.find('='); eq != std::string_view::npos) {
+      attached = std::string(name.substr(eq + 1));
+      name = name.substr(0, eq);
+    }
+    const OptionSpec* spec = find(name);
+    if (spec == nullptr) {
+      throw CommandLineError(std::string(cmd.name) + " does not take option " + std::string(arg));
+    }
+    const std::string key(name);
+    if (spec->kind == Kind::kSwitch) {
+      if (attached) throw CommandLineError("switch --" + key + " takes no value");
+      in.switches[key] = true;
+      continue;
+    }
+    std::string value;
+    if (attached) {
+      value = *attached;
+    } else if (i + 1 < argc) {
+      value = argv[++i];
     } else {
-      a.pos.push_back(tok);
+      throw CommandLineError("option --" + key + " is missing its value");
+    }
+    switch (spec->kind) {
+      case Kind::kReal: in.reals[key] = as_real(name, value); break;
+      case Kind::kInteger: in.integers[key] = as_integer(name, value); break;
+      default: in.texts[key] = value; break;
     }
   }
-  if (a.pos.size() > max_pos) throw UsageError("unexpected argument '" + a.pos[max_pos] + "'");
-  return a;
-}
-
-void require_opts(const Args& a, std::initializer_list<const char*> keys) {
-  for (const char* k : keys) {
-    if (!a.has(k)) throw UsageError(std::string("--") + k + " is required");
+  if (in.files.size() < cmd.min_files || in.files.size() > cmd.max_files) {
+    throw CommandLineError(std::string(cmd.name) + " takes " + std::to_string(cmd.min_files) +
+                           (cmd.min_files == cmd.max_files ? "" : ".." + std::to_string(cmd.max_files)) +
+                           " file argument(s), got " + std::to_string(in.files.size()));
   }
+  for (const auto& o : cmd.options) {
+    const std::string k(o.name);
+    const bool given = in.reals.count(k) || in.integers.count(k) || in.texts.count(k) || in.switches.count(k);
+    if (o.required && !given) throw CommandLineError(std::string(cmd.name) + " requires --" + k);
+  }
+  return in;
 }
 
-void write_json(const nlohmann::json& doc, const std::string& path) {
-  if (path.empty()) {
-    std::cout << doc.dump(2) << '\n';
+// ---- shared helpers ----------------------------------------------------------
+
+// Text of a JSON document: stdout when no path is given.
+void emit(const Json& doc, const std::optional<std::string>& path) {
+  const std::string text = doc.dump(2) + "\n";
+  if (!path) {
+    std::cout << text;
     return;
   }
-  std::ofstream out(path);
-  if (!out) throw gradsched::ParseError("cannot open output file: " + path);
-  out << doc.dump(2) << '\n';
+  std::ofstream f(*path);
+  if (!f) throw gs::ParseError("could not create " + *path);
+  f << text;
 }
 
-gradsched::AllReduceModel read_model(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) throw gradsched::ParseError("cannot open model file: " + path);
-  nlohmann::json doc;
+// The cost-model file written by `fit`: {"a_sec": a, "b_sec_per_byte": b, ...}.
+gs::AllReduceModel model_file(const std::string& path) {
+  std::ifstream f(path);
+  if (!f) throw gs::ParseError("model " + path + " is not readable");
   try {
-    in >> doc;
-  } catch (const nlohmann::json::exception& e) {
-    throw gradsched::ParseError("model file " + path + ": invalid JSON: " + e.what());
+    const Json doc = Json::parse(f);
+    return gs::AllReduceModel{doc.at("a_sec").get<double>(), doc.at("b_sec_per_byte").get<double>()};
+  } catch (const Json::exception& e) {
+    throw gs::ParseError("model " + path + " must be a JSON object with numbers a_sec and b_sec_per_byte (" +
+                         e.what() + ")");
   }
-  const auto num = [&](const char* k) {
-    return doc.is_object() && doc.contains(k) && doc[k].is_number();
+}
+
+gs::NetworkParams network(const Inputs& in) {
+  gs::NetworkParams net;
+  net.alpha = in.real("alpha").value_or(0.0);
+  net.beta = in.real("beta").value_or(0.0);
+  net.gamma = in.real("gamma").value_or(0.0);
+  return net;
+}
+
+gs::DbtStartup dbt(const Inputs& in) {
+  return in.on("dbt-literal") ? gs::DbtStartup::kLiteral : gs::DbtStartup::kAlphaCorrected;
+}
+
+// --workers: "lo..hi" = every power of two in [lo, hi]; else "n1,n2,...".
+std::vector<int> workers_list(const std::string& spec) {
+  std::vector<int> counts;
+  const auto bad = [&] { return gs::ValidationError("--workers \"" + spec + "\" is not lo..hi or a list of counts"); };
+  if (const auto dots = spec.find(".."); dots != std::string::npos) {
+    const long long lo = as_integer("workers", std::string_view(spec).substr(0, dots));
+    const long long hi = as_integer("workers", std::string_view(spec).substr(dots + 2));
+    for (int s = 0; s < 62 && (1ll << s) <= hi; ++s) {
+      if ((1ll << s) >= lo) counts.push_back(static_cast<int>(1ll << s));
+    }
+  } else {
+    std::istringstream items(spec);
+    for (std::string item; std::getline(items, item, ',');) {
+      if (item.empty()) continue;
+      try {
+        counts.push_back(static_cast<int>(as_integer("workers", item)));
+      } catch (const CommandLineError&) {
+        throw bad();
+      }
+    }
+  }
+  if (counts.empty()) throw bad();
+  return counts;
+}
+
+// ---- subcommands ------------------------------------------------------------
+
+int do_fit(const Inputs& in) {
+  Json doc;
+  std::vector<std::string> notes;
+  gs::AllReduceModel m;
+  const auto algo = in.text("algo");
+  if (!in.files.empty() == algo.has_value()) {
+    throw gs::ValidationError("fit takes exactly one source: a measurements CSV or --algo with network parameters");
+  }
+  if (algo) {  // Table 2 of the paper (comm_model.hpp:140-191)
+    gs::NetworkParams net = network(in);
+    net.n_workers = static_cast<int>(in.integer("workers").value_or(0));
+    m = gs::coefficients_for(gs::algorithm_from_string(*algo), net, dbt(in), &notes);
+    doc["source"] = "table2";
+  } else {     // measured sweep (comm_model.hpp:209-308)
+    m = gs::fit_model(gs::load_measurements_csv(in.files.front()));
+    doc["source"] = "fit";
+  }
+  doc["a_sec"] = m.a;
+  doc["b_sec_per_byte"] = m.b;
+  doc["warnings"] = notes;
+  emit(doc, in.text("out"));
+  return kExitOk;
+}
+
+int do_plan(const Inputs& in) {
+  const gs::ModelTrace trace = gs::load_trace(in.files[0]);
+  const gs::AllReduceModel m = model_file(in.files[1]);
+  const gs::MergePlan best = gs::optimal_plan(trace, m);
+  if (in.on("oracle")) {  // cross-check the DP against exhaustive search (small L only)
+    const double dp = gs::iteration_time(trace, best, m).iteration_time;
+    const double ex = gs::brute_force_plan(trace, m).iteration_time;
+    if (std::fabs(ex - dp) > 1e-9) {
+      std::cerr << "plan --oracle: the DP plan takes " << dp * 1e6 << " us, exhaustive search finds "
+                << ex * 1e6 << " us\n";
+      return kExitPlanner;
+    }
+  }
+  emit(gs::plan_to_json(trace, best, m), in.text("out"));
+  return kExitOk;
+}
+
+int do_simulate(const Inputs& in) {
+  const gs::ModelTrace trace = gs::load_trace(in.files[0]);
+  const gs::AllReduceModel m = model_file(in.files[1]);
+  const std::size_t L = trace.n_layers();
+  using Maker = std::function<gs::Timeline()>;
+  const std::map<gs::Strategy, Maker> timeline_of = {
+      {gs::Strategy::kNaive, [&] { return gs::naive_timeline(trace, m); }},
+      {gs::Strategy::kWfbp, [&] { return gs::iteration_time(trace, gs::MergePlan::all_normal(L), m); }},
+      {gs::Strategy::kSyncEasgd, [&] { return gs::iteration_time(trace, gs::MergePlan::all_merged(L), m); }},
+      {gs::Strategy::kMgWfbp, [&] { return gs::iteration_time(trace, gs::optimal_plan(trace, m), m); }},
   };
-  if (!num("a_sec") || !num("b_sec_per_byte")) {
-    throw gradsched::ParseError("model file " + path +
-                                ": expected numeric fields a_sec and b_sec_per_byte");
+  const gs::Timeline tl = timeline_of.at(gs::strategy_from_string(*in.text("strategy")))();
+  std::ostringstream line;
+  line << std::setprecision(15) << "iter_time_us=" << tl.iteration_time * 1e6
+       << " comm_nonoverlap_us=" << tl.comm_nonoverlap * 1e6;
+  if (const auto n = in.integer("workers"); n && *n > 0) {
+    line << " speedup="
+         << gs::speedup(static_cast<int>(*n), trace.forward_time, trace.total_backward_time(), tl.comm_nonoverlap);
   }
-  return {doc["a_sec"].get<double>(), doc["b_sec_per_byte"].get<double>()};
+  std::cout << line.str() << '\n';
+  if (const auto out = in.text("out")) emit(gs::timeline_to_json(tl), out);
+  return kExitOk;
 }
 
-// "lo..hi": powers of two in [lo, hi]; otherwise a comma list.
-std::vector<int> worker_counts(const std::string& spec) {
-  std::vector<int> out;
-  try {
-    const auto dots = spec.find("..");
-    if (dots != std::string::npos) {
-      const int lo = std::stoi(spec.substr(0, dots));
-      const int hi = std::stoi(spec.substr(dots + 2));
-      for (long long p = 1; p <= hi; p *= 2) {
-        if (p >= lo) out.push_back(static_cast<int>(p));
-      }
-    } else {
-      std::size_t start = 0;
-      while (start <= spec.size()) {
-        const auto comma = spec.find(',', start);
-        const std::string tok = spec.substr(start, comma == std::string::npos ? std::string::npos
-                                                                               : comma - start);
-        if (!tok.empty()) out.push_back(std::stoi(tok));
-        if (comma == std::string::npos) break;
-        start = comma + 1;
-      }
-    }
-  } catch (const std::exception&) {
-    throw gradsched::ValidationError("invalid --workers spec: '" + spec + "'");
-  }
-  if (out.empty()) throw gradsched::ValidationError("--workers spec '" + spec + "' yields no worker counts");
-  return out;
-}
-
-int cmd_fit(int argc, char** argv) {
-  const Args a = parse(argc, argv, 2, {"algo", "workers", "alpha", "beta", "gamma", "out"},
-                       {"dbt-literal"}, 1);
-  const bool have_csv = !a.pos.empty();
-  if (have_csv && a.has("algo")) {
-    throw gradsched::ValidationError("fit: give either a measurements CSV or --algo, not both");
-  }
-  gradsched::AllReduceModel model;
-  std::vector<std::string> warnings;
-  std::string source;
-  if (have_csv) {
-    model = gradsched::fit_model(gradsched::load_measurements_csv(a.pos[0]));
-    source = "fit";
-  } else if (a.has("algo")) {
-    gradsched::NetworkParams net;
-    net.alpha = a.has("alpha") ? to_double("alpha", a.str("alpha")) : 0.0;
-    net.beta = a.has("beta") ? to_double("beta", a.str("beta")) : 0.0;
-    net.gamma = a.has("gamma") ? to_double("gamma", a.str("gamma")) : 0.0;
-    net.n_workers = a.has("workers") ? to_int("workers", a.str("workers")) : 0;
-    model = gradsched::coefficients_for(
-        gradsched::algorithm_from_string(a.str("algo")), net,
-        a.flags.count("dbt-literal") ? gradsched::DbtStartup::kLiteral
-                                     : gradsched::DbtStartup::kAlphaCorrected,
-        &warnings);
-    source = "table2";
-  } else {
-    throw gradsched::ValidationError("fit: need a measurements CSV or --algo with network parameters");
-  }
-  nlohmann::json doc;
-  doc["a_sec"] = model.a;
-  doc["b_sec_per_byte"] = model.b;
-  doc["source"] = source;
-  doc["warnings"] = warnings;
-  write_json(doc, a.str("out"));
-  return kOk;
-}
-
-int cmd_plan(int argc, char** argv) {
-  const Args a = parse(argc, argv, 2, {"out"}, {"oracle"}, 2);
-  if (a.pos.size() != 2) throw UsageError("plan: need trace.json and model.json");
-  const auto trace = gradsched::load_trace(a.pos[0]);
-  const auto model = read_model(a.pos[1]);
-  const auto plan = gradsched::optimal_plan(trace, model);
-  const double t = gradsched::iteration_time(trace, plan, model).iteration_time;
-  if (a.flags.count("oracle")) {
-    const auto brute = gradsched::brute_force_plan(trace, model);
-    if (std::abs(brute.iteration_time - t) > 1e-9) {
-      std::cerr << "plan: oracle mismatch: planner " << t * 1e6 << " us vs exhaustive minimum "
-                << brute.iteration_time * 1e6 << " us\n";
-      return kPlanner;
-    }
-  }
-  write_json(gradsched::plan_to_json(trace, plan, model), a.str("out"));
-  return kOk;
-}
-
-int cmd_simulate(int argc, char** argv) {
-  const Args a = parse(argc, argv, 2, {"strategy", "workers", "out"}, {}, 2);
-  if (a.pos.size() != 2) throw UsageError("simulate: need trace.json and model.json");
-  require_opts(a, {"strategy"});
-  const auto trace = gradsched::load_trace(a.pos[0]);
-  const auto model = read_model(a.pos[1]);
-  const auto strategy = gradsched::strategy_from_string(a.str("strategy"));
-  const std::size_t n = trace.n_layers();
-  gradsched::Timeline tl;
-  if (strategy == gradsched::Strategy::kNaive) {
-    tl = gradsched::naive_timeline(trace, model);
-  } else if (strategy == gradsched::Strategy::kWfbp) {
-    tl = gradsched::iteration_time(trace, gradsched::MergePlan::all_normal(n), model);
-  } else if (strategy == gradsched::Strategy::kSyncEasgd) {
-    tl = gradsched::iteration_time(trace, gradsched::MergePlan::all_merged(n), model);
-  } else {
-    tl = gradsched::iteration_time(trace, gradsched::optimal_plan(trace, model), model);
-  }
-  const int workers = a.has("workers") ? to_int("workers", a.str("workers")) : 0;
-  std::cout << std::setprecision(15) << "iter_time_us=" << tl.iteration_time * 1e6
-            << " comm_nonoverlap_us=" << tl.comm_nonoverlap * 1e6;
-  if (workers > 0) {
-    std::cout << " speedup="
-              << gradsched::speedup(workers, trace.forward_time, trace.total_backward_time(),
-                                    tl.comm_nonoverlap);
-  }
-  std::cout << '\n';
-  if (a.has("out")) write_json(gradsched::timeline_to_json(tl), a.str("out"));
-  return kOk;
-}
-
-int cmd_sweep(int argc, char** argv) {
-  const Args a = parse(argc, argv, 2, {"algo", "workers", "alpha", "beta", "gamma", "out", "json"},
-                       {"dbt-literal"}, 1);
-  if (a.pos.size() != 1) throw UsageError("sweep: need trace.json");
-  require_opts(a, {"algo", "alpha"});
-  const auto trace = gradsched::load_trace(a.pos[0]);
-  gradsched::NetworkParams net;
-  net.alpha = to_double("alpha", a.str("alpha"));
-  net.beta = a.has("beta") ? to_double("beta", a.str("beta")) : 0.0;
-  net.gamma = a.has("gamma") ? to_double("gamma", a.str("gamma")) : 0.0;
-  net.n_workers = 2;
-  const auto result = gradsched::run_sweep(
-      trace, net, gradsched::algorithm_from_string(a.str("algo")),
-      worker_counts(a.str("workers", "4..2048")),
-      a.flags.count("dbt-literal") ? gradsched::DbtStartup::kLiteral
-                                   : gradsched::DbtStartup::kAlphaCorrected);
-  bool any_ok = false;
-  for (const auto& row : result.rows) {
+int do_sweep(const Inputs& in) {
+  const gs::ModelTrace trace = gs::load_trace(in.files[0]);
+  gs::NetworkParams net = network(in);
+  net.n_workers = 2;  // replaced per row by run_sweep
+  const gs::SweepResult res = gs::run_sweep(trace, net, gs::algorithm_from_string(*in.text("algo")),
+                                            workers_list(in.text("workers").value_or("4..2048")), dbt(in));
+  std::size_t good = 0;
+  for (const auto& row : res.rows) {
     if (row.ok()) {
-      any_ok = true;
+      ++good;
     } else {
-      std::cerr << "sweep row failed: " << row.error << '\n';
+      std::cerr << "row n_workers=" << row.n_workers << " skipped: " << row.error << '\n';
     }
   }
-  for (const auto& w : result.warnings) std::cerr << "warning: " << w << '\n';
-  if (!any_ok) {
-    std::cerr << "sweep: every row failed\n";
-    return kAllRowsFailed;
+  for (const auto& w : res.warnings) std::cerr << "warning: " << w << '\n';
+  if (good == 0) {
+    std::cerr << "sweep: no worker count produced a result\n";
+    return kExitNoSweepRows;
   }
-  if (a.has("out")) {
-    std::ofstream out(a.str("out"));
-    if (!out) throw gradsched::ParseError("cannot open output file: " + a.str("out"));
-    gradsched::write_sweep_csv(result, out);
+  if (const auto out = in.text("out")) {
+    std::ofstream f(*out);
+    if (!f) throw gs::ParseError("could not create " + *out);
+    gs::write_sweep_csv(res, f);
   } else {
-    gradsched::write_sweep_csv(result, std::cout);
+    gs::write_sweep_csv(res, std::cout);
   }
-  if (a.has("json")) write_json(gradsched::sweep_to_json(result), a.str("json"));
-  return kOk;
+  if (const auto js = in.text("json")) emit(gs::sweep_to_json(res), js);
+  return kExitOk;
 }
 
-void usage(std::ostream& os) {
-  os << "gradsched: plan and simulate gradient merge schedules (mgwfbp-b200)\n"
-        "usage: gradsched {fit|plan|simulate|sweep} ...\n";
+const std::vector<CommandSpec>& commands() {
+  static const std::vector<CommandSpec> kCommands = {
+      {"fit", 0, 1,
+       {{"algo", Kind::kText, false}, {"workers", Kind::kInteger, false}, {"alpha", Kind::kReal, false},
+        {"beta", Kind::kReal, false}, {"gamma", Kind::kReal, false}, {"dbt-literal", Kind::kSwitch, false},
+        {"out", Kind::kText, false}},
+       do_fit},
+      {"plan", 2, 2, {{"oracle", Kind::kSwitch, false}, {"out", Kind::kText, false}}, do_plan},
+      {"simulate", 2, 2,
+       {{"strategy", Kind::kText, true}, {"workers", Kind::kInteger, false}, {"out", Kind::kText, false}},
+       do_simulate},
+      {"sweep", 1, 1,
+       {{"algo", Kind::kText, true}, {"alpha", Kind::kReal, true}, {"beta", Kind::kReal, false},
+        {"gamma", Kind::kReal, false}, {"workers", Kind::kText, false}, {"dbt-literal", Kind::kSwitch, false},
+        {"out", Kind::kText, false}, {"json", Kind::kText, false}},
+       do_sweep},
+  };
+  return kCommands;
+}
+
+void print_usage(std::ostream& os) {
+  os << "gradsched (mgwfbp-b200): gradient-merge planning and timeline simulation\n"
+        "commands:";
+  for (const auto& c : commands()) os << ' ' << c.name;
+  os << "\n";
+}
+
+// Exception -> exit status (proj/tools/main.cpp:31-35 semantics).
+int status_of_current_exception() {
+  try {
+    throw;
+  } catch (const gs::GuardError& e) {
+    std::cerr << "gradsched: " << e.what() << '\n';
+    return kExitGuard;
+  } catch (const gs::PlannerError& e) {
+    std::cerr << "gradsched: " << e.what() << '\n';
+    return kExitPlanner;
+  } catch (const std::exception& e) {
+    std::cerr << "gradsched: " << e.what() << '\n';
+    return kExitBadInput;
+  }
 }
 
 }  // namespace
 
 int main(int argc, char** argv) {
-  if (argc < 2) {
-    usage(std::cerr);
-    return kInput;
+  const std::string_view first = argc > 1 ? std::string_view(argv[1]) : std::string_view();
+  if (first == "-h" || first == "--help") {
+    print_usage(std::cout);
+    return kExitOk;
   }
-  const std::string sub = argv[1];
-  if (sub == "-h" || sub == "--help") {
-    usage(std::cout);
-    return kOk;
+  for (const auto& cmd : commands()) {
+    if (cmd.name != first) continue;
+    try {
+      return cmd.run(read_command_line(cmd, argc, argv));
+    } catch (...) {
+      return status_of_current_exception();
+    }
   }
-  try {
-    if (sub == "fit") return cmd_fit(argc, argv);
-    if (sub == "plan") return cmd_plan(argc, argv);
-    if (sub == "simulate") return cmd_simulate(argc, argv);
-    if (sub == "sweep") return cmd_sweep(argc, argv);
-    usage(std::cerr);
-    return kInput;
-  } catch (const UsageError& e) {
-    std::cerr << "error: " << e.what() << '\n';
-    return kInput;
-  } catch (const gradsched::GuardError& e) {
-    std::cerr << "error: " << e.what() << '\n';
-    return kGuard;
-  } catch (const gradsched::PlannerError& e) {
-    std::cerr << "error: " << e.what() << '\n';
-    return kPlanner;
-  } catch (const std::exception& e) {
-    std::cerr << "error: " << e.what() << '\n';
-    return kInput;
-  }
+  print_usage(std::cerr);
+  return kExitBadInput;
 }

@@ -125,7 +125,7 @@ __device__ __forceinline__ float4 ld4_stream<float>(const float* p) {
 template <>
 __device__ __forceinline__ float4 ld4_stream<bf16>(const bf16* p) {
   uint32_t a, b;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
+  asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
   return unpack_bf16x4(a, b);
 }
 
@@ -245,41 +245,83 @@ __device__ __forceinline__ void epilogue(const Tile& t, uint32_t e, float4 g, fl
   }
 }
 
+// Errors: a bounded wait (10 s of %globaltimer) expired — a peer or the
+// compute side never arrived. The error is recorded in the rank's state word
+// and in the communicator's host-mapped word (the host reads it without a
+// CUDA call); every later wait gives up at once, a CTA that gave up stops
+// publishing its barrier flags (so its peers time out too instead of
+// reducing partial data), and no SGD / write-back epilogue runs on data that
+// was never synchronised. A communicator that raised an error stays failed.
+__device__ __forceinline__ void raise_error(const RankView& v) {
+  atomicExch(v.state + kStateError, 1u);
+  if (v.host_err != nullptr) *reinterpret_cast<volatile uint32_t*>(v.host_err) = 1u;
+}
+
+__device__ __forceinline__ bool error_raised(const RankView& v) {
+  return ld_volatile_u32(v.state + kStateError) != 0;
+}
+
+// Spin until done() holds; false on timeout or when an error was raised
+// elsewhere (checked every 64 polls, off the fast path).
+template <typename Done>
+__device__ __forceinline__ bool spin_until(const RankView& v, Done done) {
+  if (done()) return true;
+  const uint64_t t0 = globaltimer_ns();
+  for (uint32_t n = 1;; ++n) {
+    if (done()) return true;
+    if ((n & 63) == 0) {
+      if (error_raised(v)) return false;
+      if (globaltimer_ns() - t0 > kTimeoutNs) {
+        raise_error(v);
+        return false;
+      }
+    }
+  }
+}
+
+// Everything a CTA needs to run groups: its barrier counter, the launch's LL
+// epoch, the abort state and, for the producer warp, the TMA ring.
+struct PushRing {
+  uint32_t head;
+  uint32_t phase;  // bit k: parity to wait for on stage k
+};
+
+struct CtaCtx {
+  uint32_t count;     // barrier count of this CTA index (identical on every rank)
+  uint32_t epoch;     // LL epoch of this launch: the rank's launch sequence + 1
+  bool abort;         // a wait of this CTA gave up: no more epilogues, no more flags
+  uint32_t* s_abort;  // CTA-shared abort word
+  PushRing ring;
+  uint8_t* stages;
+  float4* staging;  // data warps' cp.async slots (after the TMA ring)
+  uint64_t* bars;
+  bool producer;
+};
+
 // Barrier of CTA index `cta` with the same CTA index of every rank.
-// `count` is this CTA's barrier counter (same value in every thread).
 // bar.sync orders every warp's posted NVLink stores (and the producer warp's
 // completed, proxy-fenced bulk copies) before the flag writers'
 // st.release.sys; release is cumulative at system scope, so a peer that
 // acquires the flag sees the data (no per-thread fence.sys).
-__device__ __forceinline__ void cta_barrier(const RankView& v, int P, uint32_t cta, uint32_t& count) {
-  ++count;
+//
+// The flag slot is the PHYSICAL CTA index (blockIdx.x), whose counter cx.count
+// is: inside the engine a CTA runs groups under a rotated, group-local index,
+// and two CTAs with different counters must never share a slot.
+__device__ __forceinline__ void cta_barrier(const RankView& v, int P, CtaCtx& cx) {
+  const uint32_t cta = blockIdx.x;
+  ++cx.count;
   __syncthreads();
-  if (threadIdx.x < P) {
+  if (threadIdx.x < P && !cx.abort) {
     const int q = threadIdx.x;
-    st_release_sys(v.signal[q] + cta * kMaxRanks + v.rank, count);
+    const uint32_t want = cx.count;
+    st_release_sys(v.signal[q] + cta * kMaxRanks + v.rank, want);
     const uint32_t* mine = v.signal[v.rank] + cta * kMaxRanks + q;
-    if (static_cast<int32_t>(ld_acquire_sys(mine) - count) < 0) {
-      const uint64_t t0 = globaltimer_ns();
-      while (static_cast<int32_t>(ld_acquire_sys(mine) - count) < 0) {
-        if (globaltimer_ns() - t0 > kTimeoutNs) {
-          atomicExch(v.state + kStateError, 1u);
-          break;
-        }
-      }
+    if (!spin_until(v, [&] { return static_cast<int32_t>(ld_acquire_sys(mine) - want) >= 0; })) {
+      *cx.s_abort = 1u;
     }
   }
   __syncthreads();
-}
-
-__device__ __forceinline__ uint32_t load_cta_count(const RankView& v, uint32_t cta) {
-  __shared__ uint32_t s_count;
-  if (threadIdx.x == 0) s_count = ld_volatile_u32(v.state + kStateCtaBase + cta);
-  __syncthreads();
-  return s_count;
-}
-
-__device__ __forceinline__ void store_cta_count(const RankView& v, uint32_t cta, uint32_t count) {
-  if (threadIdx.x == 0) v.state[kStateCtaBase + cta] = count;
+  cx.abort = *reinterpret_cast<volatile uint32_t*>(cx.s_abort) != 0;
 }
 
 // ---- push data path -------------------------------------------------------
@@ -305,13 +347,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Producer state (meaningful in lane 0 of the producer warp only): the next
-// stage of the ring and the phase parity of each stage's mbarrier.
-struct PushRing {
-  uint32_t head;
-  uint32_t phase;  // bit k: parity to wait for on stage k
-};
-
 __device__ __forceinline__ void ring_init(uint64_t* bars) {
 #pragma unroll
   for (int k = 0; k < kStages; ++k) {
@@ -333,28 +368,17 @@ __device__ __forceinline__ void tma_store(void* dst, uint32_t stage_addr, uint32
                : "memory");
 }
 
-// Wait for stage `bar` to reach `parity`; a 10 s timeout raises the error
-// flag instead of hanging.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, uint32_t* err) {
-  uint32_t done = 0;
-  asm volatile(
-      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-      : "=r"(done)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  if (done) return;
-  const uint64_t t0 = globaltimer_ns();
-  while (!done) {
+// Wait for stage `bar` to reach `parity` (bounded like every wait).
+__device__ __forceinline__ bool mbar_wait(const RankView& v, uint32_t bar, uint32_t parity) {
+  return spin_until(v, [&] {
+    uint32_t done = 0;
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
-    if (!done && globaltimer_ns() - t0 > kTimeoutNs) {
-      atomicExch(err, 1u);
-      return;
-    }
-  }
+    return done != 0;
+  });
 }
 
 // Bulk copies of the tile's 16-byte body (a multiple of Elem<T>::kVec
@@ -379,7 +403,8 @@ struct PushItem {
 // Push the items of one chunk, enumerated by `item(i)`. Producer warp only.
 template <int P, typename T, typename Item>
 __device__ __forceinline__ void push_items(const RankView& v, uint32_t n_items, uint64_t my_slot,
-                                           PushRing& ring, uint8_t* stages, uint64_t* bars, Item item) {
+                                           PushRing& ring, uint8_t* stages, uint64_t* bars,
+                                           uint32_t* s_abort, Item item) {
   const uint32_t lane = threadIdx.x & 31;
   if (lane == 0) {
     // gradients were written by generic-proxy stores (backward / earlier
@@ -406,7 +431,7 @@ __device__ __forceinline__ void push_items(const RankView& v, uint32_t n_items, 
         it = item(iS++);
       } while (it.mask == 0 || !tma_able<T>(it.t));
       const uint32_t k = (ring.head + ns) % kStages;
-      mbar_wait(smem_u32(bars + k), (ring.phase >> k) & 1u, v.state + kStateError);
+      if (!mbar_wait(v, smem_u32(bars + k), (ring.phase >> k) & 1u)) *s_abort = 1u;
       ring.phase ^= 1u << k;
       const uint32_t bytes = tma_body<T>(it.t) * static_cast<uint32_t>(sizeof(T));
 #pragma unroll
@@ -639,28 +664,23 @@ __device__ __forceinline__ bool ll_pair(const uint64_t* p, uint32_t epoch, uint3
   return static_cast<uint32_t>(a >> 32) == epoch && static_cast<uint32_t>(b >> 32) == epoch;
 }
 
-// Spin until the vector's packets carry `epoch` (10 s timeout -> error flag).
+// Spin until the vector's packets carry `epoch` (bounded); false if the
+// wait gave up (the caller then skips this vector's epilogue).
 template <typename T>
-__device__ __forceinline__ float4 ll_recv(const uint64_t* src, uint32_t epoch, uint32_t* err) {
-  uint32_t w[4];
+__device__ __forceinline__ bool ll_recv(const RankView& v, const uint64_t* src, uint32_t epoch, float4& out) {
+  uint32_t w[4] = {0, 0, 0, 0};
   constexpr int kPairs = sizeof(T) == 4 ? 2 : 1;
+  bool ok = true;
 #pragma unroll
   for (int k = 0; k < kPairs; ++k) {
-    if (!ll_pair(src + 2 * k, epoch, w[2 * k], w[2 * k + 1])) {
-      const uint64_t t0 = globaltimer_ns();
-      while (!ll_pair(src + 2 * k, epoch, w[2 * k], w[2 * k + 1])) {
-        if (globaltimer_ns() - t0 > kTimeoutNs) {
-          atomicExch(err, 1u);
-          break;
-        }
-      }
-    }
+    ok = ok && spin_until(v, [&] { return ll_pair(src + 2 * k, epoch, w[2 * k], w[2 * k + 1]); });
   }
   if constexpr (sizeof(T) == 4) {
-    return make_float4(__uint_as_float(w[0]), __uint_as_float(w[1]), __uint_as_float(w[2]), __uint_as_float(w[3]));
+    out = make_float4(__uint_as_float(w[0]), __uint_as_float(w[1]), __uint_as_float(w[2]), __uint_as_float(w[3]));
   } else {
-    return unpack_bf16x4(w[0], w[1]);
+    out = unpack_bf16x4(w[0], w[1]);
   }
+  return ok;
 }
 
 // A small one-shot group over LL packets, all 16 warps. Work unit: one
@@ -668,13 +688,16 @@ __device__ __forceinline__ float4 ll_recv(const uint64_t* src, uint32_t epoch, u
 // group spreads over 8 CTAs — the group is latency-bound, not per-CTA
 // bandwidth-bound. Send the vector to every peer, then receive, rank-order
 // sum (own contribution in place), SGD. Tile t's packets start at
-// ll_pkt + (t.moff - mbase) * sizeof(T) / 4.
+// ll_pkt + (t.moff - mbase) * sizeof(T) / 4. The epoch is the launch's
+// (unique per launch of the communicator, identical on every rank), so a
+// packet left in a slot by an earlier launch — any plan, any CTA mapping —
+// never matches.
 constexpr uint32_t kLLParts = kTileElems / 4 / kBlock;  // parts per tile
 
 template <int P, typename T>
 __device__ __noinline__ void ll_group(const RankView& v, const Tile* tiles, uint32_t n_tiles, uint32_t ll_pkt,
-                                         uint32_t mbase, float scale, float lr, int epi, uint32_t cta,
-                                         uint32_t ncta, uint32_t epoch) {
+                                      uint32_t mbase, float scale, float lr, int epi, uint32_t cta,
+                                      uint32_t ncta, uint32_t epoch) {
   constexpr uint32_t kW = sizeof(T);  // packets per 4-element vector
   const int me = v.rank;
   for (uint32_t u = cta; u < n_tiles * kLLParts; u += ncta) {
@@ -696,26 +719,27 @@ __device__ __noinline__ void ll_group(const RankView& v, const Tile* tiles, uint
     }
     load_w_batch<1>(t, i, kBlock, w, epi, wv);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool ok = true;
 #pragma unroll
     for (int r = 0; r < P; ++r) {
-      const float4 xr = r == me ? x[0] : ll_recv<T>(ll_slot(v, me, r) + pkt, epoch, v.state + kStateError);
+      float4 xr = x[0];
+      if (r != me) ok = ll_recv<T>(v, ll_slot(v, me, r) + pkt, epoch, xr) && ok;
       acc = r == 0 ? mul4(xr, scale) : add4(acc, mul4(xr, scale));
     }
     x[0] = round4<T>(acc);
-    apply_batch<1, T>(t, i, kBlock, x, wv, w, g, lr, epi);
+    if (ok) apply_batch<1, T>(t, i, kBlock, x, wv, w, g, lr, epi);
   }
 }
 
-// Everything a CTA needs to run groups: its barrier counter and, for the
-// producer warp, the TMA ring.
-struct CtaCtx {
-  uint32_t count;
-  PushRing ring;
-  uint8_t* stages;
-  float4* staging;  // data warps' cp.async slots (after the TMA ring)
-  uint64_t* bars;
-  bool producer;
-};
+// Chunk of a CTA's pipelined loop: at most `cap` units, and small enough
+// that a CTA with `mine` units runs at least `min_chunks` chunks (so the
+// push of chunk c overlaps the reduction of chunk c-1 even for mid-size
+// groups where every CTA owns only a few units).
+__device__ __forceinline__ uint32_t chunk_units(uint32_t mine, uint32_t cap, uint32_t min_chunks) {
+  const uint32_t m = min_chunks > 0 ? min_chunks : 1;
+  const uint32_t c = (mine + m - 1) / m;
+  return c < 1 ? 1 : (c > cap ? cap : c);
+}
 
 // One-shot, pipelined over chunks of this CTA's tiles (cta + j*ncta):
 //   step t: producer pushes chunk t to every peer (TMA) | data warps reduce
@@ -725,30 +749,30 @@ template <int P, typename T>
 __device__ __forceinline__ void one_shot_group(const RankView& v, const Tile* tiles,
                                                uint32_t n_tiles, uint64_t slot_stride, float scale,
                                                float lr, int epi, uint32_t cta, uint32_t ncta,
-                                               uint32_t chunk, CtaCtx& cx) {
+                                               uint32_t chunk, uint32_t min_chunks, CtaCtx& cx) {
   const uint64_t my_slot = static_cast<uint64_t>(v.rank) * slot_stride;
   const uint32_t mine = cta < n_tiles ? (n_tiles - cta + ncta - 1) / ncta : 0;  // my tiles
-  const uint32_t C = chunk;
+  const uint32_t C = chunk_units(mine, chunk, min_chunks);
   const uint32_t n_chunks = (mine + C - 1) / C;
   const uint32_t peers = ((1u << P) - 1u) & ~(1u << v.rank);
 #pragma unroll 1
   for (uint32_t t = 0; t <= n_chunks && n_chunks > 0; ++t) {
     if (cx.producer) {
-      if (t < n_chunks) {
+      if (t < n_chunks && !cx.abort) {
         const uint32_t j0 = t * C;
         const uint32_t n = mine - j0 < C ? mine - j0 : C;
-        push_items<P, T>(v, n, my_slot, cx.ring, cx.stages, cx.bars, [&](uint32_t i) {
+        push_items<P, T>(v, n, my_slot, cx.ring, cx.stages, cx.bars, cx.s_abort, [&](uint32_t i) {
           return PushItem{tiles[cta + (j0 + i) * ncta], peers};
         });
         push_drain();
       }
-    } else if (t >= 1) {
+    } else if (t >= 1 && !cx.abort) {
 #pragma unroll 1
       for (uint32_t j = (t - 1) * C; j < mine && j < t * C; ++j) {
         reduce_tile_staged<P, T>(v, tiles[cta + j * ncta], slot_stride, false, my_slot, scale, lr, epi, cx.staging);
       }
     }
-    if (t < n_chunks) cta_barrier(v, P, cta, cx.count);
+    if (t < n_chunks) cta_barrier(v, P, cx);
   }
 }
 
@@ -763,30 +787,30 @@ template <int P, typename T>
 __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* tiles,
                                                uint32_t n_tiles, uint64_t slot_stride, float scale,
                                                float lr, int epi, uint32_t cta, uint32_t ncta,
-                                               uint32_t chunk, CtaCtx& cx) {
-  const uint32_t C = chunk > P ? chunk / P : 1;
+                                               uint32_t chunk, uint32_t min_chunks, CtaCtx& cx) {
   const uint64_t my_slot = static_cast<uint64_t>(v.rank) * slot_stride;
   const uint32_t n_super = (n_tiles + P - 1) / P;
   const uint32_t mine = cta < n_super ? (n_super - cta + ncta - 1) / ncta : 0;  // my super-tiles
+  const uint32_t C = chunk_units(mine, chunk > P ? chunk / P : 1, min_chunks);
   const uint32_t n_chunks = (mine + C - 1) / C;
   const int me = v.rank;
 #pragma unroll 1
   for (uint32_t t = 0; t <= n_chunks + 1 && n_chunks > 0; ++t) {
     if (cx.producer) {
-      if (t < n_chunks) {
+      if (t < n_chunks && !cx.abort) {
         const uint32_t j0 = t * C;
         const uint32_t ns = mine - j0 < C ? mine - j0 : C;
-        push_items<P, T>(v, ns * (P - 1), my_slot, cx.ring, cx.stages, cx.bars,
-                      [&](uint32_t i) {
-                        const uint32_t s = cta + (j0 + i / (P - 1)) * ncta;
-                        const int qi = static_cast<int>(i % (P - 1));
-                        const int q = qi < me ? qi : qi + 1;
-                        const uint32_t ti = s * P + q;
-                        return ti < n_tiles ? PushItem{tiles[ti], 1u << q} : PushItem{Tile{}, 0u};
-                      });
+        push_items<P, T>(v, ns * (P - 1), my_slot, cx.ring, cx.stages, cx.bars, cx.s_abort,
+                         [&](uint32_t i) {
+                           const uint32_t s = cta + (j0 + i / (P - 1)) * ncta;
+                           const int qi = static_cast<int>(i % (P - 1));
+                           const int q = qi < me ? qi : qi + 1;
+                           const uint32_t ti = s * P + q;
+                           return ti < n_tiles ? PushItem{tiles[ti], 1u << q} : PushItem{Tile{}, 0u};
+                         });
         push_drain();
       }
-    } else {
+    } else if (!cx.abort) {
       if (t >= 1 && t <= n_chunks) {  // RA(t-1)
 #pragma unroll 1
         for (uint32_t j = (t - 1) * C; j < mine && j < t * C; ++j) {
@@ -819,19 +843,31 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
         }
       }
     }
-    if (t <= n_chunks) cta_barrier(v, P, cta, cx.count);
+    if (t <= n_chunks) cta_barrier(v, P, cx);
   }
 }
 
+// Group-level parameters shared by both launch styles.
+struct GroupArgs {
+  const Tile* tiles;
+  uint32_t n_tiles;
+  uint64_t slot_stride;
+  float scale;
+  float lr;
+  int epi;
+  uint32_t chunk;
+  uint32_t min_chunks;
+  uint32_t ll_pkt;
+  uint32_t mbase;
+};
+
 // One merge group, executed by CTA `cta` of `ncta`.
 template <int P, typename T>
-__device__ __forceinline__ void run_group(bool two_shot, const RankView& v, const Tile* tiles,
-                                          uint32_t n_tiles, uint64_t slot_stride, float scale,
-                                          float lr, int epi, uint32_t cta, uint32_t ncta,
-                                          uint32_t chunk, uint32_t ll_pkt, uint32_t mbase, CtaCtx& cx) {
+__device__ __forceinline__ void run_group(bool two_shot, const RankView& v, const GroupArgs& a, uint32_t cta,
+                                          uint32_t ncta, CtaCtx& cx) {
   if constexpr (P > 1) {
-    if (ll_pkt != kNoLL) {
-      ll_group<P, T>(v, tiles, n_tiles, ll_pkt, mbase, scale, lr, epi, cta, ncta, cx.count);
+    if (a.ll_pkt != kNoLL) {
+      ll_group<P, T>(v, a.tiles, a.n_tiles, a.ll_pkt, a.mbase, a.scale, a.lr, a.epi, cta, ncta, cx.epoch);
       return;
     }
   }
@@ -839,8 +875,8 @@ __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, cons
     // Single rank: no exchange. grad x 1/P (= 1) straight into the epilogue;
     // all kB gradient and weight loads of a thread are in flight together.
     constexpr uint32_t kB = kTileElems / 4 / kBlock;
-    for (uint32_t ti = cta; ti < n_tiles; ti += ncta) {
-      const Tile t = tiles[ti];
+    for (uint32_t ti = cta; ti < a.n_tiles; ti += ncta) {
+      const Tile t = a.tiles[ti];
       const uint32_t layer = t.layer & kLayerMask;
       T* g = as<T>(v.grads[layer]);
       const T* src = g + t.src;
@@ -854,21 +890,27 @@ __device__ __forceinline__ void run_group(bool two_shot, const RankView& v, cons
         const uint32_t e = i * 4;
         if (i < nvec) x[k] = (aligned && e + 4 <= t.len) ? ld4_stream<T>(src + e) : ld4_tail<T>(src + e, t.len - e);
       }
-      load_w_batch<kB>(t, threadIdx.x, kBlock, w, epi, wv);
+      load_w_batch<kB>(t, threadIdx.x, kBlock, w, a.epi, wv);
 #pragma unroll
-      for (uint32_t k = 0; k < kB; ++k) x[k] = round4<T>(mul4(x[k], scale));
-      apply_batch<kB, T>(t, threadIdx.x, kBlock, x, wv, w, g, lr, epi);
+      for (uint32_t k = 0; k < kB; ++k) x[k] = round4<T>(mul4(x[k], a.scale));
+      apply_batch<kB, T>(t, threadIdx.x, kBlock, x, wv, w, g, a.lr, a.epi);
     }
   } else if (two_shot) {
-    two_shot_group<P, T>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, chunk, cx);
+    two_shot_group<P, T>(v, a.tiles, a.n_tiles, a.slot_stride, a.scale, a.lr, a.epi, cta, ncta, a.chunk,
+                         a.min_chunks, cx);
   } else {
-    one_shot_group<P, T>(v, tiles, n_tiles, slot_stride, scale, lr, epi, cta, ncta, chunk, cx);
+    one_shot_group<P, T>(v, a.tiles, a.n_tiles, a.slot_stride, a.scale, a.lr, a.epi, cta, ncta, a.chunk,
+                         a.min_chunks, cx);
   }
 }
 
-// Per-CTA set-up: barrier counter, TMA ring (P > 1).
+// Per-CTA set-up: barrier counter, launch epoch, TMA ring (P > 1), then the
+// entry barrier: every peer has left every older launch of the communicator
+// before this CTA index pushes into their arenas or LL slots.
 template <int P>
-__device__ __forceinline__ void cta_ctx_init(CtaCtx& cx, const RankView& v, uint8_t* dsmem, uint64_t* bars) {
+__device__ __forceinline__ void cta_ctx_init(CtaCtx& cx, const RankView& v, uint8_t* dsmem, uint64_t* bars,
+                                             uint32_t* s_abort) {
+  __shared__ uint32_t s_init[2];
   cx.producer = threadIdx.x >= kThreads;
   cx.stages = dsmem;
   cx.staging = reinterpret_cast<float4*>(dsmem + static_cast<size_t>(kStages) * kStageBytes);
@@ -876,13 +918,39 @@ __device__ __forceinline__ void cta_ctx_init(CtaCtx& cx, const RankView& v, uint
   cx.ring.head = 0;
   cx.ring.phase = 0;
   cx.count = 0;
+  cx.epoch = 0;
+  cx.abort = false;
+  cx.s_abort = s_abort;
+  if (threadIdx.x == 0) *s_abort = 0u;
   if constexpr (P > 1) {
     if (threadIdx.x == kThreads) ring_init(bars);
-    cx.count = load_cta_count(v, blockIdx.x);  // (its __syncthreads also publishes the ring init)
-    // entry: peers have left every older launch before any push
-    cta_barrier(v, P, blockIdx.x, cx.count);
+    if (threadIdx.x == 0) {
+      s_init[0] = ld_volatile_u32(v.state + kStateCtaBase + blockIdx.x);
+      s_init[1] = ld_volatile_u32(v.state + kStateSeq);
+    }
+    __syncthreads();  // (also publishes the ring init)
+    cx.count = s_init[0];
+    cx.epoch = s_init[1] + 1u;
+    cta_barrier(v, P, cx);
   } else {
     __syncthreads();
+  }
+}
+
+// Per-CTA exit: persist the barrier counter; the last CTA of this rank's
+// launch advances the launch sequence (the next launch's LL epoch). Every CTA
+// read the sequence at entry, before any CTA can get here.
+template <int P>
+__device__ __forceinline__ void cta_exit(const RankView& v, const CtaCtx& cx) {
+  if constexpr (P > 1) {
+    if (threadIdx.x == 0) {
+      v.state[kStateCtaBase + blockIdx.x] = cx.count;
+      __threadfence();
+      if (atomicAdd(v.state + kStateExit, 1u) == gridDim.x - 1) {
+        v.state[kStateExit] = 0u;
+        v.state[kStateSeq] = cx.epoch;
+      }
+    }
   }
 }
 
@@ -890,70 +958,75 @@ template <int P, bool TWO_SHOT, bool LOOPBACK, typename T>
 __global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid_constant__ GroupLaunch L) {
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ uint32_t s_abort;
   const RankView& v = L.views[LOOPBACK ? blockIdx.y : 0];
   CtaCtx cx;
-  cta_ctx_init<P>(cx, v, dsmem, bars);
-  run_group<P, T>(TWO_SHOT, v, L.tiles, L.n_tiles, L.slot_stride, L.scale, L.lr, L.epilogue,
-                  blockIdx.x, gridDim.x, L.chunk, L.ll_pkt, L.mbase, cx);
-  if constexpr (P > 1) store_cta_count(v, blockIdx.x, cx.count);
+  cta_ctx_init<P>(cx, v, dsmem, bars, &s_abort);
+  const GroupArgs a{L.tiles, L.n_tiles, L.slot_stride, L.scale, L.lr, L.epilogue,
+                    L.chunk, L.min_chunks, L.ll_pkt, L.mbase};
+  run_group<P, T>(TWO_SHOT, v, a, blockIdx.x, gridDim.x, cx);
+  cta_exit<P>(v, cx);
 }
 
+// The persistent comm engine. Grid (ncta, 1) for a real rank, (ncta, P) in
+// loopback (blockIdx.y = emulated rank). Groups run FIFO in backward order;
+// group k's units go to CTAs cta0_k, cta0_k + 1, ... (mod ncta), where cta0
+// rotates by the CTAs the previous groups used — so a run of small groups
+// spreads over the SMs and their latencies overlap instead of queueing on
+// CTA 0. The mapping is a pure function of the plan: CTA index b does the
+// same groups, tiles and barriers on every rank.
 template <int P, typename T>
 __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant__ EngineLaunch E) {
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t bars[kStages];
-  const RankView& v = E.v;
   __shared__ uint32_t s_iter;
+  __shared__ uint32_t s_abort;
+  const RankView& v = E.views[blockIdx.y];
   if (threadIdx.x == 0) s_iter = ld_volatile_u32(E.pipe + 1);
   // Entry barrier inside (runs while the compute stream replays the forward
   // pass): every peer has finished every older launch before any push.
   CtaCtx cx;
-  cta_ctx_init<P>(cx, v, dsmem, bars);
+  cta_ctx_init<P>(cx, v, dsmem, bars, &s_abort);
   const uint32_t iter = s_iter;
+  const uint32_t ncta = gridDim.x;
+  const uint32_t slot = blockIdx.y * gridDim.x + blockIdx.x;      // stamp column
+  const size_t row = static_cast<size_t>(gridDim.x) * gridDim.y;  // stamp row width
   for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
     const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
     const EngineGroup grp = E.groups[gi];
-    const bool two = P > 1 && grp.two_shot != 0;
-    const uint32_t units = two ? (grp.n_tiles + P - 1) / P
-                               : (grp.ll_pkt != kNoLL && P > 1 ? grp.n_tiles * kLLParts : grp.n_tiles);
-    if (blockIdx.x >= units) continue;  // same on every rank: no barrier to skip
+    const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;  // this CTA's index inside the group
+    if (j >= grp.units) continue;  // same on every rank: no barrier to skip
     if (threadIdx.x == 0) {
       // group gi is ready for iteration `iter` once its flag reached iter+1
       // (set by the replay, or by a mark kernel after the real backward of
       // the group's layers — groups may complete out of FIFO order)
-      const uint32_t target = iter + 1;
-      const uint32_t* flag = E.ready + gi;
-      if (static_cast<int32_t>(ld_acquire_gpu(flag) - target) < 0) {
-        const uint64_t t0 = globaltimer_ns();
-        while (static_cast<int32_t>(ld_acquire_gpu(flag) - target) < 0) {
-          if (globaltimer_ns() - t0 > kTimeoutNs) {  // compute side never signalled
-            atomicExch(E.pipe + 3, 1u);
-            break;
-          }
+      if (!E.no_wait && !cx.abort) {
+        const uint32_t target = iter + 1;
+        const uint32_t* flag = E.ready + gi;
+        if (!spin_until(v, [&] { return static_cast<int32_t>(ld_acquire_gpu(flag) - target) >= 0; })) {
+          atomicExch(E.pipe + 3, 1u);  // compute side never signalled
+          s_abort = 1u;
         }
       }
-      if (E.stamps != nullptr && blockIdx.x == 0) E.stamps[2 * gi] = globaltimer_ns();
+      if (E.stamps != nullptr) E.stamps[(gi * row + slot) * 2] = globaltimer_ns();
     }
     __syncthreads();
-    run_group<P, T>(two, v, E.tiles + grp.tile_first, grp.n_tiles, E.slot_stride, E.scale, E.lr,
-                    E.epilogue, blockIdx.x, gridDim.x, E.chunk, grp.ll_pkt, grp.mbase, cx);
+    cx.abort = *reinterpret_cast<volatile uint32_t*>(&s_abort) != 0;
+    if (!cx.abort) {
+      const GroupArgs a{E.tiles + grp.tile_first, grp.n_tiles, E.slot_stride, E.scale, E.lr, E.epilogue,
+                        E.chunk, E.min_chunks, grp.two_shot ? kNoLL : grp.ll_pkt, grp.mbase};
+      run_group<P, T>(P > 1 && grp.two_shot != 0, v, a, j, ncta, cx);
+    }
     if (E.stamps != nullptr) {
       __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        const uint32_t active = units < gridDim.x ? units : gridDim.x;
-        if (atomicAdd(E.group_done + gi, 1u) == active - 1) {
-          E.group_done[gi] = 0;
-          E.stamps[2 * gi + 1] = globaltimer_ns();
-        }
-      }
+      if (threadIdx.x == 0) E.stamps[(gi * row + slot) * 2 + 1] = globaltimer_ns();
     }
   }
-  if constexpr (P > 1) store_cta_count(v, blockIdx.x, cx.count);
+  cta_exit<P>(v, cx);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(E.pipe + 2, 1u) == gridDim.x - 1) {
+    if (atomicAdd(E.pipe + 2, 1u) == gridDim.x * gridDim.y - 1) {
       atomicExch(E.pipe + 2, 0u);
       __threadfence();
       atomicExch(E.pipe + 1, iter + 1);
@@ -1139,11 +1212,11 @@ cudaError_t launch_group_allreduce(const GroupLaunch& L, int ctas_per_rank, bool
                   : launch_lb<false, float>(L, grid, two_shot, stream);
 }
 
-cudaError_t launch_engine(const EngineLaunch& E, int ctas, cudaStream_t stream) {
+cudaError_t launch_engine(const EngineLaunch& E, int ctas, int ranks, cudaStream_t stream) {
   const void* fn = engine_fn(E.nranks, E.dtype);
   if (fn == nullptr) return cudaErrorInvalidValue;
   void* args[] = {const_cast<EngineLaunch*>(&E)};
-  return cudaLaunchKernel(fn, dim3(ctas), dim3(kBlock), args, smem_for(E.nranks), stream);
+  return cudaLaunchKernel(fn, dim3(ctas, ranks), dim3(kBlock), args, smem_for(E.nranks), stream);
 }
 
 cudaError_t engine_ctas_per_sm(int nranks, int dtype, int* out) {

@@ -14,8 +14,10 @@
 //                 barrier count CTA b of rank q last published (written by
 //                 q over NVLink with st.release.sys, spun on locally with
 //                 ld.acquire.sys).
-//   state         [2] barrier-timeout error flag, [64 + b] barrier count of
-//                 CTA index b (identical on every rank).
+//   state         [2] timeout error flag, [3] launch sequence number (the
+//                 LL epoch source: identical on every rank, +1 per collective
+//                 launch), [4] exit count of the running launch, [64 + b]
+//                 barrier count of CTA index b (identical on every rank).
 // Work unit: a Tile = up to kTileElems consecutive elements of ONE layer,
 // so pack/unpack read and write contiguous 16-byte vectors.
 #ifndef MGWFBP_DEVICE_CUH_
@@ -38,6 +40,8 @@ constexpr int kSignalWords = kMaxCtas * kMaxRanks;  // flag [cta][src rank]
 // state words: [kStateError] barrier-timeout flag, [kStateCtaBase + b] the
 // barrier count of CTA index b (persists across launches)
 constexpr int kStateError = 2;
+constexpr int kStateSeq = 3;
+constexpr int kStateExit = 4;
 constexpr int kStateCtaBase = 64;
 constexpr int kStateWords = kStateCtaBase + kMaxCtas;
 // LL (flag-in-data) area, right after the signal flags of every rank's
@@ -61,6 +65,7 @@ struct RankView {
   float* arena[kMaxRanks];       // every rank's merge arena (peer-mapped)
   uint32_t* signal[kMaxRanks];   // every rank's signal area (peer-mapped)
   uint32_t* state;               // this rank's counters
+  uint32_t* host_err;            // host-mapped error word of the communicator (may be NULL)
   float* const* grads;           // this rank's layer gradient pointers
   float* const* weights;         // this rank's layer weight pointers (may hold NULLs)
   int rank;
@@ -76,7 +81,8 @@ struct GroupLaunch {
   float lr;
   int epilogue;          // MGW_SGD | MGW_WRITE_GRAD
   uint64_t slot_stride;  // elements between the per-source-rank slots of an arena
-  uint32_t chunk;        // tiles per pipelined chunk of one CTA (two-shot: max(1, chunk/P) super-tiles)
+  uint32_t chunk;        // max tiles per pipelined chunk of one CTA (two-shot: max(1, chunk/P) super-tiles)
+  uint32_t min_chunks;   // a CTA with enough tiles splits them into at least this many chunks
   int dtype;             // MGW_DTYPE_* of the gradients / arena
   RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
 };
@@ -88,14 +94,17 @@ struct EngineGroup {
   uint32_t two_shot;
   uint32_t ll_pkt;       // kNoLL unless the group travels as LL packets (one-shot only)
   uint32_t mbase;        // merge-layout element offset of the group's first element
-  uint32_t pad[3];
+  uint32_t cta0;         // first CTA of the group: groups rotate over the CTAs in FIFO order,
+                         // so consecutive small groups run on different SMs concurrently
+  uint32_t units;        // work units (tiles / super-tiles / LL parts); min(units, ncta) CTAs take part
+  uint32_t pad;
 };
 
 // The persistent comm engine (paper Algorithm 2's communication daemon, on
 // the GPU): ONE kernel per iteration walks the groups in backward order,
 // each one the moment the compute side marks its head layer ready.
 struct EngineLaunch {
-  RankView v;
+  RankView views[kMaxRanks];     // [0] for a real rank; [r] per emulated rank (loopback, blockIdx.y)
   const Tile* tiles;
   const EngineGroup* groups;     // ascending group index
   uint32_t G;
@@ -106,11 +115,13 @@ struct EngineLaunch {
   int epilogue;
   uint64_t slot_stride;
   uint32_t chunk;                // as GroupLaunch::chunk
+  uint32_t min_chunks;           // as GroupLaunch::min_chunks
   int dtype;                     // MGW_DTYPE_* of the gradients / arena
   uint32_t* pipe;                // [1] iteration, [2] CTA exit count, [3] ready-timeout flag
   const uint32_t* ready;         // G flags: group g ready for iteration i when >= i + 1
-  uint32_t* group_done;          // G counters for end stamps (NULL: no timing)
-  unsigned long long* stamps;    // 2*G: (start, end) %globaltimer of each group (NULL: no timing)
+  uint32_t no_wait;              // 1: every group is ready (standalone drain: roofline / ncu runs)
+  unsigned long long* stamps;    // [G][ranks*ncta][2]: (start, end) %globaltimer of each group on each
+                                 // CTA (NULL: no timing); the group's span is min start .. max end
 };
 
 #ifdef __CUDACC__
@@ -157,10 +168,12 @@ __device__ __forceinline__ float4 ld_cg_v4(const float* p) {
   return v;
 }
 
-// Streaming gradient reads: read once per iteration, keep L1 clean.
+// Streaming gradient reads: read once per iteration, L2 only. Not .nc: in
+// a real backward the gradients are written by other kernels while the
+// persistent engine runs, so they are not read-only for the kernel's life.
 __device__ __forceinline__ float4 ld_stream_v4(const float* p) {
   float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "l"(p));
   return v;

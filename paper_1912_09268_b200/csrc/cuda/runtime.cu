@@ -15,6 +15,7 @@
 #include <cstring>
 #include <string>
 #include <cstdlib>
+#include <memory>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -36,7 +37,7 @@ cudaError_t launch_unpack_sgd(const Tile* tiles, uint32_t n_tiles, float* const*
                               int epi, int dtype, int ctas, cudaStream_t stream);
 cudaError_t launch_replay(unsigned long long* clock, unsigned long long deadline_ns, int first,
                           uint32_t* ready, cudaStream_t stream);
-cudaError_t launch_engine(const EngineLaunch& E, int ctas, cudaStream_t stream);
+cudaError_t launch_engine(const EngineLaunch& E, int ctas, int ranks, cudaStream_t stream);
 cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long long* deadlines_ns,
                               uint32_t n, const uint32_t* pipe, uint32_t* flags,
                               cudaStream_t stream);
@@ -81,10 +82,13 @@ struct mgw_comm {
   size_t arena_elems = 0;  // per copy
   uint64_t oneshot_max = 512 * 1024;
   int num_sms = 148;
-  uint32_t chunk_tiles = 16;  // pipelined chunk per CTA (MGW_CHUNK_TILES overrides, for probing)
-  uint64_t ll_max = 64 << 10; // one-shot groups up to this many bytes use LL packets
+  uint32_t chunk_tiles = 16;  // max tiles of a CTA's pipelined chunk (mgw_comm_set_chunk_tiles)
+  uint32_t min_chunks = 4;    // a CTA splits its tiles into at least this many chunks (mgw_comm_set_min_chunks)
+  uint64_t ll_max = 64 << 10; // one-shot groups up to this many bytes use LL packets (mgw_comm_set_ll_max)
   int max_ctas = 0;           // cap on the CTAs of a standalone group launch (0: one per SM)
-  uint64_t small_tile_max = 0; // groups below this many bytes use kTileElems / 4 tiles (more CTAs)
+  uint64_t small_tile_max = 0; // groups below this many bytes use kTileElems / 4 tiles (mgw_comm_set_small_tile_max)
+  uint32_t* host_err = nullptr;   // host-mapped error word (kernels raise it on a timeout)
+  uint32_t* host_err_d = nullptr; // its device alias
   // own allocations (loopback: one per emulated rank)
   std::vector<float*> arenas;
   std::vector<uint32_t*> signals;
@@ -142,8 +146,9 @@ struct mgw_pipeline {
   bool engine = false;
   int engine_ctas = 0;
   uint32_t* d_pipe = nullptr;             // ready count, iteration, exit count
-  uint32_t* d_group_done = nullptr;       // G
-  unsigned long long* d_stamps = nullptr; // 2G
+  unsigned long long* d_stamps = nullptr; // [G][stamp_cols][2] per-CTA (start, end)
+  size_t stamp_cols = 0;                  // CTAs (all emulated ranks) per stamp row
+  int grid_y = 1;                         // emulated ranks of the engine grid (loopback)
   mgw::EngineGroup* d_groups = nullptr;   // G
   unsigned long long* d_deadlines = nullptr;  // G group-head ready times (ns), backward order
   uint32_t* d_ready = nullptr;            // G ready flags (iteration stamps)
@@ -176,6 +181,9 @@ void init_common(mgw_comm* c, int device, size_t arena_bytes) {
   c->device = device;
   c->arena_elems = (arena_bytes / sizeof(float) + 3) & ~size_t{3};
   ck(cudaSetDevice(device), "cudaSetDevice");
+  ck(cudaHostAlloc(&c->host_err, sizeof(uint32_t), cudaHostAllocMapped), "cudaHostAlloc(error word)");
+  *c->host_err = 0;
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->host_err_d), c->host_err, 0), "error word alias");
   ck(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(preload_kernels(), "preload kernels (lazy module loading would deadlock the engine)");
   ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
@@ -195,6 +203,7 @@ RankView make_view(const mgw_comm* c, int r, float* const* grads, float* const* 
     }
   }
   v.state = c->states[c->loopback ? r : 0];
+  v.host_err = c->host_err_d;
   v.grads = grads;
   v.weights = weights;
   v.rank = c->loopback ? r : c->rank;
@@ -219,9 +228,9 @@ size_t signal_words(int nranks) {
 // Measured on B200 (tools/probe_bw.py, engine, LL vs barrier one-shot): LL
 // wins up to 512 KiB at P = 2 (8.0 vs 10.7 us) and 128 KiB at P = 4 (8.5
 // vs 12.4 us); LL sends 2(P-1) x the bytes, so P = 8 gets 32 KiB.
+// Tuning knobs are C-ABI setters (mgw_comm_set_*), never environment
+// variables: every rank must hold the same values.
 uint64_t default_ll_max(int nranks) {
-  const char* e = std::getenv("MGW_LL_MAX");
-  if (e != nullptr) return std::strtoull(e, nullptr, 10);
   if (nranks <= 2) return 512ull << 10;
   if (nranks <= 4) return 128ull << 10;
   return 32ull << 10;
@@ -231,16 +240,7 @@ uint64_t default_ll_max(int nranks) {
 // spread over more CTAs. Measured on B200 (tools/probe_bw.py, engine): 1 MiB
 // P = 2 one-shot 11.0 -> 9.9 us, 2 MiB P = 4 two-shot 23.4 -> 21.2 us; from
 // 4 MiB on the 32 KiB tiles are as fast or faster (P = 2 8 MiB 24.2 vs 28.1).
-uint64_t default_small_tile_max() {
-  const char* e = std::getenv("MGW_SMALL_TILE_MAX");
-  return e != nullptr ? std::strtoull(e, nullptr, 10) : (3ull << 20);
-}
-
-uint32_t default_chunk_tiles() {
-  const char* e = std::getenv("MGW_CHUNK_TILES");
-  const long v = e != nullptr ? std::strtol(e, nullptr, 10) : 0;
-  return v > 0 ? static_cast<uint32_t>(v) : 16u;
-}
+constexpr uint64_t kDefaultSmallTileMax = 3ull << 20;
 
 bool use_two_shot(const mgw_comm* c, uint64_t bytes, int algo) {
   if (c->nranks == 1) return false;
@@ -282,6 +282,7 @@ void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStre
   L.epilogue = epilogue;
   L.slot_stride = p->slot_stride;
   L.chunk = c->chunk_tiles;
+  L.min_chunks = c->min_chunks;
   L.dtype = p->dtype;
   for (int r = 0; r < p->n_views; ++r) {
     L.views[r] = make_view(c, r, p->d_grads + static_cast<size_t>(r) * p->L,
@@ -299,8 +300,8 @@ void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStre
 void check_barrier_flags(const mgw_comm* c) {
   for (uint32_t* st : c->states) {
     uint32_t flag = 0;
-    ck(cudaMemcpy(&flag, st + 2, sizeof flag, cudaMemcpyDeviceToHost), "read barrier flag");
-    if (flag != 0) throw CudaFailure("cross-rank barrier timed out (a peer never arrived)");
+    ck(cudaMemcpy(&flag, st + kStateError, sizeof flag, cudaMemcpyDeviceToHost), "read barrier flag");
+    if (flag != 0) throw CudaFailure("cross-rank wait timed out (a peer never arrived); the communicator is failed");
   }
 }
 
@@ -319,7 +320,10 @@ mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* w
   require(grads != nullptr && counts != nullptr && tags != nullptr, "NULL plan arrays");
   require(tags[0] == 0, "the first layer cannot be merged (tags[0] must be 0)");
   set_device(c);
-  auto* p = new mgw_plan();
+  // held by a unique_ptr until every check and allocation succeeded: any
+  // throw below frees the plan and its device tables
+  std::unique_ptr<mgw_plan, void (*)(mgw_plan*)> owner(new mgw_plan(), destroy_plan);
+  mgw_plan* p = owner.get();
   p->comm = c;
   p->L = L;
   require(dtype == MGW_DTYPE_F32 || dtype == MGW_DTYPE_BF16, "dtype must be MGW_DTYPE_F32 or MGW_DTYPE_BF16");
@@ -338,10 +342,8 @@ mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* w
   }
   p->heads.push_back(L);
   if (p->offs[L] > p->slot_stride) {
-    const std::string msg = "plan needs " + std::to_string(p->offs[L] * p->esize) +
-                            " arena bytes; communicator has " + std::to_string(c->arena_elems * 4);
-    delete p;
-    throw gradsched::ValidationError(msg);
+    throw gradsched::ValidationError("plan needs " + std::to_string(p->offs[L] * p->esize) +
+                                     " arena bytes; communicator has " + std::to_string(c->arena_elems * 4));
   }
   require(p->offs[L] < (uint64_t{1} << 32), "model too large for 32-bit tile offsets");
   const size_t nv = static_cast<size_t>(p->n_views);
@@ -400,7 +402,7 @@ mgw_plan* build_plan(mgw_comm* c, size_t L, float* const* grads, float* const* w
   ck(cudaMemcpy(p->d_weights, p->h_weights.data(), nv * L * sizeof(float*),
                 cudaMemcpyHostToDevice),
      "upload weights table");
-  return p;
+  return owner.release();
 }
 
 // Optional per-step host I/O captured into the pipeline graph (e2e runs).
@@ -435,9 +437,8 @@ int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_co
     c->rank = rank;
     c->nranks = nranks;
     c->oneshot_max = mgw::default_oneshot_max(nranks);
-    c->chunk_tiles = mgw::default_chunk_tiles();
     c->ll_max = mgw::default_ll_max(nranks);
-    c->small_tile_max = mgw::default_small_tile_max();
+    c->small_tile_max = mgw::kDefaultSmallTileMax;
     mgw::init_common(c, device, arena_bytes);
     c->arenas.push_back(mgw::alloc_arena(c->arena_elems, nranks));
     c->signals.push_back(mgw::alloc_zero_u32(mgw::signal_words(nranks)));
@@ -458,9 +459,8 @@ int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_com
     auto* c = new mgw_comm();
     c->nranks = nranks;
     c->oneshot_max = mgw::default_oneshot_max(nranks);
-    c->chunk_tiles = mgw::default_chunk_tiles();
     c->ll_max = mgw::default_ll_max(nranks);
-    c->small_tile_max = mgw::default_small_tile_max();
+    c->small_tile_max = mgw::kDefaultSmallTileMax;
     c->loopback = true;
     mgw::init_common(c, device, arena_bytes);
     for (int r = 0; r < nranks; ++r) {
@@ -526,6 +526,52 @@ int mgw_comm_set_max_ctas(mgw_comm* c, int max_ctas) {
   MGW_CATCH
 }
 
+int mgw_comm_set_ll_max(mgw_comm* c, uint64_t bytes) {
+  MGW_TRY {
+    require(c != nullptr, "comm is NULL");
+    c->ll_max = bytes;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_set_small_tile_max(mgw_comm* c, uint64_t bytes) {
+  MGW_TRY {
+    require(c != nullptr, "comm is NULL");
+    c->small_tile_max = bytes;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_set_chunk_tiles(mgw_comm* c, uint32_t max_tiles, uint32_t min_chunks) {
+  MGW_TRY {
+    require(c != nullptr && max_tiles >= 1 && min_chunks >= 1, "chunk tiles and min chunks must be >= 1");
+    c->chunk_tiles = max_tiles;
+    c->min_chunks = min_chunks;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_get_tuning(const mgw_comm* c, uint64_t* oneshot_max, uint64_t* ll_max, uint64_t* small_tile_max,
+                        uint32_t* chunk_tiles, uint32_t* min_chunks) {
+  MGW_TRY {
+    require(c != nullptr, "comm is NULL");
+    if (oneshot_max) *oneshot_max = c->oneshot_max;
+    if (ll_max) *ll_max = c->ll_max;
+    if (small_tile_max) *small_tile_max = c->small_tile_max;
+    if (chunk_tiles) *chunk_tiles = c->chunk_tiles;
+    if (min_chunks) *min_chunks = c->min_chunks;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_error(const mgw_comm* c, int* failed) {
+  MGW_TRY {
+    require(c != nullptr && failed != nullptr, "NULL argument");
+    *failed = *reinterpret_cast<volatile const uint32_t*>(c->host_err) != 0 ? 1 : 0;
+  }
+  MGW_CATCH
+}
+
 int mgw_comm_get_oneshot_max(const mgw_comm* c, uint64_t* bytes) {
   MGW_TRY {
     require(c != nullptr && bytes != nullptr, "comm / out is NULL");
@@ -546,6 +592,7 @@ int mgw_comm_destroy(mgw_comm* c) {
     for (uint32_t* s : c->states) cudaFree(s);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->d_clock) cudaFree(c->d_clock);
+    if (c->host_err) cudaFreeHost(c->host_err);
     delete c;
   }
   MGW_CATCH
@@ -664,6 +711,7 @@ int mgw_allreduce(mgw_comm* c, float* buf, size_t n, int algo, void* stream) {
     L.epilogue = MGW_WRITE_GRAD;
     L.slot_stride = p->slot_stride;
     L.chunk = c->chunk_tiles;
+    L.min_chunks = c->min_chunks;
     L.dtype = MGW_DTYPE_F32;
     L.ll_pkt = mgw::kNoLL;
     L.mbase = 0;
@@ -776,6 +824,8 @@ namespace {
 
 // Persistent-engine resources of a pipeline: group table, ready flags,
 // counters, stamps, and the kernel arguments (fixed for the pipeline's life).
+// Loopback communicators run ONE engine grid (ctas, P) for all emulated
+// ranks; the replay's ready flags are shared by them.
 void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, float lr, bool timed) {
   mgw_comm* c = p->comm;
   const int G = p->G();
@@ -786,33 +836,55 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
   // scheduled next to engine CTAs when every SM holds one (the engine then
   // waits forever for a ready signal), so kFreeSms SMs are always left
   // without an engine CTA. A real backward needs SMs too (use few CTAs).
+  // Every CTA of the grid must be resident at once (cross-rank barriers pair
+  // CTA b with CTA b of every peer): at most one CTA per SM, fewer CTAs than
+  // SMs.
   constexpr int kFreeSms = 8;
-  const int cap = std::max(1, std::min({kMaxCtas, std::max(1, occ) * c->num_sms - 1,
-                                        c->num_sms - kFreeSms}));
+  pipe->grid_y = c->loopback ? c->nranks : 1;
+  const int cap = std::max(1, std::min({kMaxCtas, (std::max(1, occ) * c->num_sms - 1) / pipe->grid_y,
+                                        (c->num_sms - kFreeSms) / pipe->grid_y}));
   pipe->engine_ctas = std::min(cap, engine_ctas < 0 ? cap : engine_ctas);
   const size_t g1 = static_cast<size_t>(std::max(G, 1));
+  pipe->stamp_cols = static_cast<size_t>(pipe->engine_ctas) * pipe->grid_y;
   ck(cudaMalloc(&pipe->d_pipe, 4 * sizeof(uint32_t)), "cudaMalloc(pipe)");
   ck(cudaMemset(pipe->d_pipe, 0, 4 * sizeof(uint32_t)), "memset(pipe)");
   ck(cudaMalloc(&pipe->d_ready, g1 * sizeof(uint32_t)), "cudaMalloc(ready)");
   ck(cudaMemset(pipe->d_ready, 0, g1 * sizeof(uint32_t)), "memset(ready)");
-  ck(cudaMalloc(&pipe->d_group_done, g1 * sizeof(uint32_t)), "cudaMalloc");
-  ck(cudaMemset(pipe->d_group_done, 0, g1 * sizeof(uint32_t)), "memset");
-  ck(cudaMalloc(&pipe->d_stamps, 2 * g1 * sizeof(unsigned long long)), "cudaMalloc");
-  ck(cudaMemset(pipe->d_stamps, 0, 2 * g1 * sizeof(unsigned long long)), "memset");
+  if (timed) {
+    const size_t n = 2 * g1 * pipe->stamp_cols;
+    ck(cudaMalloc(&pipe->d_stamps, n * sizeof(unsigned long long)), "cudaMalloc(stamps)");
+    ck(cudaMemset(pipe->d_stamps, 0, n * sizeof(unsigned long long)), "memset(stamps)");
+  }
+  // Groups in FIFO (backward) order rotate over the CTAs: group k starts at
+  // the CTA after the last one group k-1 used (a pure function of the plan
+  // and the CTA count, so identical on every rank).
+  const uint32_t ncta = static_cast<uint32_t>(pipe->engine_ctas);
   std::vector<EngineGroup> groups(G);
-  for (int g = 0; g < G; ++g) {
-    groups[g].tile_first = p->tile_first[g];
-    groups[g].n_tiles = p->tile_first[g + 1] - p->tile_first[g];
-    groups[g].two_shot = use_two_shot(c, group_bytes(p, g), algo) ? 1u : 0u;
-    groups[g].ll_pkt = groups[g].two_shot ? kNoLL : p->ll_pkt[g];
-    groups[g].mbase = static_cast<uint32_t>(p->offs[p->heads[g]]);
+  uint64_t next = 0;
+  for (int g = G - 1; g >= 0; --g) {
+    EngineGroup& e = groups[g];
+    e.tile_first = p->tile_first[g];
+    e.n_tiles = p->tile_first[g + 1] - p->tile_first[g];
+    e.two_shot = use_two_shot(c, group_bytes(p, g), algo) ? 1u : 0u;
+    e.ll_pkt = e.two_shot ? kNoLL : p->ll_pkt[g];
+    e.mbase = static_cast<uint32_t>(p->offs[p->heads[g]]);
+    const uint32_t P = static_cast<uint32_t>(c->nranks);
+    e.units = (P > 1 && e.two_shot) ? (e.n_tiles + P - 1) / P
+                                    : (P > 1 && e.ll_pkt != kNoLL ? e.n_tiles * (kTileElems / 4 / kBlock) : e.n_tiles);
+    e.cta0 = static_cast<uint32_t>(next % ncta);
+    next += std::min<uint32_t>(e.units, ncta);
   }
   ck(cudaMalloc(&pipe->d_groups, g1 * sizeof(EngineGroup)), "cudaMalloc(groups)");
-  ck(cudaMemcpy(pipe->d_groups, groups.data(), G * sizeof(EngineGroup), cudaMemcpyHostToDevice),
-     "upload groups");
+  if (G > 0) {
+    ck(cudaMemcpy(pipe->d_groups, groups.data(), G * sizeof(EngineGroup), cudaMemcpyHostToDevice),
+       "upload groups");
+  }
   EngineLaunch& E = pipe->args;
   E = EngineLaunch{};
-  E.v = make_view(c, 0, p->d_grads, p->d_weights);
+  for (int r = 0; r < p->n_views; ++r) {
+    E.views[r] = make_view(c, r, p->d_grads + static_cast<size_t>(r) * p->L,
+                           p->d_weights + static_cast<size_t>(r) * p->L);
+  }
   E.tiles = p->d_tiles;
   E.groups = pipe->d_groups;
   E.G = static_cast<uint32_t>(G);
@@ -822,11 +894,39 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
   E.epilogue = MGW_SGD;
   E.slot_stride = p->slot_stride;
   E.chunk = c->chunk_tiles;
+  E.min_chunks = c->min_chunks;
   E.dtype = p->dtype;
   E.pipe = pipe->d_pipe;
   E.ready = pipe->d_ready;
-  E.group_done = timed ? pipe->d_group_done : nullptr;
+  E.no_wait = 0;
   E.stamps = timed ? pipe->d_stamps : nullptr;
+}
+
+// Reduce the per-CTA stamps of the last engine launch to (start, end) per
+// group: the earliest CTA start and the latest CTA end (0, 0 for groups no
+// CTA takes part in).
+void read_group_stamps(mgw_pipeline* pipe, std::vector<unsigned long long>& out) {
+  const int G = pipe->plan->G();
+  std::vector<unsigned long long> raw(2 * static_cast<size_t>(G) * pipe->stamp_cols);
+  if (!raw.empty()) {
+    ck(cudaMemcpy(raw.data(), pipe->d_stamps, raw.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost),
+       "read stamps");
+  }
+  out.assign(2 * static_cast<size_t>(G), 0ull);
+  for (int g = 0; g < G; ++g) {
+    unsigned long long lo = ~0ull, hi = 0;
+    for (size_t k = 0; k < pipe->stamp_cols; ++k) {
+      const unsigned long long a = raw[(g * pipe->stamp_cols + k) * 2];
+      const unsigned long long b = raw[(g * pipe->stamp_cols + k) * 2 + 1];
+      if (a == 0 || b == 0) continue;
+      lo = std::min(lo, a);
+      hi = std::max(hi, b);
+    }
+    if (hi > 0) {
+      out[2 * g] = lo;
+      out[2 * g + 1] = hi;
+    }
+  }
 }
 
 // Backward-replay pipeline as one CUDA graph per iteration. engine_ctas == 0:
@@ -836,8 +936,9 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
 mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float lr, int algo,
                              bool timed, size_t l2_flush_bytes, int engine_ctas, const StepIo& io) {
   {
-    require(!p->comm->loopback, "pipelines run on a real communicator");
     require(t_f >= 0.0, "t_f must be >= 0");
+    require(!p->comm->loopback || engine_ctas != 0,
+            "loopback pipelines run the persistent engine (engine_ctas != 0)");
     set_device(p->comm);
     const size_t L = p->L;
     // Ready time of every layer, reference timeline.hpp:99-108 / planner.hpp:67-70.
@@ -904,7 +1005,7 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
         ck(launch_l2_flush(pipe->flush_buf, pipe->flush_bytes, flush_ctas, pipe->comm), "l2 flush");
       }
       if (pipe->engine) {
-        ck(launch_engine(pipe->args, pipe->engine_ctas, pipe->comm), "engine launch");
+        ck(launch_engine(pipe->args, pipe->engine_ctas, pipe->grid_y, pipe->comm), "engine launch");
         // one replay kernel walks every group head's ready time
         ck(launch_replay_all(pipe->d_clock, pipe->d_deadlines, static_cast<uint32_t>(G), pipe->d_pipe,
                              pipe->d_ready, pipe->compute),
@@ -974,7 +1075,6 @@ int mgw_pipeline_destroy(mgw_pipeline* pipe) {
     cudaFree(pipe->d_clock);
     if (pipe->flush_buf) cudaFree(pipe->flush_buf);
     if (pipe->d_pipe) cudaFree(pipe->d_pipe);
-    if (pipe->d_group_done) cudaFree(pipe->d_group_done);
     if (pipe->d_stamps) cudaFree(pipe->d_stamps);
     if (pipe->d_groups) cudaFree(pipe->d_groups);
     if (pipe->d_deadlines) cudaFree(pipe->d_deadlines);
@@ -1041,10 +1141,8 @@ int mgw_pipeline_group_times(mgw_pipeline* pipe, float* group_ms) {
     ck(cudaStreamSynchronize(pipe->comm), "sync");
     if (pipe->engine) {
       const int G = pipe->plan->G();
-      std::vector<unsigned long long> st(2 * static_cast<size_t>(G));
-      ck(cudaMemcpy(st.data(), pipe->d_stamps, st.size() * sizeof(unsigned long long),
-                    cudaMemcpyDeviceToHost),
-         "read stamps");
+      std::vector<unsigned long long> st;
+      mgw::read_group_stamps(pipe, st);
       for (int g = 0; g < G; ++g) {
         // zero-tile groups are no-ops in the engine (no CTA active)
         group_ms[g] = st[2 * g + 1] > st[2 * g] ? static_cast<float>(st[2 * g + 1] - st[2 * g]) * 1e-6f
@@ -1147,7 +1245,6 @@ int mgw_engine_create(mgw_plan* p, float lr, int algo, int engine_ctas, int reco
                       mgw_pipeline** out) {
   MGW_TRY {
     require(p != nullptr && out != nullptr, "bad engine arguments");
-    require(!p->comm->loopback, "engines run on a real communicator");
     require(engine_ctas != 0, "engine_ctas must be non-zero (< 0: default)");
     mgw::set_device(p->comm);
     auto* pipe = new mgw_pipeline();
@@ -1175,7 +1272,7 @@ int mgw_engine_begin(mgw_pipeline* pipe, void* after_stream) {
     // NULL is the legacy default stream (torch's default), not "no stream"
     ck(cudaEventRecord(pipe->fork, static_cast<cudaStream_t>(after_stream)), "fork");
     ck(cudaStreamWaitEvent(pipe->comm, pipe->fork, 0), "fork wait");
-    ck(mgw::launch_engine(pipe->args, pipe->engine_ctas, pipe->comm), "engine launch");
+    ck(mgw::launch_engine(pipe->args, pipe->engine_ctas, pipe->grid_y, pipe->comm), "engine launch");
     mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   }
   MGW_CATCH
@@ -1229,6 +1326,38 @@ int mgw_engine_check(mgw_pipeline* pipe) {
   MGW_CATCH
 }
 
+int mgw_pipeline_drain(mgw_pipeline* pipe, int iters, float* ms_out) {
+  MGW_TRY {
+    require(pipe != nullptr && pipe->engine && iters >= 1 && ms_out != nullptr, "bad drain arguments");
+    mgw::set_device(pipe->plan->comm);
+    mgw_comm* c = pipe->plan->comm;
+    mgw::EngineLaunch E = pipe->args;
+    E.no_wait = 1;  // every group ready at launch: the engine streams the whole plan
+    std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(iters));
+    for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    try {
+      for (int i = 0; i < iters; ++i) {
+        if (pipe->flush_buf != nullptr) {
+          ck(mgw::launch_l2_flush(pipe->flush_buf, pipe->flush_bytes, c->num_sms, pipe->comm), "l2 flush");
+          mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+        }
+        ck(cudaEventRecord(ev[2 * i], pipe->comm), "record");
+        ck(mgw::launch_engine(E, pipe->engine_ctas, pipe->grid_y, pipe->comm), "engine launch");
+        mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+        ck(cudaEventRecord(ev[2 * i + 1], pipe->comm), "record");
+      }
+      ck(cudaEventSynchronize(ev.back()), "drain sync");
+      for (int i = 0; i < iters; ++i) ck(cudaEventElapsedTime(&ms_out[i], ev[2 * i], ev[2 * i + 1]), "elapsed");
+      mgw::check_barrier_flags(c);
+    } catch (...) {
+      for (auto e : ev) cudaEventDestroy(e);
+      throw;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  MGW_CATCH
+}
+
 int mgw_pipeline_stamps(mgw_pipeline* pipe, uint64_t* stamps_2g) {
   MGW_TRY {
     require(pipe != nullptr && stamps_2g != nullptr && pipe->engine && pipe->timed_groups,
@@ -1236,9 +1365,9 @@ int mgw_pipeline_stamps(mgw_pipeline* pipe, uint64_t* stamps_2g) {
     mgw::set_device(pipe->plan->comm);
     ck(cudaStreamSynchronize(pipe->compute), "sync");
     ck(cudaStreamSynchronize(pipe->comm), "sync");
-    ck(cudaMemcpy(stamps_2g, pipe->d_stamps, 2 * pipe->plan->G() * sizeof(uint64_t),
-                  cudaMemcpyDeviceToHost),
-       "read stamps");
+    std::vector<unsigned long long> st;
+    mgw::read_group_stamps(pipe, st);
+    std::copy(st.begin(), st.end(), stamps_2g);
   }
   MGW_CATCH
 }

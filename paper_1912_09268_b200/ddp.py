@@ -76,6 +76,7 @@ class MGWFBP:
         check(_lib.mgw_engine_create(self.dplan.handle, lr, ALGO[algo], engine_ctas,
                                      int(record_group_times), C.byref(h)))
         self.handle = h
+        self.dplan._adopt(self)
         self.lr, self.algo = lr, algo
         self.groups = self.plan.groups()
         self.tail = max(0, min(int(tail_groups), len(self.groups)))
@@ -85,6 +86,7 @@ class MGWFBP:
             for i in members:
                 self.group_of[i] = g
         self.remaining = [len(m) for m in self.groups]
+        self._next = len(self.groups) - 1
         self._iters = 0
         self._launched = False
         self._lazy_launch = False
@@ -102,12 +104,24 @@ class MGWFBP:
         check(_lib.mgw_group_allreduce(self.dplan.handle, g, self.lr, 1, ALGO[self.algo],
                                        self.comm_stream.cuda_stream))
 
+    def _advance(self, stream) -> None:
+        """launch mode: launch the complete groups in backward (FIFO) order.
+
+        A group is launched only after every group before it in backward
+        order: if parameter use differs between ranks (data-dependent unused
+        parameters), hooks fire in different orders, but every rank still
+        issues the same sequence of collective launches — the cross-rank
+        barriers pair launches by order, not by group id."""
+        while self._next >= self.tail and self.remaining[self._next] == 0:
+            self._launch(self._next, stream)
+            self._next -= 1
+
     def _hook(self, i: int):
         def hook(_p):
             g = self.group_of[i]
             self.remaining[g] -= 1
             if self.remaining[g] == 0 and g >= self.tail and self.mode == "launch":
-                self._launch(g, torch.cuda.current_stream())
+                self._advance(torch.cuda.current_stream())
             elif self.remaining[g] == 0 and g >= self.tail:
                 stream = torch.cuda.current_stream().cuda_stream
                 if self._lazy_launch and not self._launched:
@@ -136,6 +150,7 @@ class MGWFBP:
                 raise RuntimeError("a parameter's .grad was replaced; keep zero_grad(set_to_none=False)")
         self.flat_grad.zero_()
         self.remaining = [len(m) for m in self.groups]
+        self._next = len(self.groups) - 1
         self._launched = False
         # overlap from the 2nd iteration (or from the start with eager module
         # loading); the engine starts at the first finished group
@@ -146,8 +161,9 @@ class MGWFBP:
         stream = torch.cuda.current_stream().cuda_stream
         missing = [g for g, r in enumerate(self.remaining) if r != 0 and g >= self.tail]
         if self.mode == "launch":
-            for g in reversed(missing):  # parameters that got no gradient this iteration
+            for g in range(self._next, self.tail - 1, -1):  # the rest in order (incl. groups without gradients)
                 self._launch(g, torch.cuda.current_stream())
+            self._next = self.tail - 1
             done = self._events[-1]
             done.record(self.comm_stream)
             torch.cuda.current_stream().wait_event(done)
@@ -161,6 +177,11 @@ class MGWFBP:
         for g in reversed(range(self.tail)):  # backward order, full width
             check(_lib.mgw_group_allreduce(self.dplan.handle, g, self.lr, 1, ALGO[self.algo], stream))
         self._iters += 1
+        # a timed-out wait of an earlier iteration (host-mapped flag: no sync);
+        # its kernels skipped their SGD, so the weights are stale, not corrupt
+        if self.comm.failed():
+            raise RuntimeError("MG-WFBP: a cross-rank or ready wait timed out (a peer or a group never "
+                               "arrived); the communicator has failed")
 
     def check(self) -> None:
         check(_lib.mgw_engine_check(self.handle))
@@ -171,7 +192,7 @@ class MGWFBP:
         return list(out)[: len(self.groups)]
 
     def close(self) -> None:
-        for h in self._hooks:
+        for h in getattr(self, "_hooks", []):
             h.remove()
         self._hooks = []
         if self.handle:

@@ -7,6 +7,7 @@ the CUDA IPC handles once at start-up (paper Algorithm 2 line 8, Bcast).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from typing import List, Optional, Sequence, Tuple
 
 import torch
@@ -44,7 +45,26 @@ def dtype_of(t: torch.Tensor) -> int:
     raise TypeError(f"gradients must be float32 or bfloat16, got {t.dtype}")
 
 
-class Comm:
+class _Owner:
+    """Native handles form a tree — communicator > device plans > pipelines /
+    engines — and a child must be destroyed before its parent. close()
+    closes the live children first, so teardown order never depends on the
+    garbage collector (which finalises reference cycles in arbitrary order)."""
+
+    def _adopt(self, child) -> None:
+        if not hasattr(self, "_children"):
+            self._children = weakref.WeakSet()
+        self._children.add(child)
+
+    def _close_children(self) -> None:
+        kids = list(getattr(self, "_children", ()))
+        if kids:
+            self._children.clear()
+        for child in kids:
+            child.close()
+
+
+class Comm(_Owner):
     """One rank's communicator (or a single-GPU loopback of `nranks` ranks)."""
 
     def __init__(self, rank: int, nranks: int, device: int, arena_bytes: int,
@@ -79,9 +99,41 @@ class Comm:
     def set_oneshot_max(self, nbytes: int) -> None:
         check(_lib.mgw_comm_set_oneshot_max(self.handle, int(nbytes)))
 
+    def set_ll_max(self, nbytes: int) -> None:
+        """One-shot groups up to nbytes travel as LL packets (0: never)."""
+        check(_lib.mgw_comm_set_ll_max(self.handle, int(nbytes)))
+
+    def set_small_tile_max(self, nbytes: int) -> None:
+        """Groups below nbytes use 8 KiB tiles (more CTAs per group)."""
+        check(_lib.mgw_comm_set_small_tile_max(self.handle, int(nbytes)))
+
+    def set_chunk_tiles(self, max_tiles: int, min_chunks: int = 4) -> None:
+        """A CTA's tiles run in pipelined chunks of <= max_tiles tiles and at
+        least min_chunks chunks when it owns enough tiles."""
+        check(_lib.mgw_comm_set_chunk_tiles(self.handle, int(max_tiles), int(min_chunks)))
+
+    def failed(self) -> bool:
+        """True once a kernel of this communicator gave up a bounded wait
+        (host-mapped flag: no CUDA call, no sync)."""
+        v = C.c_int()
+        check(_lib.mgw_comm_error(self.handle, C.byref(v)))
+        return bool(v.value)
+
     def set_max_ctas(self, n: int) -> None:
         """Cap the CTAs of standalone fused launches (0: one per SM)."""
         check(_lib.mgw_comm_set_max_ctas(self.handle, int(n)))
+
+    def tuning(self) -> dict:
+        """The communicator's knob values."""
+        o, l, t = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        ct, mc = C.c_uint32(), C.c_uint32()
+        check(_lib.mgw_comm_get_tuning(self.handle, C.byref(o), C.byref(l), C.byref(t), C.byref(ct), C.byref(mc)))
+        return {"oneshot_max": o.value, "ll_max": l.value, "small_tile_max": t.value,
+                "chunk_tiles": ct.value, "min_chunks": mc.value}
+
+    @property
+    def ll_max_bytes(self) -> int:
+        return self.tuning()["ll_max"]
 
     @property
     def oneshot_max(self) -> int:
@@ -114,6 +166,7 @@ class Comm:
         return [CommMeasurement(out[i].size_bytes, out[i].time_sec) for i in range(len(sizes))]
 
     def close(self) -> None:
+        self._close_children()
         if self.handle:
             check(_lib.mgw_comm_destroy(self.handle))
             self.handle = None
@@ -125,7 +178,7 @@ class Comm:
             pass
 
 
-class DevicePlan:
+class DevicePlan(_Owner):
     """A merge plan bound to this rank's gradient / weight tensors.
 
     grads / weights: one CUDA tensor per layer in forward order (for a
@@ -135,6 +188,7 @@ class DevicePlan:
 
     def __init__(self, comm: Comm, grads, weights, plan: MergePlan):
         self.comm = comm
+        self.handle = None
         if comm.loopback:
             assert len(grads) == comm.nranks
             flat_g = [t for per in grads for t in per]
@@ -157,6 +211,7 @@ class DevicePlan:
         check(_lib.mgw_plan_create_ex(comm.handle, L, gp, wp, arr(C.c_uint64, counts),
                                       arr(C.c_uint8, (int(t) for t in plan.tags)), self.dtype, C.byref(h)))
         self.handle = h
+        comm._adopt(self)
         n = C.c_int()
         check(_lib.mgw_plan_num_groups(h, C.byref(n)))
         self.n_groups = n.value
@@ -179,6 +234,7 @@ class DevicePlan:
         check(_lib.mgw_group_allreduce(self.handle, g, lr, epilogue, ALGO[algo], _stream_ptr(stream)))
 
     def close(self) -> None:
+        self._close_children()
         if self.handle:
             check(_lib.mgw_plan_destroy(self.handle))
             self.handle = None
@@ -204,6 +260,7 @@ class Pipeline:
         h2d=(pinned_host_src, device_dst) / d2h=(pinned_host_dst, device_src):
         per-step host I/O captured into the iteration graph (end-to-end runs)."""
         self.dplan = dplan
+        self.handle = None
         self.engine_ctas = engine_ctas
         self._io = (h2d, d2h)  # keep the buffers alive
         tb = arr(C.c_double, (l.backward_time for l in trace.layers))
@@ -227,6 +284,7 @@ class Pipeline:
                 dd.data_ptr() if dd is not None else None, ds.data_ptr() if ds is not None else None, nb_out,
                 C.byref(h)))
         self.handle = h
+        dplan._adopt(self)
         s = C.c_void_p()
         check(_lib.mgw_pipeline_stream(h, C.byref(s)))
         self.stream = torch.cuda.ExternalStream(s.value, device=torch.device("cuda", dplan.comm.device))
@@ -237,6 +295,14 @@ class Pipeline:
     def run(self, iters: int) -> List[float]:
         out = (C.c_float * iters)()
         check(_lib.mgw_pipeline_run(self.handle, iters, out))
+        return list(out)
+
+    def drain(self, iters: int) -> List[float]:
+        """Standalone engine launches with every group ready (each after the
+        pipeline's L2 flush): per-launch device ms of the whole plan's merged
+        all-reduce + SGD — the kernel the roofline is quoted on."""
+        out = (C.c_float * iters)()
+        check(_lib.mgw_pipeline_drain(self.handle, iters, out))
         return list(out)
 
     def device_timeline(self) -> dict:
