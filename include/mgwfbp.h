@@ -311,7 +311,8 @@ int mgw_calibrate(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int war
                   int algo, mgw_meas* out);
 
 /* Calibration of the persistent comm engine: per size, `reps` iterations of
- * an engine running ONE group of that size, ready at once; the median group
+ * an engine running ONE group of that size, made ready 100 us into the
+ * iteration (the engine is already waiting, as in a pipeline); the median group
  * device duration (%globaltimer, first CTA start -> last CTA end) is the
  * sample (L2 evicted before every rep). This is the T(M) the planner sees in
  * engine pipelines. */

@@ -968,6 +968,37 @@ __global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid
   cta_exit<P>(v, cx);
 }
 
+// Off the critical path of a group: while thread 0 waits for the group's
+// ready flag, warp 1 warms what the first tile of this CTA needs — its
+// descriptor and the layer's pointer-table entries into L1 (read-only for
+// the kernel's life), the weight lines into L2 — so once the flag flips only
+// the gradient load (written by the backward, so read after the flag) is a
+// memory round trip.
+template <int P>
+__device__ __forceinline__ void warm_group(const RankView& v, const Tile* tiles, const EngineGroup& grp, uint32_t j,
+                                           float lr_nonzero) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t ti;
+  if (P > 1 && grp.two_shot) {
+    ti = j * P + static_cast<uint32_t>(v.rank);
+  } else if (P > 1 && grp.ll_pkt != kNoLL) {
+    ti = j / kLLParts;
+  } else {
+    ti = j;
+  }
+  if (ti >= grp.n_tiles) return;
+  const Tile t = tiles[grp.tile_first + ti];
+  const uint32_t layer = t.layer & kLayerMask;
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(v.grads + layer));
+  const float* w = v.weights[layer];
+  if (w == nullptr || lr_nonzero == 0.0f) return;
+  const char* wb = reinterpret_cast<const char*>(w + t.src);
+  const uint32_t bytes = t.len * 4u;
+  for (uint32_t off = lane * 128u; off < bytes; off += 32u * 128u) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(wb + off));
+  }
+}
+
 // The persistent comm engine. Grid (ncta, 1) for a real rank, (ncta, P) in
 // loopback (blockIdx.y = emulated rank). Groups run FIFO in backward order;
 // group k's units go to CTAs cta0_k, cta0_k + 1, ... (mod ncta), where cta0
@@ -996,6 +1027,7 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
     const EngineGroup grp = E.groups[gi];
     const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;  // this CTA's index inside the group
     if (j >= grp.units) continue;  // same on every rank: no barrier to skip
+    if (threadIdx.x >= 32 && threadIdx.x < 64) warm_group<P>(v, E.tiles, grp, j, E.lr);
     if (threadIdx.x == 0) {
       // group gi is ready for iteration `iter` once its flag reached iter+1
       // (set by the replay, or by a mark kernel after the real backward of

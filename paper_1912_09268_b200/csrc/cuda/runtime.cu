@@ -1173,8 +1173,8 @@ int mgw_calibrate_engine_ex(mgw_comm* c, const uint64_t* sizes, size_t n, int wa
     uint64_t max_bytes = 16;
     for (size_t i = 0; i < n; ++i) max_bytes = std::max(max_bytes, sizes[i]);
     const size_t max_elems = (max_bytes + esize - 1) / esize;  // gradient elements
-    // ONE group per iteration, ready at t = 0: the planner's cost T(M) is a
-    // group's time on an idle engine (back-to-back groups overlap at CTA
+    // ONE group per iteration: the planner's cost T(M) is a group's time on
+    // an idle engine (back-to-back groups overlap at CTA
     // granularity, which made per-group stamps of a multi-group iteration
     // unreliable at large sizes).
     constexpr int kGroups = 1;
@@ -1202,7 +1202,10 @@ int mgw_calibrate_engine_ex(mgw_comm* c, const uint64_t* sizes, size_t n, int wa
           // branch before the engine; the group's stamps start after it):
           // cold-HBM group times, as in a pipeline iteration — a warm L2 made
           // the P = 1 slope look faster than HBM
-          pipe = mgw::build_pipeline(p, tb.data(), 0.0, 0.0f, algo, true, size_t{256} << 20, engine_ctas);
+          // the group becomes ready 100 us into the iteration, after the L2
+          // flush: the engine is already waiting for it, as in a pipeline,
+          // so T(M) is the ready -> reduced latency the planner trades
+          pipe = mgw::build_pipeline(p, tb.data(), 100e-6, 0.0f, algo, true, size_t{256} << 20, engine_ctas);
           std::vector<float> ms;
           std::vector<float> gm(R);
           for (int k = 0; k < warmup + reps; ++k) {

@@ -1,14 +1,14 @@
 #!/bin/bash
-# Chunk-size sweep of the fused two-shot engine (tools/probe_bw.py) at P=2 and P=NG.
+# Two-shot / one-shot chunking sweep of the fused engine (tools/probe_bw.py) at
+# P = 2 and P = NG: KNOBS = "chunk_tiles,min_chunks,small_tile_max_KiB;..." set
+# through the C-ABI setters (mgw_comm_set_chunk_tiles / _set_small_tile_max).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 NG=$(nvidia-smi -L | wc -l)
-for P in 2 $NG; do
-  [[ $P == 2 && $NG == 2 ]] && [[ -n "${DONE2:-}" ]] && continue
+for P in $(echo 2 $NG | tr ' ' '\n' | sort -u); do
   DEVS=$(seq -s, 0 $((P-1)))
-  for C in ${CHUNKS:-2 4 8 16}; do
-    echo "== P=$P chunk=$C"
-    CUDA_VISIBLE_DEVICES=$DEVS MGW_CHUNK_TILES=$C SIZES_KB=${SIZES_KB:-16384,65536,92672,185364,262144} ALGOS=${ALGOS:-twoshot} CTAS=140 STANDALONE= \
-      timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $P --master-addr 127.0.0.1 --master-port 29512 tools/probe_bw.py 2>&1 | grep -A4 "^P=" | grep -v "^P="
-  done
-  DONE2=1
+  echo "== P=$P"
+  CUDA_VISIBLE_DEVICES=$DEVS KNOBS="${KNOBS:-16,1,3072;16,4,3072;16,4,65536;32,4,65536}" \
+    SIZES_KB=${SIZES_KB:-4096,16384,65536,262144} ALGOS=${ALGOS:-twoshot} CTAS=${CTAS:-140} STANDALONE= \
+    timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $P --master-addr 127.0.0.1 \
+    --master-port 29512 tools/probe_bw.py 2>&1 | grep -v "^W\|^\s*$" | tail -20
 done

@@ -1,5 +1,10 @@
 """Merged all-reduce bus bandwidth probe at P ranks (torchrun, tools only):
-fused engine kernel (one-shot / two-shot, CTA counts) vs NCCL, large sizes."""
+fused engine kernel (one-shot / two-shot, CTA counts) vs NCCL, large sizes.
+
+Tool-level env (the library itself reads no environment): SIZES_KB / SIZES_MB,
+ALGOS, CTAS, REPS, DTYPE, STANDALONE, and KNOBS = ";"-separated
+"chunk_tiles,min_chunks,small_tile_max_KiB[,ll_max_KiB]" configurations set
+through the C-ABI setters (default: the library defaults)."""
 import os
 import sys
 
@@ -17,14 +22,24 @@ sizes = ([int(s) << 10 for s in os.environ["SIZES_KB"].split(",")] if "SIZES_KB"
 comm = rt.Comm(rank, P, local, max(sizes) + (1 << 20))
 f = 2 * (P - 1) / P
 out = []
-for algo in os.environ.get("ALGOS", "oneshot,twoshot").split(","):
-    for ctas in [int(c) for c in os.environ.get("CTAS", "64,140").split(",")]:
-        m = comm.calibrate_engine(sizes, warmup=2, reps=int(os.environ.get("REPS", "10")), algo=algo, engine_ctas=ctas,
-                                  dtype=1 if os.environ.get("DTYPE") == "bf16" else 0)
-        t = torch.tensor([x.time_sec for x in m], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        out.append((f"engine {algo} ctas={ctas}", [f * s / tt / 1e9 for s, tt in zip(sizes, t.tolist())],
-                    [tt * 1e6 for tt in t.tolist()]))
+base = comm.tuning()
+knobs = [k for k in os.environ.get("KNOBS", "").split(";") if k] or [""]
+for knob in knobs:
+    tag = ""
+    if knob:
+        v = [int(x) for x in knob.split(",")]
+        comm.set_chunk_tiles(v[0], v[1])
+        comm.set_small_tile_max(v[2] << 10)
+        comm.set_ll_max((v[3] << 10) if len(v) > 3 else base["ll_max"])
+        tag = f" [ct={v[0]} mc={v[1]} stm={v[2]}K]"
+    for algo in os.environ.get("ALGOS", "oneshot,twoshot").split(","):
+        for ctas in [int(c) for c in os.environ.get("CTAS", "64,140").split(",")]:
+            m = comm.calibrate_engine(sizes, warmup=2, reps=int(os.environ.get("REPS", "10")), algo=algo,
+                                      engine_ctas=ctas, dtype=1 if os.environ.get("DTYPE") == "bf16" else 0)
+            t = torch.tensor([x.time_sec for x in m], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            out.append((f"engine {algo} ctas={ctas}{tag}", [f * s / tt / 1e9 for s, tt in zip(sizes, t.tolist())],
+                        [tt * 1e6 for tt in t.tolist()]))
 for algo in os.environ.get("STANDALONE", "twoshot").split(","):
     if not algo:
         continue
@@ -52,6 +67,6 @@ out.append(("nccl", [f * s / tt / 1e9 for s, tt in zip(sizes, nccl)], [tt * 1e6 
 if rank == 0:
     print(f"P={P} sizes(KiB)={[s >> 10 for s in sizes]}  bus GB/s (time us)")
     for name, bw, us in out:
-        print(f"  {name:28s}", "  ".join(f"{b:7.1f} ({u:8.1f})" for b, u in zip(bw, us)), flush=True)
+        print(f"  {name:44s}", "  ".join(f"{b:7.1f} ({u:8.1f})" for b, u in zip(bw, us)), flush=True)
 comm.close()
 dist.destroy_process_group()
