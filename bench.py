@@ -459,6 +459,13 @@ def main():
                for c in counts]
 
     comm = rt.Comm(rank, N, local, 4 * max(padded, 1 << 20))
+    # every rank must have mapped every peer's arena over NVLink (P = 8:
+    # 7 IPC peers) before anything runs
+    peers = comm.num_peers()
+    if peers != N:
+        raise RuntimeError(f"rank {rank}: {peers} of {N} ranks mapped (CUDA IPC over NVLink)")
+    if N > 1:
+        print(f"[bench] rank {rank}/{N}: {peers} ranks mapped over NVLink (CUDA IPC)", file=sys.stderr, flush=True)
     if args.oneshot_max > 0:
         comm.set_oneshot_max(args.oneshot_max)
 
@@ -679,7 +686,7 @@ def main():
             "exposed_comm_ms": ms_step - cfg["compute_ms"],
             "gpu": {"comm": ("persistent engine, %s CTAs" % ("1/SM" if args.engine_ctas < 0 else args.engine_ctas))
                             if args.engine_ctas else "one fused kernel launch per group",
-                    "algo": args.algo, "tuning": comm.tuning(),
+                    "algo": args.algo, "tuning": comm.tuning(), "ipc_ranks_mapped": peers,
                     "l2_flush": f"{args.l2_flush_mib} MiB streaming stores on the comm stream during the forward "
                                 "replay, every iteration"},
             "calibration": {"plan_model": {"a_us": model.a * 1e6, "b_ps_per_byte": model.b * 1e12, "how": model_how},

@@ -144,6 +144,9 @@ int mgw_comm_export_handle(mgw_comm* comm, void* handle_out);
  * every peer's arena and signals into this process (NVLink P2P). */
 int mgw_comm_open_peers(mgw_comm* comm, const void* all_handles);
 int mgw_comm_destroy(mgw_comm* comm);
+/* Ranks whose arena + signal area this communicator can address (itself
+ * included): nranks once mgw_comm_open_peers mapped every peer. */
+int mgw_comm_num_peers(const mgw_comm* comm, int* mapped);
 
 /* Single-GPU emulation of `nranks` ranks (all arenas on one device, every
  * collective launched as ONE kernel over all emulated ranks: a cooperative

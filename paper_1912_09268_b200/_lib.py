@@ -77,6 +77,7 @@ mgw_comm_handle_size = _proto("mgw_comm_handle_size", [], C.c_size_t)
 mgw_comm_export_handle = _proto("mgw_comm_export_handle", [vp, vp])
 mgw_comm_open_peers = _proto("mgw_comm_open_peers", [vp, vp])
 mgw_comm_destroy = _proto("mgw_comm_destroy", [vp])
+mgw_comm_num_peers = _proto("mgw_comm_num_peers", [vp, C.POINTER(C.c_int)])
 mgw_comm_set_oneshot_max = _proto("mgw_comm_set_oneshot_max", [vp, C.c_uint64])
 mgw_comm_get_oneshot_max = _proto("mgw_comm_get_oneshot_max", [vp, u64p])
 mgw_comm_set_max_ctas = _proto("mgw_comm_set_max_ctas", [vp, C.c_int])

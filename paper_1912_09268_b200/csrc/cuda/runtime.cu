@@ -510,6 +510,22 @@ int mgw_comm_open_peers(mgw_comm* c, const void* all_handles) {
   MGW_CATCH
 }
 
+int mgw_comm_num_peers(const mgw_comm* c, int* mapped) {
+  MGW_TRY {
+    require(c != nullptr && mapped != nullptr, "NULL argument");
+    int n = 0;
+    for (int q = 0; q < c->nranks; ++q) {
+      if (c->loopback) {
+        n += c->arenas.size() > static_cast<size_t>(q) ? 1 : 0;
+      } else {
+        n += (c->peer_arena[q] != nullptr && c->peer_signal[q] != nullptr) ? 1 : 0;
+      }
+    }
+    *mapped = n;
+  }
+  MGW_CATCH
+}
+
 int mgw_comm_set_oneshot_max(mgw_comm* c, uint64_t bytes) {
   MGW_TRY {
     require(c != nullptr, "comm is NULL");

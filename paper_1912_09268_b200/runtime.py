@@ -68,7 +68,10 @@ class Comm(_Owner):
     """One rank's communicator (or a single-GPU loopback of `nranks` ranks)."""
 
     def __init__(self, rank: int, nranks: int, device: int, arena_bytes: int,
-                 group=None, loopback: bool = False):
+                 group=None, loopback: bool = False, exchange=None):
+        """exchange: optional callable(bytes) -> list of every rank's bytes
+        (rank order) used to swap the CUDA IPC handles instead of
+        torch.distributed (e.g. a file rendezvous for profiler runs)."""
         self.rank, self.nranks, self.device = rank, nranks, device
         self.loopback = loopback
         h = C.c_void_p()
@@ -78,20 +81,23 @@ class Comm(_Owner):
             check(_lib.mgw_comm_create(rank, nranks, device, arena_bytes, C.byref(h)))
         self.handle = h
         if not loopback and nranks > 1:
-            self._exchange(group)
+            self._exchange(group, exchange)
 
     @classmethod
     def create_loopback(cls, nranks: int, device: int, arena_bytes: int) -> "Comm":
         return cls(0, nranks, device, arena_bytes, loopback=True)
 
-    def _exchange(self, group) -> None:
-        import torch.distributed as dist
-
+    def _exchange(self, group, exchange=None) -> None:
         size = _lib.mgw_comm_handle_size()
         blob = (C.c_uint8 * size)()
         check(_lib.mgw_comm_export_handle(self.handle, blob))
-        gathered: List[Optional[bytes]] = [None] * self.nranks
-        dist.all_gather_object(gathered, bytes(blob), group=group)
+        if exchange is not None:
+            gathered = list(exchange(bytes(blob)))
+        else:
+            import torch.distributed as dist
+
+            gathered: List[Optional[bytes]] = [None] * self.nranks
+            dist.all_gather_object(gathered, bytes(blob), group=group)
         allb = b"".join(gathered)
         buf = (C.c_uint8 * len(allb)).from_buffer_copy(allb)
         check(_lib.mgw_comm_open_peers(self.handle, buf))
@@ -111,6 +117,12 @@ class Comm(_Owner):
         """A CTA's tiles run in pipelined chunks of <= max_tiles tiles and at
         least min_chunks chunks when it owns enough tiles."""
         check(_lib.mgw_comm_set_chunk_tiles(self.handle, int(max_tiles), int(min_chunks)))
+
+    def num_peers(self) -> int:
+        """Ranks this communicator can address (itself included)."""
+        v = C.c_int()
+        check(_lib.mgw_comm_num_peers(self.handle, C.byref(v)))
+        return v.value
 
     def failed(self) -> bool:
         """True once a kernel of this communicator gave up a bounded wait

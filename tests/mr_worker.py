@@ -45,6 +45,7 @@ def main():
     D.agree_plan(plan.tags)
     tags = [int(t) for t in plan.tags]
     comm = rt.Comm(rank, P, local, max(4 * rt.padded_elems(COUNTS), 80 << 20))
+    assert comm.num_peers() == P, comm.num_peers()
     comm.set_oneshot_max(64 * 1024)
     failures = []
     for algo in ("oneshot", "twoshot", "auto"):

@@ -78,6 +78,7 @@ def test_engine_pipeline_ragged_bit_exact(P):
     g_np, w_np = _np(rng, counts, P), _np(rng, counts, P)
     g_dev, w_dev = _dev(g_np), _dev(w_np)
     comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
+    assert comm.num_peers() == P
     comm.set_oneshot_max(256 * 1024)
     comm.set_ll_max(16 * 1024)
     dp = rt.DevicePlan(comm, g_dev, w_dev, plan)

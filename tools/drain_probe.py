@@ -1,0 +1,61 @@
+"""The bench's roofline kernel standalone (tools only; ncu target): the
+persistent engine draining a whole trace's optimal plan with every group
+ready at launch (mgw_pipeline_drain), on one GPU — P = 1, or P emulated
+ranks in loopback (engine grid (ctas, P)). No replay kernel runs beside it,
+so ncu can serialise and replay the launch.
+
+usage: python tools/drain_probe.py --trace bert_large [--P 1] [--iters 3]
+  ncu --set full -k regex:engine_kernel --launch-count 1 python tools/drain_probe.py ...
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_1912_09268_b200 import gradsched as gs  # noqa: E402
+from paper_1912_09268_b200 import runtime as rt  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--trace", default="bert_large")
+    ap.add_argument("--P", type=int, default=1)
+    ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--flush-mib", type=int, default=256)
+    args = ap.parse_args()
+    tr = gs.load_trace(os.path.join(ROOT, "traces", f"{args.trace}.json"))
+    calib = os.path.join(ROOT, "profiles", "calib", f"calib_{args.trace}_P{args.P}.csv")
+    plan = gs.optimal_plan(tr, gs.fit_model(gs.load_measurements_csv(calib)))
+    counts = [l.params for l in tr.layers]
+    P = args.P
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1)
+    grads = [[torch.empty(c, device="cuda").uniform_(-1, 1, generator=gen) for c in counts] for _ in range(P)]
+    weights = [[torch.empty(c, device="cuda").uniform_(-1, 1, generator=gen) for c in counts] for _ in range(P)]
+    if P == 1:
+        comm = rt.Comm(0, 1, 0, 4 * rt.padded_elems(counts))
+        dp = rt.DevicePlan(comm, grads[0], weights[0], plan)
+    else:
+        comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
+        dp = rt.DevicePlan(comm, grads, weights, plan)
+    pipe = rt.Pipeline(dp, tr, 0.01, l2_flush_bytes=args.flush_mib << 20, engine_ctas=-1)
+    ms = pipe.drain(args.iters)
+    S = sum(dp.group_span(g)[2] for g in range(dp.n_groups))
+    hbm = 3 * S * P
+    print(json.dumps({"trace": args.trace, "P": P, "groups": dp.n_groups, "grad_bytes_per_rank": S,
+                      "launch_ms": ms, "median_ms": statistics.median(ms),
+                      "hbm_algorithmic_bytes_per_launch": hbm,
+                      "hbm_gbs": hbm / (statistics.median(ms) / 1e3) / 1e9, "tuning": comm.tuning()}), flush=True)
+    pipe.close()
+    dp.close()
+    comm.close()
+
+
+if __name__ == "__main__":
+    main()
