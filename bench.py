@@ -74,6 +74,9 @@ def parse_args():
                          "the comm-bound regime of the paper); 1.0 = the B200-measured trace")
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"],
                     help="gradient / merge-arena type (bf16: fp32 accumulation, fp32 master weights)")
+    ap.add_argument("--protocol", default="chunked", choices=["chunked", "stream"],
+                    help="fused all-reduce protocol at N > 1: chunked (per-chunk cross-rank barrier) or stream "
+                         "(per-tile delivery counts, producer/consumer decoupled)")
     ap.add_argument("--engine-ctas", type=int, default=-1,
                     help="-1: persistent comm engine, one CTA per SM; >0: that many CTAs; "
                          "0: one fused kernel launch per group")
@@ -468,6 +471,7 @@ def main():
         print(f"[bench] rank {rank}/{N}: {peers} ranks mapped over NVLink (CUDA IPC)", file=sys.stderr, flush=True)
     if args.oneshot_max > 0:
         comm.set_oneshot_max(args.oneshot_max)
+    comm.set_protocol(args.protocol)
 
     # ---- N1: on-box calibration of the fused engine kernel at this N
     sizes = calibration_sizes(total_bytes, 4 * padded)

@@ -211,12 +211,24 @@ int mgw_comm_get_oneshot_max(const mgw_comm* comm, uint64_t* bytes);
  *    packets; 0 disables LL.
  *  small_tile_max: groups below this many bytes are cut into 8 KiB tiles
  *    (more CTAs) instead of 32 KiB tiles.
- *  chunk_tiles / min_chunks: a CTA's tiles run in pipelined chunks of at
- *    most chunk_tiles tiles (two-shot: chunk_tiles / P super-tiles) and at
- *    least min_chunks chunks when it owns enough tiles. */
+ *  protocol: MGW_PROTO_STREAM — the producer warp streams tiles
+ *    and publishes per-tile delivery counts, the data warps consume them as
+ *    they arrive (no barrier after the launch's entry barrier);
+ *    MGW_PROTO_CHUNKED (default) — a CTA's tiles run in pipelined chunks with one
+ *    cross-rank barrier per chunk (chunk_tiles / min_chunks: at most
+ *    chunk_tiles tiles per chunk, two-shot chunk_tiles / P super-tiles, and
+ *    at least min_chunks chunks when the CTA owns enough tiles). */
+#define MGW_PROTO_STREAM 0
+#define MGW_PROTO_CHUNKED 1
 int mgw_comm_set_ll_max(mgw_comm* comm, uint64_t bytes);
 int mgw_comm_set_small_tile_max(mgw_comm* comm, uint64_t bytes);
 int mgw_comm_set_chunk_tiles(mgw_comm* comm, uint32_t max_tiles, uint32_t min_chunks);
+int mgw_comm_set_protocol(mgw_comm* comm, int protocol);
+/* Streamed protocol: a producer publishes its delivery count every
+ * credit_batch (1, 2, 4 or 8) bulk items; a two-shot owner publishes its
+ * reduced tiles every ag_batch owned super-tiles. */
+int mgw_comm_set_stream_batches(mgw_comm* comm, uint32_t credit_batch, uint32_t ag_batch);
+int mgw_comm_get_protocol(const mgw_comm* comm, int* protocol);
 /* Current knob values (any output may be NULL). */
 int mgw_comm_get_tuning(const mgw_comm* comm, uint64_t* oneshot_max, uint64_t* ll_max,
                         uint64_t* small_tile_max, uint32_t* chunk_tiles, uint32_t* min_chunks);
@@ -306,6 +318,34 @@ int mgw_engine_join(mgw_pipeline* engine, void* stream);
 int mgw_engine_set_tail(mgw_pipeline* engine, int n_tail);
 /* Synchronise the engine and report a barrier / ready timeout as an error. */
 int mgw_engine_check(mgw_pipeline* engine);
+
+/* Copy-engine mode for a real backward (P > 1): no SM is taken from the
+ * backward. Each finished group's gradients travel to every peer's merge
+ * arena as copy-engine (DMA) writes over NVLink the moment the group is
+ * marked ready; after the backward ONE full-width kernel reduces every tile
+ * in rank order from the local arena (own contribution in place), fused
+ * with SGD. The merge plan sets the number of copies (the a of the
+ * copy-engine cost model, mgw_calibrate_ce). Needs the gradients in one flat
+ * buffer laid out like the merge layout (layer l at element offs[l], see
+ * mgw_plan_group_span) and weights for every layer. Reduced values are
+ * bit-identical to mgw_group_allreduce's (same rank-order arithmetic).
+ *   begin(after_stream)   at the start of an iteration (the peers finished
+ *                         reducing the previous one before any copy lands)
+ *   mark_ready(g, stream) after group g's gradients were produced on stream
+ *   join(stream)          after the backward: the reduce + SGD, `stream`
+ *                         waits for it. */
+typedef struct mgw_ce mgw_ce;
+int mgw_ce_create(mgw_plan* plan, float lr, mgw_ce** out);
+int mgw_ce_begin(mgw_ce* ce, void* after_stream);
+int mgw_ce_mark_ready(mgw_ce* ce, int group, void* stream);
+int mgw_ce_join(mgw_ce* ce, void* stream);
+/* Synchronise and report a timed-out wait as an error. */
+int mgw_ce_check(mgw_ce* ce);
+int mgw_ce_destroy(mgw_ce* ce);
+/* Copy-engine calibration: per size, the median of `reps` timed device-to-
+ * peer copies (rank -> rank+1; P = 1: local). */
+int mgw_calibrate_ce(mgw_comm* comm, const uint64_t* sizes_bytes, size_t n, int warmup, int reps,
+                     mgw_meas* out);
 
 /* On-box calibration sweep (N1): for each size, warmup + reps timed runs
  * of the fused group kernel on a single-layer group of size/4 elements;

@@ -84,6 +84,9 @@ mgw_comm_set_max_ctas = _proto("mgw_comm_set_max_ctas", [vp, C.c_int])
 mgw_comm_set_ll_max = _proto("mgw_comm_set_ll_max", [vp, C.c_uint64])
 mgw_comm_set_small_tile_max = _proto("mgw_comm_set_small_tile_max", [vp, C.c_uint64])
 mgw_comm_set_chunk_tiles = _proto("mgw_comm_set_chunk_tiles", [vp, C.c_uint32, C.c_uint32])
+mgw_comm_set_protocol = _proto("mgw_comm_set_protocol", [vp, C.c_int])
+mgw_comm_set_stream_batches = _proto("mgw_comm_set_stream_batches", [vp, C.c_uint32, C.c_uint32])
+mgw_comm_get_protocol = _proto("mgw_comm_get_protocol", [vp, C.POINTER(C.c_int)])
 mgw_comm_error = _proto("mgw_comm_error", [vp, C.POINTER(C.c_int)])
 mgw_comm_get_tuning = _proto("mgw_comm_get_tuning", [vp, u64p, u64p, u64p, C.POINTER(C.c_uint32),
                                                       C.POINTER(C.c_uint32)])
@@ -134,6 +137,13 @@ mgw_engine_mark_ready = _proto("mgw_engine_mark_ready", [vp, C.c_int, vp])
 mgw_engine_join = _proto("mgw_engine_join", [vp, vp])
 mgw_engine_set_tail = _proto("mgw_engine_set_tail", [vp, C.c_int])
 mgw_engine_check = _proto("mgw_engine_check", [vp])
+mgw_ce_create = _proto("mgw_ce_create", [vp, C.c_float, C.POINTER(vp)])
+mgw_ce_begin = _proto("mgw_ce_begin", [vp, vp])
+mgw_ce_mark_ready = _proto("mgw_ce_mark_ready", [vp, C.c_int, vp])
+mgw_ce_join = _proto("mgw_ce_join", [vp, vp])
+mgw_ce_check = _proto("mgw_ce_check", [vp])
+mgw_ce_destroy = _proto("mgw_ce_destroy", [vp])
+mgw_calibrate_ce = _proto("mgw_calibrate_ce", [vp, u64p, C.c_size_t, C.c_int, C.c_int, C.POINTER(Meas)])
 mgw_kernel_launches = _proto("mgw_kernel_launches", [], C.c_uint64)
 
 # Every symbol the header declares (checked by tests/test_capi_symbols.py).

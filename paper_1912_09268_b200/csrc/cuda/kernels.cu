@@ -635,7 +635,7 @@ __device__ __forceinline__ void reduce_tile_staged(const RankView& v, const Tile
 // increasing across launches; LL groups of one launch use disjoint packets).
 
 __device__ __forceinline__ uint64_t* ll_slot(const RankView& v, int q, int src) {
-  return reinterpret_cast<uint64_t*>(v.signal[q] + kSignalWords) + static_cast<uint64_t>(src) * kLLSlotPackets;
+  return reinterpret_cast<uint64_t*>(v.signal[q] + kLLWord) + static_cast<uint64_t>(src) * kLLSlotPackets;
 }
 
 // The 4-element vector's raw gradient words: fp32 4 words, bf16 2.
@@ -692,17 +692,17 @@ __device__ __forceinline__ bool ll_recv(const RankView& v, const uint64_t* src, 
 // (unique per launch of the communicator, identical on every rank), so a
 // packet left in a slot by an earlier launch — any plan, any CTA mapping —
 // never matches.
-constexpr uint32_t kLLParts = kTileElems / 4 / kBlock;  // parts per tile
-
+// (kLLParts: mgw_device.cuh; the data threads [0, kThreads) take part.)
 template <int P, typename T>
 __device__ __noinline__ void ll_group(const RankView& v, const Tile* tiles, uint32_t n_tiles, uint32_t ll_pkt,
                                       uint32_t mbase, float scale, float lr, int epi, uint32_t cta,
                                       uint32_t ncta, uint32_t epoch) {
   constexpr uint32_t kW = sizeof(T);  // packets per 4-element vector
   const int me = v.rank;
+  if (threadIdx.x >= kThreads) return;
   for (uint32_t u = cta; u < n_tiles * kLLParts; u += ncta) {
     const Tile t = tiles[u / kLLParts];
-    const uint32_t i = (u % kLLParts) * kBlock + threadIdx.x;  // this thread's vector
+    const uint32_t i = (u % kLLParts) * kThreads + threadIdx.x;  // this thread's vector
     const uint32_t nvec = (t.len + 3) >> 2;
     if (i >= nvec) continue;
     const uint32_t layer = t.layer & kLayerMask;
@@ -717,7 +717,7 @@ __device__ __noinline__ void ll_group(const RankView& v, const Tile* tiles, uint
     for (int q = 0; q < P; ++q) {
       if (q != me) ll_send<T>(ll_slot(v, q, me) + pkt, x[0], epoch);
     }
-    load_w_batch<1>(t, i, kBlock, w, epi, wv);
+    load_w_batch<1>(t, i, kThreads, w, epi, wv);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     bool ok = true;
 #pragma unroll
@@ -727,7 +727,7 @@ __device__ __noinline__ void ll_group(const RankView& v, const Tile* tiles, uint
       acc = r == 0 ? mul4(xr, scale) : add4(acc, mul4(xr, scale));
     }
     x[0] = round4<T>(acc);
-    if (ok) apply_batch<1, T>(t, i, kBlock, x, wv, w, g, lr, epi);
+    if (ok) apply_batch<1, T>(t, i, kThreads, x, wv, w, g, lr, epi);
   }
 }
 
@@ -847,6 +847,370 @@ __device__ __forceinline__ void two_shot_group(const RankView& v, const Tile* ti
   }
 }
 
+// ---- streamed protocol: no per-chunk barrier --------------------------------
+// The producer warp and the data warps of a CTA run DECOUPLED over the CTA's
+// whole work list (every group of the launch in FIFO order). The producer
+// streams gradient tiles to their destinations with TMA bulk copies and, once
+// a tile's copies have completed (cp.async.bulk.wait_group, two tiles of
+// lag), raises the destination's rs[b][me] delivery count; the data warps
+// consume tiles in the same order as their counts arrive (two-shot owners
+// push the reduced tile to every peer with register stores and raise
+// ag[b][me]). Every tile of a launch lands in its own arena bytes, so no
+// one ever waits for a consumer: the only cross-rank waits are data
+// arrivals, the NVLink pipe never drains between chunks, and the producer
+// runs ahead into the next group while the data warps still reduce the
+// previous one. The launch's entry barrier (cta_ctx_init) keeps arena reuse
+// across launches safe.
+
+__device__ __forceinline__ uint64_t* rs_flag(const RankView& v, int at, uint32_t cta, int src) {
+  return reinterpret_cast<uint64_t*>(v.signal[at] + kStreamRsWord) + cta * kMaxRanks + src;
+}
+
+__device__ __forceinline__ uint64_t* ag_flag(const RankView& v, int at, uint32_t cta, int src) {
+  return reinterpret_cast<uint64_t*>(v.signal[at] + kStreamAgWord) + cta * kMaxRanks + src;
+}
+
+// Named barrier of the data warps only (the producer never joins it).
+__device__ __forceinline__ void data_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
+
+// Producer bookkeeping (lane 0 of the producer warp). Delivery counts are
+// published per BATCH of kCreditBatch bulk items, one batch behind: when a
+// batch closes, cp.async.bulk.wait_group kCreditBatch completes the batch
+// before it (the newest batch stays in flight), so a publication never
+// drains this CTA's NVLink pipe, and the system-scope release it needs is
+// paid once per batch.
+constexpr uint32_t kCreditBatch = 8;
+
+template <int P>
+struct Producer {
+  uint64_t cur;       // items per destination (byte q) of the open batch
+  uint64_t prev;      // items per destination of the closed batch still in flight
+  uint32_t n_cur;     // items in the open batch
+  uint32_t batch;     // items per batch (kCreditBatch unless tuned: 1, 2, 4, 8)
+  uint64_t epoch_hi;  // launch epoch << 32
+  uint32_t* done;     // shared [kMaxRanks]: counts published so far (this launch)
+};
+
+// Publish `counts` (byte q: newly completed items into rank q's arena):
+// async-proxy fence (the completed bulk copies before the generic release),
+// then a system-scope release of the new total per destination.
+template <int P>
+__device__ __forceinline__ void publish(const RankView& v, Producer<P>& pr, uint64_t counts) {
+  if (counts == 0) return;
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    const uint32_t c = static_cast<uint32_t>(counts >> (8 * q)) & 0xffu;
+    if (c != 0) {
+      pr.done[q] += c;
+      st_release_sys_u64(rs_flag(v, q, blockIdx.x, v.rank), pr.epoch_hi | pr.done[q]);
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t mask_counts(uint32_t mask) {
+  uint64_t c = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxRanks; ++q) c |= static_cast<uint64_t>((mask >> q) & 1u) << (8 * q);
+  return c;
+}
+
+// One bulk item (destinations `mask`) was committed; a batch closes every
+// pr.batch items (1, 2, 4 or 8: the wait_group operand is an immediate).
+template <int P>
+__device__ __forceinline__ void committed(const RankView& v, Producer<P>& pr, uint32_t mask) {
+  pr.cur += mask_counts(mask);
+  if (++pr.n_cur == pr.batch) {
+    switch (pr.batch) {
+      case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+      case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+      case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
+      default: asm volatile("cp.async.bulk.wait_group 8;" ::: "memory"); break;
+    }
+    publish<P>(v, pr, pr.prev);
+    pr.prev = pr.cur;
+    pr.cur = 0;
+    pr.n_cur = 0;
+  }
+}
+
+// Complete and publish everything committed (before the producer blocks on
+// a group that is not ready yet, before a register-path item, at the end).
+template <int P>
+__device__ __forceinline__ void flush(const RankView& v, Producer<P>& pr) {
+  if (pr.prev == 0 && pr.cur == 0) return;
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  publish<P>(v, pr, pr.prev + pr.cur);  // bytes <= 2 * kCreditBatch: no carries
+  pr.prev = 0;
+  pr.cur = 0;
+  pr.n_cur = 0;
+}
+
+// This CTA's push items of one group (unit j of ncta): one-shot, every tile
+// to every peer; two-shot, tile s*P+q of each super-tile s to its owner q.
+template <int P>
+__device__ __forceinline__ uint32_t stream_items(const Tile* tiles, uint32_t n_tiles, bool two_shot, uint32_t j,
+                                                 uint32_t ncta) {
+  if (!two_shot) return j < n_tiles ? (n_tiles - j + ncta - 1) / ncta : 0;
+  const uint32_t n_super = (n_tiles + P - 1) / P;
+  return (j < n_super ? (n_super - j + ncta - 1) / ncta : 0) * (P - 1);
+}
+
+template <int P>
+__device__ __forceinline__ PushItem stream_item(const Tile* tiles, uint32_t n_tiles, bool two_shot, uint32_t j,
+                                                uint32_t ncta, int me, uint32_t i) {
+  if (!two_shot) return PushItem{tiles[j + i * ncta], ((1u << P) - 1u) & ~(1u << me)};
+  const uint32_t s = j + (i / (P - 1)) * ncta;
+  const int qi = static_cast<int>(i % (P - 1));
+  const int q = qi < me ? qi : qi + 1;
+  const uint32_t ti = s * P + q;
+  return ti < n_tiles ? PushItem{tiles[ti], 1u << q} : PushItem{Tile{}, 0u};
+}
+
+// Producer warp: push one group's items in order. The whole warp runs the
+// loop (uniform control flow); lane 0 drives the TMA: loads run up to two
+// items ahead in the kStages ring (a stage is reused once the store that
+// read it has finished reading: wait_group.read 1), each item is stored to
+// every destination from its stage and committed as one bulk group; the
+// < 16-byte tail goes through lane 0's registers. Tiles TMA cannot take
+// (16-byte-unaligned layer views) go through the whole warp's registers,
+// after a flush so the published counts stay in item order.
+template <int P, typename T>
+__device__ __forceinline__ void produce_group(const RankView& v, const Tile* tiles, uint32_t n_tiles,
+                                              bool two_shot, uint32_t j, uint32_t ncta, uint64_t my_slot,
+                                              Producer<P>& pr, CtaCtx& cx) {
+  const uint32_t lane = threadIdx.x & 31;
+  const int me = v.rank;
+  const uint32_t n = stream_items<P>(tiles, n_tiles, two_shot, j, ncta);
+  const uint32_t s0 = smem_u32(cx.stages);
+  auto item = [&](uint32_t i) { return stream_item<P>(tiles, n_tiles, two_shot, j, ncta, me, i); };
+  uint32_t iL = 0, iS = 0, nl = 0, ns = 0;  // next item to load / store; TMA loads / stores issued
+  for (;;) {
+    // loads ahead, up to the first register-path item
+    while (iL < n && (nl < kStages || nl + 2 <= ns + kStages)) {
+      const PushItem it = item(iL);
+      if (it.mask == 0) {
+        ++iL;
+        continue;
+      }
+      if (!tma_able<T>(it.t)) break;
+      if (lane == 0) {
+        if (nl >= kStages) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        const uint32_t k = (cx.ring.head + nl) % kStages;
+        tma_load(s0 + k * kStageBytes, as<T>(v.grads[it.t.layer & kLayerMask]) + it.t.src,
+                 tma_body<T>(it.t) * static_cast<uint32_t>(sizeof(T)), smem_u32(cx.bars + k));
+      }
+      ++nl;
+      ++iL;
+    }
+    while (iS < n && item(iS).mask == 0) ++iS;
+    if (iS >= n) break;
+    const PushItem it = item(iS);
+    const T* src = as<T>(v.grads[it.t.layer & kLayerMask]) + it.t.src;
+    if (tma_able<T>(it.t)) {
+      if (lane == 0) {
+        const uint32_t k = (cx.ring.head + ns) % kStages;
+        if (!mbar_wait(v, smem_u32(cx.bars + k), (cx.ring.phase >> k) & 1u)) *cx.s_abort = 1u;
+        cx.ring.phase ^= 1u << k;
+        const uint32_t bytes = tma_body<T>(it.t) * static_cast<uint32_t>(sizeof(T));
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          if (it.mask & (1u << q)) tma_store(as<T>(v.arena[q]) + my_slot + it.t.moff, s0 + k * kStageBytes, bytes);
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        for (uint32_t e = tma_body<T>(it.t); e < it.t.len; e += 4) {  // tail (< one 16-byte vector)
+          const float4 x = ld4_tail<T>(src + e, it.t.len - e);
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            if (it.mask & (1u << q)) st4<T>(as<T>(v.arena[q]) + my_slot + it.t.moff + e, x);
+          }
+        }
+        committed<P>(v, pr, it.mask);
+      }
+      ++ns;
+    } else {  // register path; every earlier item is stored (loads stop here)
+      if (lane == 0) flush<P>(v, pr);
+      __syncwarp();
+      const uint32_t nvec = (it.t.len + 3) >> 2;
+      for (uint32_t jv = lane; jv < nvec; jv += 32) {
+        const uint32_t e = jv * 4;
+        const float4 x = ld4_tail<T>(src + e, it.t.len - e);
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          if (it.mask & (1u << q)) st4<T>(as<T>(v.arena[q]) + my_slot + it.t.moff + e, x);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) publish<P>(v, pr, mask_counts(it.mask));
+      if (iL == iS) ++iL;
+    }
+    ++iS;
+    __syncwarp();
+    // a wait of this CTA gave up: stop pushing and publishing
+    if (__shfl_sync(0xffffffffu, lane == 0 ? *reinterpret_cast<volatile uint32_t*>(cx.s_abort) : 0u, 0)) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      return;
+    }
+  }
+  cx.ring.head = (cx.ring.head + nl) % kStages;
+}
+
+// Consumer bookkeeping (data threads). Delivery counts observed by the
+// pollers (thread t < P watches peer t) are cached: a later tile whose count
+// was already seen needs no poll and no barrier (the acquire that saw it and
+// the data barrier after it already ordered the reads).
+
+struct Consumer {
+  uint32_t rs;        // tiles expected from every peer's producer so far (this launch)
+  uint32_t rs_avail;  // min over the peers of the counts observed (identical in every data thread)
+  uint32_t ag;        // thread t < P: reduced tiles expected from owner t so far
+  uint32_t ag_out;    // reduced tiles published as an owner
+  uint32_t round;     // poll rounds (parity selects the exchange buffer)
+  uint32_t ag_batch;  // two-shot: owned super-tiles per all-gather publication
+  uint64_t epoch_hi;
+  uint32_t* s_cnt;    // shared [2][kMaxRanks]: counts seen by the pollers, per round parity
+};
+
+template <int P>
+__device__ __forceinline__ void wait_flag(const RankView& v, const uint64_t* flag, uint64_t want, uint32_t* seen,
+                                          CtaCtx& cx) {
+  uint64_t val = 0;
+  if (!spin_until(v, [&] {
+        val = ld_acquire_sys_u64(flag);
+        return val >= want;
+      })) {
+    *cx.s_abort = 1u;
+  }
+  *seen = static_cast<uint32_t>(val);
+}
+
+// All data threads: the first `cs.rs` tiles of every peer's producer have
+// arrived (false: a wait gave up).
+template <int P>
+__device__ __forceinline__ bool arrived_rs(const RankView& v, Consumer& cs, CtaCtx& cx) {
+  if (cs.rs_avail >= cs.rs) return true;
+  const int t = static_cast<int>(threadIdx.x);
+  const int me = v.rank;
+  uint32_t* cnt = cs.s_cnt + (cs.round & 1u) * kMaxRanks;
+  if (t < P && t != me && !cx.abort) wait_flag<P>(v, rs_flag(v, me, blockIdx.x, t), cs.epoch_hi | cs.rs, cnt + t, cx);
+  data_bar();
+  cx.abort = *reinterpret_cast<volatile uint32_t*>(cx.s_abort) != 0;
+  uint32_t m = 0xffffffffu;
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    if (q != me) m = min(m, cnt[q]);
+  }
+  cs.rs_avail = m;
+  ++cs.round;
+  return !cx.abort;
+}
+
+// AP of owned super-tiles [s_lo, s_hi) (stride ncta): wait for the other
+// owners' reduced tiles, then SGD from the local slots.
+template <int P, typename T>
+__device__ __forceinline__ bool apply_batch_supers(const RankView& v, const Tile* tiles, uint32_t n_tiles,
+                                                   uint32_t s_lo, uint32_t n_s, uint32_t ncta, uint64_t slot_stride,
+                                                   float lr, int epi, Consumer& cs, CtaCtx& cx) {
+  const int me = v.rank;
+  const int t = static_cast<int>(threadIdx.x);
+  if (t < P && t != me) {
+    uint32_t add = 0;  // owner t's tiles in this batch (none: t publishes nothing for it)
+    for (uint32_t m = 0; m < n_s; ++m) add += (s_lo + m * ncta) * P + t < n_tiles ? 1u : 0u;
+    cs.ag += add;
+    uint32_t seen;
+    if (add != 0 && !cx.abort) wait_flag<P>(v, ag_flag(v, me, blockIdx.x, t), cs.epoch_hi | cs.ag, &seen, cx);
+  }
+  data_bar();
+  cx.abort = *reinterpret_cast<volatile uint32_t*>(cx.s_abort) != 0;
+  if (cx.abort) return false;
+#pragma unroll 1
+  for (uint32_t m = 0; m < n_s; ++m) {
+    const uint32_t s = s_lo + m * ncta;
+#pragma unroll 1
+    for (int q = 0; q < P; ++q) {
+      const uint32_t ti = s * P + q;
+      if (q == me || ti >= n_tiles) continue;
+      const Tile tl = tiles[ti];
+      const T* red = as<T>(v.arena[me]) + static_cast<uint64_t>(q) * slot_stride + tl.moff;
+      const uint32_t layer = tl.layer & kLayerMask;
+      const uint32_t nvec = (tl.len + 3) >> 2;
+      float4 x[kVecPerThread], wv[kVecPerThread];
+#pragma unroll
+      for (uint32_t k = 0; k < kVecPerThread; ++k) {
+        const uint32_t i = threadIdx.x + k * kThreads;
+        if (i < nvec) x[k] = ld4_cg<T>(red + i * 4);
+      }
+      load_w_batch<kVecPerThread>(tl, threadIdx.x, kThreads, v.weights[layer], epi, wv);
+      apply_batch<kVecPerThread, T>(tl, threadIdx.x, kThreads, x, wv, v.weights[layer], as<T>(v.grads[layer]),
+                                    lr, epi);
+    }
+  }
+  return true;
+}
+
+// Data warps: consume one group (unit j of ncta) as its tiles arrive.
+//   one-shot: per tile, every peer's delivery, then the rank-order reduce + SGD.
+//   two-shot: per batch of kAgBatch owned super-tiles, RA (reduce + SGD of
+//   the owned tile, result pushed to every peer), one ag publication, then
+//   AP of the previous batch (the other owners' results, SGD).
+template <int P, typename T>
+__device__ __forceinline__ void consume_group(const RankView& v, const Tile* tiles, uint32_t n_tiles,
+                                              bool two_shot, uint32_t ll_pkt, uint32_t mbase, uint64_t slot_stride,
+                                              float scale, float lr, int epi, uint32_t j, uint32_t ncta,
+                                              Consumer& cs, CtaCtx& cx) {
+  const int me = v.rank;
+  const int t = static_cast<int>(threadIdx.x);
+  const uint64_t my_slot = static_cast<uint64_t>(me) * slot_stride;
+  if (ll_pkt != kNoLL) {
+    ll_group<P, T>(v, tiles, n_tiles, ll_pkt, mbase, scale, lr, epi, j, ncta, cx.epoch);
+    return;
+  }
+  if (!two_shot) {
+#pragma unroll 1
+    for (uint32_t ti = j; ti < n_tiles; ti += ncta) {
+      ++cs.rs;
+      if (!arrived_rs<P>(v, cs, cx)) return;
+      reduce_tile_staged<P, T>(v, tiles[ti], slot_stride, false, my_slot, scale, lr, epi, cx.staging);
+    }
+    return;
+  }
+  const uint32_t n_super = (n_tiles + P - 1) / P;
+  const uint32_t mine = j < n_super ? (n_super - j + ncta - 1) / ncta : 0;
+  uint32_t prev_lo = 0, prev_n = 0;
+#pragma unroll 1
+  const uint32_t agb = cs.ag_batch;
+  for (uint32_t b0 = 0; b0 < mine; b0 += agb) {
+    const uint32_t nb = mine - b0 < agb ? mine - b0 : agb;
+    uint32_t owned = 0;
+#pragma unroll 1
+    for (uint32_t m = b0; m < b0 + nb; ++m) {
+      const uint32_t ti = (j + m * ncta) * P + me;
+      if (ti >= n_tiles) continue;
+      ++cs.rs;
+      if (!arrived_rs<P>(v, cs, cx)) return;
+      reduce_tile_staged<P, T>(v, tiles[ti], slot_stride, true, my_slot, scale, lr, epi, cx.staging);
+      ++owned;
+    }
+    // AP of the previous batch BEFORE publishing this one: its local HBM
+    // work overlaps the NVLink drain of this batch's result stores, which
+    // the release below has to wait for
+    if (prev_n != 0 && !apply_batch_supers<P, T>(v, tiles, n_tiles, j + prev_lo * ncta, prev_n, ncta, slot_stride,
+                                                 lr, epi, cs, cx)) {
+      return;
+    }
+    if (owned != 0) {
+      data_bar();  // every data warp's result stores precede the release
+      cs.ag_out += owned;
+      if (t < P && t != me) st_release_sys_u64(ag_flag(v, t, blockIdx.x, me), cs.epoch_hi | cs.ag_out);
+    }
+    prev_lo = b0;
+    prev_n = nb;
+  }
+  if (prev_n != 0) {
+    apply_batch_supers<P, T>(v, tiles, n_tiles, j + prev_lo * ncta, prev_n, ncta, slot_stride, lr, epi, cs, cx);
+  }
+}
+
 // Group-level parameters shared by both launch styles.
 struct GroupArgs {
   const Tile* tiles;
@@ -959,9 +1323,35 @@ __global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t bars[kStages];
   __shared__ uint32_t s_abort;
+  __shared__ uint32_t s_stream[3 * kMaxRanks];  // producer counts, consumer poll exchange [2][ranks]
   const RankView& v = L.views[LOOPBACK ? blockIdx.y : 0];
+  if (threadIdx.x < 3 * kMaxRanks) s_stream[threadIdx.x] = 0u;
   CtaCtx cx;
   cta_ctx_init<P>(cx, v, dsmem, bars, &s_abort);
+  if constexpr (P > 1) {
+    if (L.stream) {
+      const uint64_t epoch_hi = static_cast<uint64_t>(cx.epoch) << 32;
+      if (cx.producer) {
+        if (L.ll_pkt == kNoLL && !cx.abort) {
+          Producer<P> pr{};
+          pr.epoch_hi = epoch_hi;
+          pr.done = s_stream;
+          pr.batch = L.credit_batch;
+          if ((threadIdx.x & 31) == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+          produce_group<P, T>(v, L.tiles, L.n_tiles, TWO_SHOT, blockIdx.x, gridDim.x,
+                              static_cast<uint64_t>(v.rank) * L.slot_stride, pr, cx);
+          if ((threadIdx.x & 31) == 0 && *reinterpret_cast<volatile uint32_t*>(cx.s_abort) == 0) flush<P>(v, pr);
+        }
+      } else if (!cx.abort) {
+        Consumer cs{0, 0, 0, 0, 0, L.ag_batch, epoch_hi, s_stream + kMaxRanks};
+        consume_group<P, T>(v, L.tiles, L.n_tiles, TWO_SHOT, L.ll_pkt, L.mbase, L.slot_stride, L.scale, L.lr,
+                            L.epilogue, blockIdx.x, gridDim.x, cs, cx);
+      }
+      __syncthreads();
+      cta_exit<P>(v, cx);
+      return;
+    }
+  }
   const GroupArgs a{L.tiles, L.n_tiles, L.slot_stride, L.scale, L.lr, L.epilogue,
                     L.chunk, L.min_chunks, L.ll_pkt, L.mbase};
   run_group<P, T>(TWO_SHOT, v, a, blockIdx.x, gridDim.x, cx);
@@ -999,6 +1389,79 @@ __device__ __forceinline__ void warm_group(const RankView& v, const Tile* tiles,
   }
 }
 
+// The engine's streamed body (P > 1): the producer warp walks the groups
+// pushing tiles (waiting for each group's ready flag, after publishing what
+// it has in flight), the data warps walk the same groups consuming them.
+template <int P, typename T>
+__device__ __forceinline__ void engine_stream(const EngineLaunch& E, const RankView& v, CtaCtx& cx, uint32_t iter,
+                                              uint32_t slot, size_t row, uint32_t* s_stream) {
+  const uint32_t ncta = gridDim.x;
+  const uint64_t epoch_hi = static_cast<uint64_t>(cx.epoch) << 32;
+  const uint32_t target = iter + 1;
+  if (cx.producer) {
+    const uint32_t lane = threadIdx.x & 31;
+    Producer<P> pr{};
+    pr.epoch_hi = epoch_hi;
+    pr.done = s_stream;
+    pr.batch = E.credit_batch;
+    const uint64_t my_slot = static_cast<uint64_t>(v.rank) * E.slot_stride;
+    for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
+      const uint32_t gi = E.G - 1 - k;
+      const EngineGroup grp = E.groups[gi];
+      const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;
+      if (j >= grp.units || (!grp.two_shot && grp.ll_pkt != kNoLL)) continue;
+      uint32_t abort = 0;
+      if (lane == 0) {
+        abort = *reinterpret_cast<volatile uint32_t*>(cx.s_abort);
+        const uint32_t* flag = E.ready + gi;
+        if (!abort && !E.no_wait && static_cast<int32_t>(ld_acquire_gpu(flag) - target) < 0) {
+          flush<P>(v, pr);  // publish what is in flight before blocking
+          if (!spin_until(v, [&] { return static_cast<int32_t>(ld_acquire_gpu(flag) - target) >= 0; })) {
+            atomicExch(E.pipe + 3, 1u);
+            *cx.s_abort = 1u;
+            abort = 1;
+          }
+        }
+        // gradients written by generic-proxy stores: visible to the TMA
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      if (__shfl_sync(0xffffffffu, abort, 0)) break;
+      produce_group<P, T>(v, E.tiles + grp.tile_first, grp.n_tiles, grp.two_shot != 0, j, ncta, my_slot, pr, cx);
+    }
+    if (lane == 0 && *reinterpret_cast<volatile uint32_t*>(cx.s_abort) == 0) flush<P>(v, pr);
+    __syncwarp();
+    return;
+  }
+  Consumer cs{0, 0, 0, 0, 0, E.ag_batch, epoch_hi, s_stream + kMaxRanks};
+  for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
+    const uint32_t gi = E.G - 1 - k;
+    const EngineGroup grp = E.groups[gi];
+    const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;
+    if (j >= grp.units) continue;
+    if (threadIdx.x >= 32 && threadIdx.x < 64) warm_group<P>(v, E.tiles, grp, j, E.lr);
+    if (threadIdx.x == 0) {
+      if (!E.no_wait && !cx.abort) {
+        const uint32_t* flag = E.ready + gi;
+        if (!spin_until(v, [&] { return static_cast<int32_t>(ld_acquire_gpu(flag) - target) >= 0; })) {
+          atomicExch(E.pipe + 3, 1u);
+          *cx.s_abort = 1u;
+        }
+      }
+      if (E.stamps != nullptr) E.stamps[(gi * row + slot) * 2] = globaltimer_ns();
+    }
+    data_bar();
+    cx.abort = *reinterpret_cast<volatile uint32_t*>(cx.s_abort) != 0;
+    if (cx.abort) break;
+    consume_group<P, T>(v, E.tiles + grp.tile_first, grp.n_tiles, grp.two_shot != 0,
+                        grp.two_shot ? kNoLL : grp.ll_pkt, grp.mbase, E.slot_stride, E.scale, E.lr, E.epilogue, j,
+                        ncta, cs, cx);
+    if (E.stamps != nullptr) {
+      data_bar();
+      if (threadIdx.x == 0) E.stamps[(gi * row + slot) * 2 + 1] = globaltimer_ns();
+    }
+  }
+}
+
 // The persistent comm engine. Grid (ncta, 1) for a real rank, (ncta, P) in
 // loopback (blockIdx.y = emulated rank). Groups run FIFO in backward order;
 // group k's units go to CTAs cta0_k, cta0_k + 1, ... (mod ncta), where cta0
@@ -1006,12 +1469,16 @@ __device__ __forceinline__ void warm_group(const RankView& v, const Tile* tiles,
 // spreads over the SMs and their latencies overlap instead of queueing on
 // CTA 0. The mapping is a pure function of the plan: CTA index b does the
 // same groups, tiles and barriers on every rank.
-template <int P, typename T>
+// STREAM: the streamed protocol (a separate kernel, so each protocol gets
+// the whole register budget).
+template <int P, typename T, bool STREAM>
 __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant__ EngineLaunch E) {
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t bars[kStages];
   __shared__ uint32_t s_iter;
   __shared__ uint32_t s_abort;
+  __shared__ uint32_t s_stream[3 * kMaxRanks];  // producer counts, consumer poll exchange [2][ranks]
+  if (threadIdx.x < 3 * kMaxRanks) s_stream[threadIdx.x] = 0u;
   const RankView& v = E.views[blockIdx.y];
   if (threadIdx.x == 0) s_iter = ld_volatile_u32(E.pipe + 1);
   // Entry barrier inside (runs while the compute stream replays the forward
@@ -1022,7 +1489,11 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
   const uint32_t ncta = gridDim.x;
   const uint32_t slot = blockIdx.y * gridDim.x + blockIdx.x;      // stamp column
   const size_t row = static_cast<size_t>(gridDim.x) * gridDim.y;  // stamp row width
-  for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
+  if constexpr (P > 1 && STREAM) {
+    engine_stream<P, T>(E, v, cx, iter, slot, row, s_stream);
+    __syncthreads();
+  }
+  for (uint32_t k = 0; k + E.g_lo < E.G && !(P > 1 && STREAM); ++k) {
     const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
     const EngineGroup grp = E.groups[gi];
     const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;  // this CTA's index inside the group
@@ -1062,6 +1533,90 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
       atomicExch(E.pipe + 2, 0u);
       __threadfence();
       atomicExch(E.pipe + 1, iter + 1);
+    }
+  }
+}
+
+// ---- copy-engine mode ---------------------------------------------------------
+// During a real backward the gradients of each finished group travel to the
+// peers' arenas as copy-engine (DMA) writes over NVLink — no SM is taken
+// from the backward. After it: ce_signal_kernel publishes "iteration delivered"
+// to every peer, ce_reduce_kernel (full width) waits for every peer's
+// delivery, reduces every tile in rank order from the local arena (own
+// contribution in place) fused with SGD, and, when its last CTA is done,
+// publishes "iteration reduced" so the peers may overwrite the arena with the
+// next iteration's copies (ce_wait_kernel, before the first copy).
+
+__device__ __forceinline__ uint64_t* ce_pushed(const RankView& v, int at, int src) {
+  return reinterpret_cast<uint64_t*>(v.signal[at] + kCeWord) + src;
+}
+
+__device__ __forceinline__ uint64_t* ce_reduced(const RankView& v, int at, int src) {
+  return reinterpret_cast<uint64_t*>(v.signal[at] + kCeWord) + kMaxRanks + src;
+}
+
+// One thread per (emulated) rank: every peer has reduced iteration iter-1.
+template <int P>
+__global__ void ce_wait_kernel_t(const __grid_constant__ CeLaunch C, int n_views) {
+  if (static_cast<int>(threadIdx.x) >= n_views) return;
+  const RankView& v = C.views[threadIdx.x];
+  const uint64_t want = C.iter - 1;
+#pragma unroll 1
+  for (int q = 0; q < P; ++q) {
+    if (q == v.rank) continue;
+    const uint64_t* f = ce_reduced(v, v.rank, q);
+    if (!spin_until(v, [&] { return ld_acquire_sys_u64(f) >= want; })) return;
+  }
+}
+
+// One thread per (emulated) rank: this rank's copies of iteration `iter`
+// (queued before this kernel on its stream) are complete; tell every peer.
+template <int P>
+__global__ void ce_signal_kernel(const __grid_constant__ CeLaunch C, int n_views) {
+  if (static_cast<int>(threadIdx.x) >= n_views) return;
+  const RankView& v = C.views[threadIdx.x];
+  __threadfence_system();
+#pragma unroll 1
+  for (int q = 0; q < P; ++q) {
+    if (q != v.rank) st_release_sys_u64(ce_pushed(v, q, v.rank), C.iter);
+  }
+}
+
+// Full-width reduce + SGD of every tile of the plan from the local arena.
+// kThreads threads (the data-thread layout of reduce_tile_staged).
+template <int P, typename T>
+__global__ void __launch_bounds__(kThreads, 1) ce_reduce_kernel(const __grid_constant__ CeLaunch C) {
+  extern __shared__ __align__(1024) uint8_t dsmem[];
+  __shared__ uint32_t s_ok;
+  const RankView& v = C.views[blockIdx.y];
+  const int t = static_cast<int>(threadIdx.x);
+  if (t == 0) s_ok = 1u;
+  __syncthreads();
+  if (t < P && t != v.rank) {
+    const uint64_t* f = ce_pushed(v, v.rank, t);
+    if (!spin_until(v, [&] { return ld_acquire_sys_u64(f) >= C.iter; })) s_ok = 0u;
+  }
+  __syncthreads();
+  if (s_ok) {
+    float4* staging = reinterpret_cast<float4*>(dsmem);
+    const uint64_t my_slot = static_cast<uint64_t>(v.rank) * C.slot_stride;
+    for (uint32_t ti = blockIdx.x; ti < C.n_tiles; ti += gridDim.x) {
+      reduce_tile_staged<P, T>(v, C.tiles[ti], C.slot_stride, false, my_slot, C.scale, C.lr, C.epilogue, staging);
+    }
+  }
+  __syncthreads();
+  if (t == 0 && s_ok) {
+    // every CTA of this rank has read its arena tiles: the last one lets the
+    // peers push the next iteration
+    __threadfence();
+    uint32_t* done = C.done + blockIdx.y;
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      *done = 0u;
+      __threadfence_system();
+#pragma unroll 1
+      for (int q = 0; q < P; ++q) {
+        if (q != v.rank) st_release_sys_u64(ce_reduced(v, q, v.rank), C.iter);
+      }
     }
   }
 }
@@ -1193,19 +1748,20 @@ cudaError_t launch_lb(const GroupLaunch& L, dim3 grid, bool two, cudaStream_t s)
   }
 }
 
-template <typename T>
+template <typename T, bool S>
 const void* engine_fn_t(int nranks) {
   switch (nranks) {
-    case 1: return reinterpret_cast<const void*>(engine_kernel<1, T>);
-    case 2: return reinterpret_cast<const void*>(engine_kernel<2, T>);
-    case 4: return reinterpret_cast<const void*>(engine_kernel<4, T>);
-    case 8: return reinterpret_cast<const void*>(engine_kernel<8, T>);
+    case 1: return reinterpret_cast<const void*>(engine_kernel<1, T, false>);
+    case 2: return reinterpret_cast<const void*>(engine_kernel<2, T, S>);
+    case 4: return reinterpret_cast<const void*>(engine_kernel<4, T, S>);
+    case 8: return reinterpret_cast<const void*>(engine_kernel<8, T, S>);
     default: return nullptr;
   }
 }
 
-const void* engine_fn(int nranks, int dtype) {
-  return dtype == MGW_DTYPE_BF16 ? engine_fn_t<bf16>(nranks) : engine_fn_t<float>(nranks);
+const void* engine_fn(int nranks, int dtype, bool stream) {
+  if (stream) return dtype == MGW_DTYPE_BF16 ? engine_fn_t<bf16, true>(nranks) : engine_fn_t<float, true>(nranks);
+  return dtype == MGW_DTYPE_BF16 ? engine_fn_t<bf16, false>(nranks) : engine_fn_t<float, false>(nranks);
 }
 
 template <typename T>
@@ -1245,14 +1801,14 @@ cudaError_t launch_group_allreduce(const GroupLaunch& L, int ctas_per_rank, bool
 }
 
 cudaError_t launch_engine(const EngineLaunch& E, int ctas, int ranks, cudaStream_t stream) {
-  const void* fn = engine_fn(E.nranks, E.dtype);
+  const void* fn = engine_fn(E.nranks, E.dtype, E.stream != 0);
   if (fn == nullptr) return cudaErrorInvalidValue;
   void* args[] = {const_cast<EngineLaunch*>(&E)};
   return cudaLaunchKernel(fn, dim3(ctas, ranks), dim3(kBlock), args, smem_for(E.nranks), stream);
 }
 
 cudaError_t engine_ctas_per_sm(int nranks, int dtype, int* out) {
-  const void* fn = engine_fn(nranks, dtype);
+  const void* fn = engine_fn(nranks, dtype, true);
   if (fn == nullptr) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kBlock, smem_for(nranks));
 }
@@ -1310,6 +1866,8 @@ cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long lon
 // for the first time while the persistent engine spins waiting for it would
 // therefore deadlock (measured: the engine hit its 10 s ready timeout, then
 // the mark kernel ran). Every kernel is loaded up front instead.
+cudaError_t preload_ce_kernels();
+
 cudaError_t preload_kernels() {
   const void* fns[] = {
       reinterpret_cast<const void*>(mark_ready_kernel),
@@ -1326,9 +1884,13 @@ cudaError_t preload_kernels() {
     const cudaError_t e = cudaFuncGetAttributes(&attr, f);
     if (e != cudaSuccess) return e;
   }
+  {
+    const cudaError_t e = preload_ce_kernels();
+    if (e != cudaSuccess) return e;
+  }
   for (int dt : {MGW_DTYPE_F32, MGW_DTYPE_BF16}) {
     for (int p : {1, 2, 4, 8}) {
-      const void* ks[] = {engine_fn(p, dt), group_fn(p, false, false, dt), group_fn(p, true, false, dt),
+      const void* ks[] = {engine_fn(p, dt, true), engine_fn(p, dt, false), group_fn(p, false, false, dt), group_fn(p, true, false, dt),
                           group_fn(p, false, true, dt), group_fn(p, true, true, dt)};
       for (const void* f : ks) {
         cudaFuncAttributes attr;
@@ -1348,6 +1910,58 @@ cudaError_t launch_mark_ready(const uint32_t* pipe, uint32_t* flags, uint32_t g,
                               cudaStream_t stream) {
   mark_ready_kernel<<<1, 32, 0, stream>>>(pipe, flags, g);
   return cudaGetLastError();
+}
+
+
+namespace {
+template <int P>
+cudaError_t ce_launch_p(int what, const CeLaunch& C, int n_views, int ctas, cudaStream_t s) {
+  if (what == 0) {
+    ce_wait_kernel_t<P><<<1, 32, 0, s>>>(C, n_views);
+  } else if (what == 1) {
+    ce_signal_kernel<P><<<1, 32, 0, s>>>(C, n_views);
+  } else {
+    const size_t smem = static_cast<size_t>(kThreads) * kStageSlots * 16;
+    const dim3 grid(ctas, n_views);
+    if (C.dtype == MGW_DTYPE_BF16) {
+      ce_reduce_kernel<P, bf16><<<grid, kThreads, smem, s>>>(C);
+    } else {
+      ce_reduce_kernel<P, float><<<grid, kThreads, smem, s>>>(C);
+    }
+  }
+  return cudaGetLastError();
+}
+}  // namespace
+
+// what: 0 wait (peers reduced iter-1), 1 signal (iter delivered), 2 reduce.
+cudaError_t launch_ce(int what, const CeLaunch& C, int n_views, int ctas, cudaStream_t stream) {
+  switch (C.nranks) {
+    case 2: return ce_launch_p<2>(what, C, n_views, ctas, stream);
+    case 4: return ce_launch_p<4>(what, C, n_views, ctas, stream);
+    case 8: return ce_launch_p<8>(what, C, n_views, ctas, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t preload_ce_kernels() {
+  const size_t smem = static_cast<size_t>(kThreads) * kStageSlots * 16;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(ce_reduce_kernel<2, float>), reinterpret_cast<const void*>(ce_reduce_kernel<4, float>),
+      reinterpret_cast<const void*>(ce_reduce_kernel<8, float>), reinterpret_cast<const void*>(ce_reduce_kernel<2, bf16>),
+      reinterpret_cast<const void*>(ce_reduce_kernel<4, bf16>), reinterpret_cast<const void*>(ce_reduce_kernel<8, bf16>)};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  const void* small[] = {reinterpret_cast<const void*>(ce_wait_kernel_t<2>), reinterpret_cast<const void*>(ce_wait_kernel_t<4>),
+                         reinterpret_cast<const void*>(ce_wait_kernel_t<8>), reinterpret_cast<const void*>(ce_signal_kernel<2>),
+                         reinterpret_cast<const void*>(ce_signal_kernel<4>), reinterpret_cast<const void*>(ce_signal_kernel<8>)};
+  for (const void* f : small) {
+    cudaFuncAttributes attr;
+    const cudaError_t e = cudaFuncGetAttributes(&attr, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace mgw

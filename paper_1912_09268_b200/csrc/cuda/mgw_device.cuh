@@ -51,6 +51,26 @@ constexpr int kStateWords = kStateCtaBase + kMaxCtas;
 // so a slot holds kLLSlotPackets * 4 bytes of gradient data per plan.
 constexpr uint64_t kLLSlotPackets = 1ull << 21;  // 16 MiB per source rank
 constexpr uint32_t kNoLL = 0xffffffffu;
+// LL work unit: a PART of a tile, one vector per data thread.
+constexpr uint32_t kLLParts = (kTileElems / 4 + kThreads - 1) / kThreads;  // parts per tile
+// Stream flags (the streamed protocol, no per-chunk barrier): two arrays of
+// 64-bit words [cta][src rank] after the barrier flags of every rank's signal
+// allocation. rs[b][q] = (launch epoch << 32) | tiles CTA b of rank q has
+// delivered into this rank's arena in the current launch (its producer's
+// gradient pushes); ag[b][q] = the same for owner q's reduced (all-gather)
+// tiles. Written by the source over NVLink with st.release.sys.u64, polled
+// locally with ld.acquire.sys.u64; the epoch makes every older launch's
+// value compare lower.
+constexpr int kStreamFlagWords = 2 * kMaxCtas * kMaxRanks * 2;  // in uint32 words
+constexpr int kStreamRsWord = kSignalWords;                     // first rs flag (uint32 index)
+constexpr int kStreamAgWord = kSignalWords + kMaxCtas * kMaxRanks * 2;
+// Copy-engine mode (real backward without SMs): per source rank, the
+// iteration whose gradients that rank's copy engine has delivered into this
+// rank's arena (ce_pushed), and the iteration this rank's peers have finished
+// reducing from their arenas (ce_reduced, guards the next pushes). 64-bit.
+constexpr int kCeWord = kSignalWords + kStreamFlagWords;         // [2][kMaxRanks] uint64
+constexpr int kCeWords = 2 * kMaxRanks * 2;
+constexpr int kLLWord = kCeWord + kCeWords;                      // first LL packet (uint32 index)
 
 struct Tile {
   uint32_t layer;  // layer index | alignment flags
@@ -83,6 +103,9 @@ struct GroupLaunch {
   uint64_t slot_stride;  // elements between the per-source-rank slots of an arena
   uint32_t chunk;        // max tiles per pipelined chunk of one CTA (two-shot: max(1, chunk/P) super-tiles)
   uint32_t min_chunks;   // a CTA with enough tiles splits them into at least this many chunks
+  uint32_t stream;       // 1: streamed protocol (per-tile flags), 0: chunked (per-chunk barriers)
+  uint32_t credit_batch; // streamed: bulk items per published delivery count (1, 2, 4, 8)
+  uint32_t ag_batch;     // streamed two-shot: owned super-tiles per all-gather publication
   int dtype;             // MGW_DTYPE_* of the gradients / arena
   RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
 };
@@ -116,12 +139,31 @@ struct EngineLaunch {
   uint64_t slot_stride;
   uint32_t chunk;                // as GroupLaunch::chunk
   uint32_t min_chunks;           // as GroupLaunch::min_chunks
+  uint32_t stream;               // as GroupLaunch::stream
+  uint32_t credit_batch;         // as GroupLaunch::credit_batch
+  uint32_t ag_batch;             // as GroupLaunch::ag_batch
   int dtype;                     // MGW_DTYPE_* of the gradients / arena
   uint32_t* pipe;                // [1] iteration, [2] CTA exit count, [3] ready-timeout flag
   const uint32_t* ready;         // G flags: group g ready for iteration i when >= i + 1
   uint32_t no_wait;              // 1: every group is ready (standalone drain: roofline / ncu runs)
   unsigned long long* stamps;    // [G][ranks*ncta][2]: (start, end) %globaltimer of each group on each
                                  // CTA (NULL: no timing); the group's span is min start .. max end
+};
+
+// Copy-engine mode: the after-backward reduce of every group (the data
+// arrived during the backward as copy-engine writes into the arenas).
+struct CeLaunch {
+  RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank (loopback, blockIdx.y)
+  const Tile* tiles;          // the whole plan's tiles
+  uint32_t n_tiles;
+  int nranks;
+  float scale;
+  float lr;
+  int epilogue;
+  uint64_t slot_stride;
+  uint64_t iter;              // this iteration's sequence number (>= 1, identical on every rank)
+  uint32_t* done;             // per view: CTA completion counter
+  int dtype;
 };
 
 #ifdef __CUDACC__
@@ -149,6 +191,16 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 

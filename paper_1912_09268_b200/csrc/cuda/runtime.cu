@@ -44,6 +44,7 @@ cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long lon
 cudaError_t launch_mark_ready(const uint32_t* pipe, uint32_t* flags, uint32_t g,
                               cudaStream_t stream);
 cudaError_t preload_kernels();
+cudaError_t launch_ce(int what, const CeLaunch& C, int n_views, int ctas, cudaStream_t stream);
 cudaError_t engine_ctas_per_sm(int nranks, int dtype, int* out);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, int ctas, cudaStream_t stream);
 
@@ -83,7 +84,10 @@ struct mgw_comm {
   uint64_t oneshot_max = 512 * 1024;
   int num_sms = 148;
   uint32_t chunk_tiles = 16;  // max tiles of a CTA's pipelined chunk (mgw_comm_set_chunk_tiles)
-  uint32_t min_chunks = 4;    // a CTA splits its tiles into at least this many chunks (mgw_comm_set_min_chunks)
+  uint32_t min_chunks = 1;    // a CTA splits its tiles into at least this many chunks (mgw_comm_set_chunk_tiles)
+  uint32_t credit_batch = 8;  // streamed: bulk items per published delivery count (mgw_comm_set_stream_batches)
+  uint32_t ag_batch = 4;      // streamed two-shot: owned super-tiles per all-gather publication
+  uint32_t proto_stream = 0;  // 1: streamed protocol, 0: chunked with per-chunk barriers (mgw_comm_set_protocol)
   uint64_t ll_max = 64 << 10; // one-shot groups up to this many bytes use LL packets (mgw_comm_set_ll_max)
   int max_ctas = 0;           // cap on the CTAs of a standalone group launch (0: one per SM)
   uint64_t small_tile_max = 0; // groups below this many bytes use kTileElems / 4 tiles (mgw_comm_set_small_tile_max)
@@ -100,6 +104,7 @@ struct mgw_comm {
   bool peers_ready = false;
   cudaStream_t stream = nullptr;  // calibrate / plain all-reduce
   unsigned long long* d_clock = nullptr;  // calibration spin clock
+  uint64_t ce_seq = 0;  // copy-engine mode iterations run on this communicator (identical on every rank)
   int occ_cache[2][2] = {{0, 0}, {0, 0}};  // [dtype][two_shot]           // CTAs/SM of the one-shot / two-shot kernel
   // cached single-buffer plan for mgw_allreduce
   mgw_plan* ar_plan = nullptr;
@@ -221,7 +226,7 @@ uint64_t default_oneshot_max(int nranks) {
 
 // Signal allocation: the flags, then one LL slot per source rank.
 size_t signal_words(int nranks) {
-  return kSignalWords + static_cast<size_t>(nranks) * kLLSlotPackets * 2;
+  return kLLWord + static_cast<size_t>(nranks) * kLLSlotPackets * 2;
 }
 
 // Largest one-shot group that travels as LL packets (0 disables LL).
@@ -257,7 +262,7 @@ int grid_for(mgw_comm* c, uint32_t n_tiles, bool two_shot, int dtype = MGW_DTYPE
   cap = std::min(cap, kMaxCtas);
   if (c->max_ctas > 0) cap = std::min(cap, c->max_ctas);
   const uint32_t units = two_shot ? (n_tiles + c->nranks - 1) / c->nranks
-                                  : (ll ? n_tiles * (kTileElems / 4 / kBlock) : n_tiles);
+                                  : (ll ? n_tiles * kLLParts : n_tiles);
   return static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(units, cap)));
 }
 
@@ -283,6 +288,9 @@ void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStre
   L.slot_stride = p->slot_stride;
   L.chunk = c->chunk_tiles;
   L.min_chunks = c->min_chunks;
+  L.stream = c->proto_stream;
+  L.credit_batch = c->credit_batch;
+  L.ag_batch = c->ag_batch;
   L.dtype = p->dtype;
   for (int r = 0; r < p->n_views; ++r) {
     L.views[r] = make_view(c, r, p->d_grads + static_cast<size_t>(r) * p->L,
@@ -567,6 +575,36 @@ int mgw_comm_set_chunk_tiles(mgw_comm* c, uint32_t max_tiles, uint32_t min_chunk
   MGW_CATCH
 }
 
+int mgw_comm_set_protocol(mgw_comm* c, int protocol) {
+  MGW_TRY {
+    require(c != nullptr, "comm is NULL");
+    require(protocol == MGW_PROTO_STREAM || protocol == MGW_PROTO_CHUNKED,
+            "protocol must be MGW_PROTO_STREAM or MGW_PROTO_CHUNKED");
+    c->proto_stream = protocol == MGW_PROTO_STREAM ? 1u : 0u;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_set_stream_batches(mgw_comm* c, uint32_t credit_batch, uint32_t ag_batch) {
+  MGW_TRY {
+    require(c != nullptr, "comm is NULL");
+    require(credit_batch == 1 || credit_batch == 2 || credit_batch == 4 || credit_batch == 8,
+            "credit_batch must be 1, 2, 4 or 8");
+    require(ag_batch >= 1, "ag_batch must be >= 1");
+    c->credit_batch = credit_batch;
+    c->ag_batch = ag_batch;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_get_protocol(const mgw_comm* c, int* protocol) {
+  MGW_TRY {
+    require(c != nullptr && protocol != nullptr, "NULL argument");
+    *protocol = c->proto_stream ? MGW_PROTO_STREAM : MGW_PROTO_CHUNKED;
+  }
+  MGW_CATCH
+}
+
 int mgw_comm_get_tuning(const mgw_comm* c, uint64_t* oneshot_max, uint64_t* ll_max, uint64_t* small_tile_max,
                         uint32_t* chunk_tiles, uint32_t* min_chunks) {
   MGW_TRY {
@@ -728,6 +766,9 @@ int mgw_allreduce(mgw_comm* c, float* buf, size_t n, int algo, void* stream) {
     L.slot_stride = p->slot_stride;
     L.chunk = c->chunk_tiles;
     L.min_chunks = c->min_chunks;
+    L.stream = c->proto_stream;
+    L.credit_batch = c->credit_batch;
+    L.ag_batch = c->ag_batch;
     L.dtype = MGW_DTYPE_F32;
     L.ll_pkt = mgw::kNoLL;
     L.mbase = 0;
@@ -886,7 +927,7 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
     e.mbase = static_cast<uint32_t>(p->offs[p->heads[g]]);
     const uint32_t P = static_cast<uint32_t>(c->nranks);
     e.units = (P > 1 && e.two_shot) ? (e.n_tiles + P - 1) / P
-                                    : (P > 1 && e.ll_pkt != kNoLL ? e.n_tiles * (kTileElems / 4 / kBlock) : e.n_tiles);
+                                    : (P > 1 && e.ll_pkt != kNoLL ? e.n_tiles * kLLParts : e.n_tiles);
     e.cta0 = static_cast<uint32_t>(next % ncta);
     next += std::min<uint32_t>(e.units, ncta);
   }
@@ -911,6 +952,9 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
   E.slot_stride = p->slot_stride;
   E.chunk = c->chunk_tiles;
   E.min_chunks = c->min_chunks;
+  E.stream = c->proto_stream;
+  E.credit_batch = c->credit_batch;
+  E.ag_batch = c->ag_batch;
   E.dtype = p->dtype;
   E.pipe = pipe->d_pipe;
   E.ready = pipe->d_ready;
@@ -1417,3 +1461,209 @@ int mgw_pipeline_debug(mgw_pipeline* pipe, uint32_t* engine_state4, uint64_t* cl
 }
 
 }  // extern "C"
+
+// ---- copy-engine mode (real backward, no SMs during the backward) ----------
+struct mgw_ce {
+  mgw_plan* plan = nullptr;
+  cudaStream_t comm = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  std::vector<cudaEvent_t> ready;  // G
+  struct Copy {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  std::vector<std::vector<Copy>> copies;  // [G]: every view's copies to every peer
+  mgw::CeLaunch args{};
+  uint32_t* d_done = nullptr;  // per view: reduce-kernel CTA counter
+  int n_views = 1;
+  int reduce_ctas = 0;
+  bool begun = false;
+};
+
+int mgw_ce_create(mgw_plan* p, float lr, mgw_ce** out) {
+  MGW_TRY {
+    require(p != nullptr && out != nullptr, "NULL argument");
+    mgw_comm* c = p->comm;
+    require(c->nranks > 1, "copy-engine mode needs P > 1 (P = 1 has no exchange)");
+    require(c->loopback || c->peers_ready, "communicator peers not opened (call mgw_comm_open_peers)");
+    mgw::set_device(c);
+    const size_t L = p->L;
+    // gradients must be laid out like the merge layout (one flat buffer,
+    // layer l at element offs[l]): a group is then ONE contiguous copy
+    std::vector<const char*> base(static_cast<size_t>(p->n_views), nullptr);
+    for (int r = 0; r < p->n_views; ++r) {
+      for (size_t l = 0; l < L; ++l) {
+        if (p->counts[l] == 0) continue;
+        const char* g = reinterpret_cast<const char*>(p->h_grads[static_cast<size_t>(r) * L + l]);
+        if (base[r] == nullptr) base[r] = g - p->offs[l] * p->esize;
+        require(g == base[r] + p->offs[l] * p->esize,
+                "copy-engine mode needs the gradients in one flat buffer laid out like the merge layout "
+                "(layer l at element offs[l], 16-byte aligned layers)");
+      }
+      require(base[r] != nullptr, "plan has no gradient elements");
+      for (size_t l = 0; l < L; ++l) {
+        require(p->counts[l] == 0 || p->h_weights[static_cast<size_t>(r) * L + l] != nullptr,
+                "copy-engine mode applies SGD: every layer needs its weights");
+      }
+    }
+    std::unique_ptr<mgw_ce> e(new mgw_ce());
+    e->plan = p;
+    e->n_views = p->n_views;
+    const int G = p->G();
+    e->copies.resize(G);
+    for (int g = 0; g < G; ++g) {
+      const uint64_t lo = p->offs[p->heads[g]], hi = p->offs[p->heads[g + 1]];
+      const size_t bytes = (hi - lo) * p->esize;
+      if (bytes == 0) continue;
+      for (int r = 0; r < p->n_views; ++r) {
+        const int me = c->loopback ? r : c->rank;
+        for (int q = 0; q < c->nranks; ++q) {
+          if (q == me) continue;
+          char* arena = reinterpret_cast<char*>(c->loopback ? c->arenas[q] : c->peer_arena[q]);
+          e->copies[g].push_back(
+              {arena + (static_cast<uint64_t>(me) * p->slot_stride + lo) * p->esize, base[r] + lo * p->esize, bytes});
+        }
+      }
+    }
+    mgw::CeLaunch& C = e->args;
+    for (int r = 0; r < p->n_views; ++r) {
+      C.views[r] = mgw::make_view(c, r, p->d_grads + static_cast<size_t>(r) * L, p->d_weights + static_cast<size_t>(r) * L);
+    }
+    C.tiles = p->d_tiles;
+    C.n_tiles = p->tile_first.back();
+    C.nranks = c->nranks;
+    C.scale = 1.0f / static_cast<float>(c->nranks);
+    C.lr = lr;
+    C.epilogue = MGW_SGD;
+    C.slot_stride = p->slot_stride;
+    C.dtype = p->dtype;
+    ck(cudaMalloc(&e->d_done, sizeof(uint32_t) * mgw::kMaxRanks), "cudaMalloc(ce done)");
+    ck(cudaMemset(e->d_done, 0, sizeof(uint32_t) * mgw::kMaxRanks), "memset(ce done)");
+    C.done = e->d_done;
+    e->reduce_ctas = std::max(1, c->num_sms / (c->loopback ? 1 : 1));
+    ck(cudaStreamCreateWithFlags(&e->comm, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming), "event");
+    e->ready.resize(G);
+    for (auto& ev : e->ready) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    *out = e.release();
+  }
+  MGW_CATCH
+}
+
+int mgw_ce_begin(mgw_ce* e, void* after_stream) {
+  MGW_TRY {
+    require(e != nullptr, "NULL engine");
+    require(!e->begun, "mgw_ce_begin twice without mgw_ce_join");
+    mgw_comm* c = e->plan->comm;
+    mgw::set_device(c);
+    ck(cudaEventRecord(e->fork, static_cast<cudaStream_t>(after_stream)), "fork");
+    ck(cudaStreamWaitEvent(e->comm, e->fork, 0), "fork wait");
+    e->args.iter = ++c->ce_seq;
+    // the peers finished reducing the previous iteration out of their arenas
+    ck(mgw::launch_ce(0, e->args, e->n_views, 1, e->comm), "ce wait");
+    mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    e->begun = true;
+  }
+  MGW_CATCH
+}
+
+int mgw_ce_mark_ready(mgw_ce* e, int g, void* stream) {
+  MGW_TRY {
+    require(e != nullptr && e->begun, "mgw_ce_mark_ready outside mgw_ce_begin / mgw_ce_join");
+    require(g >= 0 && g < e->plan->G(), "group index out of range");
+    mgw::set_device(e->plan->comm);
+    ck(cudaEventRecord(e->ready[g], static_cast<cudaStream_t>(stream)), "ready");
+    ck(cudaStreamWaitEvent(e->comm, e->ready[g], 0), "ready wait");
+    for (const auto& cp : e->copies[g]) {
+      ck(cudaMemcpyAsync(cp.dst, cp.src, cp.bytes, cudaMemcpyDeviceToDevice, e->comm), "copy-engine push");
+    }
+  }
+  MGW_CATCH
+}
+
+int mgw_ce_join(mgw_ce* e, void* stream) {
+  MGW_TRY {
+    require(e != nullptr && e->begun, "mgw_ce_join without mgw_ce_begin");
+    mgw::set_device(e->plan->comm);
+    ck(mgw::launch_ce(1, e->args, e->n_views, 1, e->comm), "ce signal");
+    ck(mgw::launch_ce(2, e->args, e->n_views, e->reduce_ctas, e->comm), "ce reduce");
+    mgw::g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
+    ck(cudaEventRecord(e->join, e->comm), "join");
+    ck(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), e->join, 0), "join wait");
+    e->begun = false;
+  }
+  MGW_CATCH
+}
+
+int mgw_ce_check(mgw_ce* e) {
+  MGW_TRY {
+    require(e != nullptr, "NULL engine");
+    mgw::set_device(e->plan->comm);
+    ck(cudaStreamSynchronize(e->comm), "ce sync");
+    mgw::check_barrier_flags(e->plan->comm);
+  }
+  MGW_CATCH
+}
+
+int mgw_ce_destroy(mgw_ce* e) {
+  MGW_TRY {
+    if (e == nullptr) return 0;
+    mgw::set_device(e->plan->comm);
+    cudaStreamSynchronize(e->comm);
+    for (auto ev : e->ready) cudaEventDestroy(ev);
+    cudaEventDestroy(e->fork);
+    cudaEventDestroy(e->join);
+    cudaStreamDestroy(e->comm);
+    cudaFree(e->d_done);
+    delete e;
+  }
+  MGW_CATCH
+}
+
+int mgw_calibrate_ce(mgw_comm* c, const uint64_t* sizes_bytes, size_t n, int warmup, int reps, mgw_meas* out) {
+  MGW_TRY {
+    require(c != nullptr && sizes_bytes != nullptr && out != nullptr && n >= 1 && reps >= 1, "bad arguments");
+    require(c->loopback || c->nranks == 1 || c->peers_ready, "communicator peers not opened");
+    mgw::set_device(c);
+    const int me = c->loopback ? 0 : c->rank;
+    const int q = (me + 1) % c->nranks;
+    char* dst = reinterpret_cast<char*>(c->nranks == 1 ? c->arenas[0]
+                                                       : (c->loopback ? c->arenas[q] : c->peer_arena[q]));
+    uint64_t top = 0;
+    for (size_t i = 0; i < n; ++i) top = std::max(top, sizes_bytes[i]);
+    require(top <= c->arena_elems * sizeof(float), "calibration size exceeds the arena");
+    void* src = nullptr;
+    ck(cudaMalloc(&src, std::max<uint64_t>(top, 16)), "cudaMalloc(calibration source)");
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    try {
+      for (size_t i = 0; i < n; ++i) {
+        std::vector<float> ts;
+        for (int k = 0; k < warmup + reps; ++k) {
+          ck(cudaEventRecord(e0, c->stream), "record");
+          ck(cudaMemcpyAsync(dst, src, sizes_bytes[i], cudaMemcpyDeviceToDevice, c->stream), "copy");
+          ck(cudaEventRecord(e1, c->stream), "record");
+          ck(cudaEventSynchronize(e1), "sync");
+          float ms = 0;
+          ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+          if (k >= warmup) ts.push_back(ms);
+        }
+        std::sort(ts.begin(), ts.end());
+        out[i].size_bytes = sizes_bytes[i];
+        out[i].time_sec = ts[ts.size() / 2] * 1e-3;
+      }
+    } catch (...) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      cudaFree(src);
+      throw;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(src);
+  }
+  MGW_CATCH
+}

@@ -31,7 +31,7 @@ import torch
 
 from . import _lib
 from .gradsched import MergePlan, check
-from .runtime import ALGO, Comm, DevicePlan, padded_elems
+from .runtime import ALGO, Comm, CopyEngine, DevicePlan, padded_elems
 
 
 class MGWFBP:
@@ -47,9 +47,12 @@ class MGWFBP:
         mode: "engine" — the persistent comm engine (engine_ctas CTAs for the
         whole backward); "launch" — one fused launch per group on a comm
         stream the moment the group is complete (launch_ctas CTAs, SMs held
-        only while a group is in flight)."""
-        if mode not in ("engine", "launch"):
-            raise ValueError("mode must be 'engine' or 'launch'")
+        only while a group is in flight); "ce" — copy-engine mode: each
+        finished group's gradients go to the peers' arenas as DMA copies (no
+        SM taken from the backward), one full-width reduce + SGD after it
+        (runtime.CopyEngine; P > 1)."""
+        if mode not in ("engine", "launch", "ce"):
+            raise ValueError("mode must be 'engine', 'launch' or 'ce'")
         self.mode, self.launch_ctas, self.comm = mode, int(launch_ctas), comm
         self.params: List[torch.nn.Parameter] = (list(params) if params is not None else
                                                  [p for p in model.parameters() if p.requires_grad])
@@ -72,15 +75,21 @@ class MGWFBP:
             off += (c + 3) & ~3
         weights = [p.data.view(-1) for p in self.params]
         self.dplan = DevicePlan(comm, grads, weights, self.plan)
-        h = C.c_void_p()
-        check(_lib.mgw_engine_create(self.dplan.handle, lr, ALGO[algo], engine_ctas,
-                                     int(record_group_times), C.byref(h)))
-        self.handle = h
-        self.dplan._adopt(self)
         self.lr, self.algo = lr, algo
         self.groups = self.plan.groups()
-        self.tail = max(0, min(int(tail_groups), len(self.groups)))
-        check(_lib.mgw_engine_set_tail(h, self.tail))
+        self.handle = None
+        self.ce = None
+        if mode == "ce":
+            self.ce = CopyEngine(self.dplan, lr)
+            self.tail = 0
+        else:
+            h = C.c_void_p()
+            check(_lib.mgw_engine_create(self.dplan.handle, lr, ALGO[algo], engine_ctas,
+                                         int(record_group_times), C.byref(h)))
+            self.handle = h
+            self.dplan._adopt(self)
+            self.tail = max(0, min(int(tail_groups), len(self.groups)))
+            check(_lib.mgw_engine_set_tail(h, self.tail))
         self.group_of = [0] * L
         for g, members in enumerate(self.groups):
             for i in members:
@@ -120,7 +129,9 @@ class MGWFBP:
         def hook(_p):
             g = self.group_of[i]
             self.remaining[g] -= 1
-            if self.remaining[g] == 0 and g >= self.tail and self.mode == "launch":
+            if self.remaining[g] == 0 and self.mode == "ce":
+                self.ce.mark_ready(g, torch.cuda.current_stream())
+            elif self.remaining[g] == 0 and g >= self.tail and self.mode == "launch":
                 self._advance(torch.cuda.current_stream())
             elif self.remaining[g] == 0 and g >= self.tail:
                 stream = torch.cuda.current_stream().cuda_stream
@@ -155,12 +166,18 @@ class MGWFBP:
         # overlap from the 2nd iteration (or from the start with eager module
         # loading); the engine starts at the first finished group
         self._lazy_launch = self._iters > 0 or os.environ.get("CUDA_MODULE_LOADING", "") == "EAGER"
+        if self.mode == "ce":
+            self.ce.begin(torch.cuda.current_stream())
 
     def end(self) -> None:
         """Make the current stream wait until every group's SGD is applied."""
         stream = torch.cuda.current_stream().cuda_stream
         missing = [g for g, r in enumerate(self.remaining) if r != 0 and g >= self.tail]
-        if self.mode == "launch":
+        if self.mode == "ce":
+            for g in missing:  # parameters that got no gradient this iteration
+                self.ce.mark_ready(g, torch.cuda.current_stream())
+            self.ce.join(torch.cuda.current_stream())
+        elif self.mode == "launch":
             for g in range(self._next, self.tail - 1, -1):  # the rest in order (incl. groups without gradients)
                 self._launch(g, torch.cuda.current_stream())
             self._next = self.tail - 1
@@ -184,7 +201,10 @@ class MGWFBP:
                                "arrived); the communicator has failed")
 
     def check(self) -> None:
-        check(_lib.mgw_engine_check(self.handle))
+        if self.ce is not None:
+            self.ce.check()
+        else:
+            check(_lib.mgw_engine_check(self.handle))
 
     def group_times_ms(self) -> List[float]:
         out = (C.c_float * max(1, len(self.groups)))()
@@ -195,6 +215,9 @@ class MGWFBP:
         for h in getattr(self, "_hooks", []):
             h.remove()
         self._hooks = []
+        if self.ce is not None:
+            self.ce.close()
+            self.ce = None
         if self.handle:
             check(_lib.mgw_pipeline_destroy(self.handle))
             self.handle = None

@@ -22,12 +22,15 @@ SGD = 1
 WRITE_GRAD = 2
 
 
-def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+def _stream_ptr(stream) -> int:
+    if isinstance(stream, int):
+        return stream
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
 
 
 F32, BF16 = 0, 1  # mgw_dtype (gradient / merge-arena element type)
+PROTOCOLS = {"stream": 0, "chunked": 1}  # MGW_PROTO_*
 
 
 def padded_elems(counts: Sequence[int], dtype: int = F32) -> int:
@@ -113,10 +116,25 @@ class Comm(_Owner):
         """Groups below nbytes use 8 KiB tiles (more CTAs per group)."""
         check(_lib.mgw_comm_set_small_tile_max(self.handle, int(nbytes)))
 
-    def set_chunk_tiles(self, max_tiles: int, min_chunks: int = 4) -> None:
-        """A CTA's tiles run in pipelined chunks of <= max_tiles tiles and at
-        least min_chunks chunks when it owns enough tiles."""
+    def set_chunk_tiles(self, max_tiles: int, min_chunks: int = 1) -> None:
+        """Chunked protocol: a CTA's tiles run in pipelined chunks of <=
+        max_tiles tiles and at least min_chunks chunks when it owns enough."""
         check(_lib.mgw_comm_set_chunk_tiles(self.handle, int(max_tiles), int(min_chunks)))
+
+    def set_protocol(self, protocol: str) -> None:
+        """'chunked' (default: one cross-rank barrier per chunk) or 'stream'
+        (per-tile delivery counts, no barrier after the entry barrier)."""
+        check(_lib.mgw_comm_set_protocol(self.handle, PROTOCOLS[protocol]))
+
+    def set_stream_batches(self, credit_batch: int = 8, ag_batch: int = 4) -> None:
+        """Streamed protocol publication batches (credit_batch in 1, 2, 4, 8)."""
+        check(_lib.mgw_comm_set_stream_batches(self.handle, int(credit_batch), int(ag_batch)))
+
+    @property
+    def protocol(self) -> str:
+        v = C.c_int()
+        check(_lib.mgw_comm_get_protocol(self.handle, C.byref(v)))
+        return {i: n for n, i in PROTOCOLS.items()}[v.value]
 
     def num_peers(self) -> int:
         """Ranks this communicator can address (itself included)."""
@@ -141,7 +159,7 @@ class Comm(_Owner):
         ct, mc = C.c_uint32(), C.c_uint32()
         check(_lib.mgw_comm_get_tuning(self.handle, C.byref(o), C.byref(l), C.byref(t), C.byref(ct), C.byref(mc)))
         return {"oneshot_max": o.value, "ll_max": l.value, "small_tile_max": t.value,
-                "chunk_tiles": ct.value, "min_chunks": mc.value}
+                "chunk_tiles": ct.value, "min_chunks": mc.value, "protocol": self.protocol}
 
     @property
     def ll_max_bytes(self) -> int:
@@ -165,6 +183,12 @@ class Comm(_Owner):
         out = (_lib.Meas * len(sizes))()
         check(_lib.mgw_calibrate(self.handle, arr(C.c_uint64, sizes), len(sizes), warmup, reps,
                                  ALGO[algo], out))
+        return [CommMeasurement(out[i].size_bytes, out[i].time_sec) for i in range(len(sizes))]
+
+    def calibrate_ce(self, sizes: Sequence[int], warmup: int = 3, reps: int = 15) -> List[CommMeasurement]:
+        """Copy-engine pushes (rank -> rank+1 peer copy): median seconds per size."""
+        out = (_lib.Meas * len(sizes))()
+        check(_lib.mgw_calibrate_ce(self.handle, arr(C.c_uint64, sizes), len(sizes), warmup, reps, out))
         return [CommMeasurement(out[i].size_bytes, out[i].time_sec) for i in range(len(sizes))]
 
     def calibrate_engine(self, sizes: Sequence[int], warmup: int = 2, reps: int = 5,
@@ -341,6 +365,44 @@ class Pipeline:
     def close(self) -> None:
         if self.handle:
             check(_lib.mgw_pipeline_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class CopyEngine:
+    """Copy-engine mode of a real backward (mgw_ce_*): each group's gradients
+    go to the peers' arenas as DMA copies when the group is marked ready (no
+    SM taken from the backward); join() reduces every tile + SGD full width.
+    The plan's gradients must be one flat buffer in the merge layout."""
+
+    def __init__(self, dplan: DevicePlan, lr: float):
+        self.dplan = dplan
+        self.handle = None
+        h = C.c_void_p()
+        check(_lib.mgw_ce_create(dplan.handle, lr, C.byref(h)))
+        self.handle = h
+        dplan._adopt(self)
+
+    def begin(self, stream=None) -> None:
+        check(_lib.mgw_ce_begin(self.handle, _stream_ptr(stream)))
+
+    def mark_ready(self, g: int, stream=None) -> None:
+        check(_lib.mgw_ce_mark_ready(self.handle, g, _stream_ptr(stream)))
+
+    def join(self, stream=None) -> None:
+        check(_lib.mgw_ce_join(self.handle, _stream_ptr(stream)))
+
+    def check(self) -> None:
+        check(_lib.mgw_ce_check(self.handle))
+
+    def close(self) -> None:
+        if self.handle:
+            check(_lib.mgw_ce_destroy(self.handle))
             self.handle = None
 
     def __del__(self):  # pragma: no cover

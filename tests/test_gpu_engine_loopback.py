@@ -66,7 +66,8 @@ def algo_mix(dp, comm):
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_engine_pipeline_ragged_bit_exact(P):
+@pytest.mark.parametrize("protocol", ["stream", "chunked"])
+def test_engine_pipeline_ragged_bit_exact(P, protocol):
     """Replay pipeline, 3 iterations, LL + one-shot + two-shot groups in one
     engine launch; the rank-order result on every emulated rank."""
     rng = np.random.default_rng(700 + P)
@@ -81,6 +82,7 @@ def test_engine_pipeline_ragged_bit_exact(P):
     assert comm.num_peers() == P
     comm.set_oneshot_max(256 * 1024)
     comm.set_ll_max(16 * 1024)
+    comm.set_protocol(protocol)
     dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
     pipe = rt.Pipeline(dp, tr, LR, record_group_times=True, l2_flush_bytes=32 << 20, engine_ctas=-1)
     ms = pipe.run(3)

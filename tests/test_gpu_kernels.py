@@ -89,8 +89,9 @@ def test_unpack_sgd_kernel_bit_exact():
 
 @pytest.mark.parametrize("P", [1, 2, 4, 8])
 @pytest.mark.parametrize("algo", ["oneshot", "twoshot", "auto"])
-def test_fused_group_allreduce_bit_exact_vs_oracle(P, algo):
-    if P == 1 and algo != "auto":
+@pytest.mark.parametrize("protocol", ["stream", "chunked"])
+def test_fused_group_allreduce_bit_exact_vs_oracle(P, algo, protocol):
+    if P == 1 and (algo != "auto" or protocol != "stream"):
         pytest.skip("P=1 has no exchange")
     rng = np.random.default_rng(100 + P)
     counts = RAGGED
@@ -104,6 +105,7 @@ def test_fused_group_allreduce_bit_exact_vs_oracle(P, algo):
     else:
         comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
         comm.set_oneshot_max(16 * 1024)  # auto: small groups one-shot, big two-shot
+        comm.set_protocol(protocol)
         dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
     # three iterations (exercises the epoch counter and arena parity)
     for it in range(3):

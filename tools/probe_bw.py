@@ -2,8 +2,8 @@
 fused engine kernel (one-shot / two-shot, CTA counts) vs NCCL, large sizes.
 
 Tool-level env (the library itself reads no environment): SIZES_KB / SIZES_MB,
-ALGOS, CTAS, REPS, DTYPE, STANDALONE, and KNOBS = ";"-separated
-"chunk_tiles,min_chunks,small_tile_max_KiB[,ll_max_KiB]" configurations set
+ALGOS, CTAS, REPS, DTYPE, STANDALONE, PROTOS (stream,chunked), and KNOBS = ";"-separated
+"chunk_tiles,min_chunks,small_tile_max_KiB[,ll_max_KiB[,credit_batch,ag_batch]]" configurations set
 through the C-ABI setters (default: the library defaults)."""
 import os
 import sys
@@ -24,14 +24,17 @@ f = 2 * (P - 1) / P
 out = []
 base = comm.tuning()
 knobs = [k for k in os.environ.get("KNOBS", "").split(";") if k] or [""]
-for knob in knobs:
-    tag = ""
+for knob, proto in [(k, p) for p in os.environ.get("PROTOS", "stream").split(",") for k in knobs]:
+    comm.set_protocol(proto)
+    tag = f" {proto}"
     if knob:
         v = [int(x) for x in knob.split(",")]
         comm.set_chunk_tiles(v[0], v[1])
         comm.set_small_tile_max(v[2] << 10)
         comm.set_ll_max((v[3] << 10) if len(v) > 3 else base["ll_max"])
-        tag = f" [ct={v[0]} mc={v[1]} stm={v[2]}K]"
+        cb, ab = (v[4], v[5]) if len(v) > 5 else (8, 4)
+        comm.set_stream_batches(cb, ab)
+        tag += f" [ct={v[0]} mc={v[1]} stm={v[2]}K cb={cb} ab={ab}]"
     for algo in os.environ.get("ALGOS", "oneshot,twoshot").split(","):
         for ctas in [int(c) for c in os.environ.get("CTAS", "64,140").split(",")]:
             m = comm.calibrate_engine(sizes, warmup=2, reps=int(os.environ.get("REPS", "10")), algo=algo,

@@ -13,6 +13,7 @@ usage: torchrun --nproc-per-node N tools/train_bench.py --model resnet50 --batch
 from __future__ import annotations
 
 import argparse
+import time
 import json
 import os
 import statistics
@@ -41,11 +42,15 @@ def time_loop(step, iters, warmup):
     D.barrier()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
     evs[0].record()
+    host = []
     for i in range(iters):
+        t0 = time.perf_counter()
         step()
+        host.append((time.perf_counter() - t0) * 1e3)
         evs[i + 1].record()
     torch.cuda.synchronize()
     ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(iters)]
+    time_loop.host_ms = statistics.median(host)  # host time to enqueue one step (no sync)
     return D.max_over_ranks(statistics.median(ms))
 
 
@@ -59,7 +64,9 @@ def main():
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--strategies", default="ddp,mgwfbp,wfbp,single")
     ap.add_argument("--tail-groups", type=int, default=1)
-    ap.add_argument("--mode", default="engine", choices=["engine", "launch"])
+    ap.add_argument("--mode", default="engine", choices=["engine", "launch", "ce"],
+                    help="mgwfbp / wfbp: persistent engine, per-group launches, or copy-engine pushes + one "
+                         "reduce after the backward (single always: one full-width launch after the backward)")
     ap.add_argument("--launch-ctas", type=int, default=16)
     ap.add_argument("--debug", action="store_true")
     args = ap.parse_args()
@@ -99,9 +106,12 @@ def main():
             params = [named[l.name] for l in trace.layers]  # the trace's layer order
             counts = [p.numel() for p in params]
             comm = rt.Comm(rank, N, local, 4 * rt.padded_elems(counts))
-            if strat == "mgwfbp":
+            base, _, scale = strat.partition("@")  # "mgwfbp@10": plan with 10x the calibrated a
+            if base == "mgwfbp":
                 sizes = [4096 << k for k in range(0, 20, 2) if (4096 << k) <= 4 * rt.padded_elems(counts)]
-                if args.mode == "launch":  # the cost of one fused launch with launch_ctas CTAs
+                if args.mode == "ce":  # the cost of one copy-engine push
+                    meas = comm.calibrate_ce(sizes, warmup=2, reps=5)
+                elif args.mode == "launch":  # the cost of one fused launch with launch_ctas CTAs
                     comm.set_max_ctas(args.launch_ctas)
                     meas = comm.calibrate(sizes, warmup=1, reps=3)
                     comm.set_max_ctas(0)
@@ -111,15 +121,20 @@ def main():
                 if N > 1:
                     dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 model_ab = gs.fit_model([gs.CommMeasurement(m.size_bytes, v) for m, v in zip(meas, t.tolist())])
+                if scale:
+                    model_ab = gs.AllReduceModel(model_ab.a * float(scale), model_ab.b)
                 plan = gs.optimal_plan(trace, model_ab)
                 D.agree_plan(plan.tags)
                 extra = {"a_us": model_ab.a * 1e6, "b_ps_per_byte": model_ab.b * 1e12}
+            elif base == "merged":  # every layer in one group, in this mode
+                plan, extra = gs.MergePlan.all_merged(len(params)), {}
             elif strat == "wfbp":
                 plan, extra = gs.MergePlan.all_normal(len(params)), {}
             else:
                 plan, extra = gs.MergePlan.all_merged(len(params)), {}
+            mode = "engine" if (strat == "single" and args.mode == "ce") else args.mode
             sync = MGWFBP(model, comm, args.lr, plan=plan, engine_ctas=args.engine_ctas, params=params,
-                          tail_groups=args.tail_groups, mode=args.mode, launch_ctas=args.launch_ctas)
+                          tail_groups=args.tail_groups, mode=mode, launch_ctas=args.launch_ctas)
             if args.debug:
                 import time
                 for k in range(4):
@@ -138,7 +153,7 @@ def main():
 
             ms = time_loop(step, args.iters, args.warmup)
             sync.check()
-            results[strat] = {"iter_ms": ms, "groups": len(plan.groups()), **extra}
+            results[strat] = {"iter_ms": ms, "host_ms": time_loop.host_ms, "groups": len(plan.groups()), **extra}
             sync.close()
             comm.close()
         results[strat]["samples_per_s"] = N * args.batch / (results[strat]["iter_ms"] / 1e3)
