@@ -339,6 +339,9 @@ int mgw_ce_create(mgw_plan* plan, float lr, mgw_ce** out);
 int mgw_ce_begin(mgw_ce* ce, void* after_stream);
 int mgw_ce_mark_ready(mgw_ce* ce, int group, void* stream);
 int mgw_ce_join(mgw_ce* ce, void* stream);
+/* Groups [0, n_tail) (the last the backward makes ready) are left to the
+ * caller (e.g. mgw_group_allreduce after the backward): no copy, no reduce. */
+int mgw_ce_set_tail(mgw_ce* ce, int n_tail);
 /* Synchronise and report a timed-out wait as an error. */
 int mgw_ce_check(mgw_ce* ce);
 int mgw_ce_destroy(mgw_ce* ce);

@@ -15,7 +15,10 @@
 #include <cstring>
 #include <string>
 #include <cstdlib>
+#include <condition_variable>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -1463,6 +1466,14 @@ int mgw_pipeline_debug(mgw_pipeline* pipe, uint32_t* engine_state4, uint64_t* cl
 }  // extern "C"
 
 // ---- copy-engine mode (real backward, no SMs during the backward) ----------
+// The paper's communication daemon thread, on the host:
+// the backward's hook only appends (group, compute stream) to a single-
+// producer / single-consumer ring — no CUDA call on the main thread; a C++
+// worker thread (spinning between begin and join, asleep otherwise) records
+// the group's ready event on the compute stream (the hook ran right after
+// autograd enqueued the group's last gradient kernel, so the event covers it;
+// recording a little later only adds work before it, never less), makes the
+// comm stream wait for it and queues the group's copy-engine pushes.
 struct mgw_ce {
   mgw_plan* plan = nullptr;
   cudaStream_t comm = nullptr;
@@ -1478,8 +1489,59 @@ struct mgw_ce {
   uint32_t* d_done = nullptr;  // per view: reduce-kernel CTA counter
   int n_views = 1;
   int reduce_ctas = 0;
+  int n_tail = 0;  // groups [0, n_tail) are not copied nor reduced here (the caller's full-width launches)
   bool begun = false;
+  // daemon
+  std::vector<int> ring;              // G + 1 slots (each group at most once per iteration)
+  std::vector<cudaStream_t> ring_stream;  // the compute stream of each appended group
+  std::atomic<uint64_t> head{0};      // groups appended by the main thread (this iteration and before)
+  std::atomic<uint64_t> tail{0};      // groups whose copies the worker queued
+  std::atomic<bool> active{false};    // between begin and join: the worker spins
+  std::atomic<bool> stop{false};
+  std::mutex mu;
+  std::condition_variable cv;
+  std::thread worker;
+  std::string error;                  // first CUDA error of the worker (guarded by mu)
 };
+
+namespace mgw {
+namespace {
+
+void ce_worker(mgw_ce* e) {
+  if (cudaSetDevice(e->plan->comm->device) != cudaSuccess) return;
+  const size_t n = e->ring.size();
+  for (;;) {
+    {
+      std::unique_lock<std::mutex> lk(e->mu);
+      e->cv.wait(lk, [&] { return e->stop.load() || e->active.load() ||
+                                  e->tail.load() != e->head.load(std::memory_order_acquire); });
+      if (e->stop.load() && e->tail.load() == e->head.load()) return;
+    }
+    // spin while the iteration is open: a hook's append is picked up at once
+    while (!e->stop.load(std::memory_order_relaxed)) {
+      const uint64_t t = e->tail.load(std::memory_order_relaxed);
+      if (t == e->head.load(std::memory_order_acquire)) {
+        if (!e->active.load(std::memory_order_acquire)) break;
+        continue;
+      }
+      const int g = e->ring[t % n];
+      cudaError_t err = cudaEventRecord(e->ready[g], e->ring_stream[t % n]);
+      if (err == cudaSuccess) err = cudaStreamWaitEvent(e->comm, e->ready[g], 0);
+      for (const auto& cp : e->copies[g]) {
+        if (err != cudaSuccess) break;
+        err = cudaMemcpyAsync(cp.dst, cp.src, cp.bytes, cudaMemcpyDeviceToDevice, e->comm);
+      }
+      if (err != cudaSuccess) {
+        std::lock_guard<std::mutex> lk(e->mu);
+        if (e->error.empty()) e->error = std::string("copy-engine push: ") + cudaGetErrorString(err);
+      }
+      e->tail.store(t + 1, std::memory_order_release);
+    }
+  }
+}
+
+}  // namespace
+}  // namespace mgw
 
 int mgw_ce_create(mgw_plan* p, float lr, mgw_ce** out) {
   MGW_TRY {
@@ -1541,12 +1603,15 @@ int mgw_ce_create(mgw_plan* p, float lr, mgw_ce** out) {
     ck(cudaMalloc(&e->d_done, sizeof(uint32_t) * mgw::kMaxRanks), "cudaMalloc(ce done)");
     ck(cudaMemset(e->d_done, 0, sizeof(uint32_t) * mgw::kMaxRanks), "memset(ce done)");
     C.done = e->d_done;
-    e->reduce_ctas = std::max(1, c->num_sms / (c->loopback ? 1 : 1));
+    e->reduce_ctas = c->num_sms;
     ck(cudaStreamCreateWithFlags(&e->comm, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming), "event");
     e->ready.resize(G);
     for (auto& ev : e->ready) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    e->ring.assign(static_cast<size_t>(G) + 1, 0);
+    e->ring_stream.assign(static_cast<size_t>(G) + 1, nullptr);
+    e->worker = std::thread(mgw::ce_worker, e.get());
     *out = e.release();
   }
   MGW_CATCH
@@ -1565,6 +1630,23 @@ int mgw_ce_begin(mgw_ce* e, void* after_stream) {
     ck(mgw::launch_ce(0, e->args, e->n_views, 1, e->comm), "ce wait");
     mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     e->begun = true;
+    {
+      std::lock_guard<std::mutex> lk(e->mu);
+      e->active.store(true, std::memory_order_release);
+    }
+    e->cv.notify_one();
+  }
+  MGW_CATCH
+}
+
+int mgw_ce_set_tail(mgw_ce* e, int n_tail) {
+  MGW_TRY {
+    require(e != nullptr && !e->begun, "mgw_ce_set_tail inside an iteration");
+    const mgw_plan* p = e->plan;
+    require(n_tail >= 0 && n_tail < p->G(), "tail group count out of range (the engine needs >= 1 group)");
+    e->n_tail = n_tail;
+    e->args.tiles = p->d_tiles + p->tile_first[n_tail];
+    e->args.n_tiles = p->tile_first.back() - p->tile_first[n_tail];
   }
   MGW_CATCH
 }
@@ -1573,12 +1655,12 @@ int mgw_ce_mark_ready(mgw_ce* e, int g, void* stream) {
   MGW_TRY {
     require(e != nullptr && e->begun, "mgw_ce_mark_ready outside mgw_ce_begin / mgw_ce_join");
     require(g >= 0 && g < e->plan->G(), "group index out of range");
-    mgw::set_device(e->plan->comm);
-    ck(cudaEventRecord(e->ready[g], static_cast<cudaStream_t>(stream)), "ready");
-    ck(cudaStreamWaitEvent(e->comm, e->ready[g], 0), "ready wait");
-    for (const auto& cp : e->copies[g]) {
-      ck(cudaMemcpyAsync(cp.dst, cp.src, cp.bytes, cudaMemcpyDeviceToDevice, e->comm), "copy-engine push");
-    }
+    if (g < e->n_tail) return 0;  // a tail group: the caller reduces it after the backward
+    const uint64_t h = e->head.load(std::memory_order_relaxed);
+    require(h - e->tail.load(std::memory_order_acquire) < e->ring.size(), "group marked ready twice");
+    e->ring[h % e->ring.size()] = g;
+    e->ring_stream[h % e->ring.size()] = static_cast<cudaStream_t>(stream);
+    e->head.store(h + 1, std::memory_order_release);  // the spinning worker picks it up
   }
   MGW_CATCH
 }
@@ -1587,6 +1669,14 @@ int mgw_ce_join(mgw_ce* e, void* stream) {
   MGW_TRY {
     require(e != nullptr && e->begun, "mgw_ce_join without mgw_ce_begin");
     mgw::set_device(e->plan->comm);
+    // every appended group's copies are queued on the comm stream
+    while (e->tail.load(std::memory_order_acquire) != e->head.load(std::memory_order_relaxed)) {
+    }
+    e->active.store(false, std::memory_order_release);
+    {
+      std::lock_guard<std::mutex> lk(e->mu);
+      if (!e->error.empty()) throw mgw::CudaFailure(e->error);
+    }
     ck(mgw::launch_ce(1, e->args, e->n_views, 1, e->comm), "ce signal");
     ck(mgw::launch_ce(2, e->args, e->n_views, e->reduce_ctas, e->comm), "ce reduce");
     mgw::g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
@@ -1610,6 +1700,13 @@ int mgw_ce_check(mgw_ce* e) {
 int mgw_ce_destroy(mgw_ce* e) {
   MGW_TRY {
     if (e == nullptr) return 0;
+    {
+      std::lock_guard<std::mutex> lk(e->mu);
+      e->stop.store(true);
+      e->active.store(false);
+    }
+    e->cv.notify_one();
+    if (e->worker.joinable()) e->worker.join();
     mgw::set_device(e->plan->comm);
     cudaStreamSynchronize(e->comm);
     for (auto ev : e->ready) cudaEventDestroy(ev);

@@ -81,7 +81,8 @@ class MGWFBP:
         self.ce = None
         if mode == "ce":
             self.ce = CopyEngine(self.dplan, lr)
-            self.tail = 0
+            self.tail = max(0, min(int(tail_groups), len(self.groups) - 1))
+            self.ce.set_tail(self.tail)
         else:
             h = C.c_void_p()
             check(_lib.mgw_engine_create(self.dplan.handle, lr, ALGO[algo], engine_ctas,
@@ -130,7 +131,9 @@ class MGWFBP:
             g = self.group_of[i]
             self.remaining[g] -= 1
             if self.remaining[g] == 0 and self.mode == "ce":
-                self.ce.mark_ready(g, torch.cuda.current_stream())
+                if g >= self.tail:  # a ring append, no CUDA call (the daemon records the event)
+                    if self._ce_mark(self.ce.handle, g, self._ce_stream) != 0:
+                        check(-1)
             elif self.remaining[g] == 0 and g >= self.tail and self.mode == "launch":
                 self._advance(torch.cuda.current_stream())
             elif self.remaining[g] == 0 and g >= self.tail:
@@ -167,7 +170,9 @@ class MGWFBP:
         # loading); the engine starts at the first finished group
         self._lazy_launch = self._iters > 0 or os.environ.get("CUDA_MODULE_LOADING", "") == "EAGER"
         if self.mode == "ce":
-            self.ce.begin(torch.cuda.current_stream())
+            self._ce_stream = torch.cuda.current_stream().cuda_stream
+            self._ce_mark = _lib.mgw_ce_mark_ready
+            self.ce.begin(self._ce_stream)
 
     def end(self) -> None:
         """Make the current stream wait until every group's SGD is applied."""
@@ -176,6 +181,10 @@ class MGWFBP:
         if self.mode == "ce":
             for g in missing:  # parameters that got no gradient this iteration
                 self.ce.mark_ready(g, torch.cuda.current_stream())
+            # the tail groups' fused launches first: they run next to the
+            # copy-engine reduce (NVLink-bound vs HBM-bound)
+            for g in reversed(range(self.tail)):
+                check(_lib.mgw_group_allreduce(self.dplan.handle, g, self.lr, 1, ALGO[self.algo], stream))
             self.ce.join(torch.cuda.current_stream())
         elif self.mode == "launch":
             for g in range(self._next, self.tail - 1, -1):  # the rest in order (incl. groups without gradients)
@@ -191,8 +200,9 @@ class MGWFBP:
             if not self._launched:
                 check(_lib.mgw_engine_begin(self.handle, stream))
             check(_lib.mgw_engine_join(self.handle, stream))
-        for g in reversed(range(self.tail)):  # backward order, full width
-            check(_lib.mgw_group_allreduce(self.dplan.handle, g, self.lr, 1, ALGO[self.algo], stream))
+        if self.mode != "ce":
+            for g in reversed(range(self.tail)):  # backward order, full width
+                check(_lib.mgw_group_allreduce(self.dplan.handle, g, self.lr, 1, ALGO[self.algo], stream))
         self._iters += 1
         # a timed-out wait of an earlier iteration (host-mapped flag: no sync);
         # its kernels skipped their SGD, so the weights are stale, not corrupt

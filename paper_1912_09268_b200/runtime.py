@@ -397,6 +397,10 @@ class CopyEngine:
     def join(self, stream=None) -> None:
         check(_lib.mgw_ce_join(self.handle, _stream_ptr(stream)))
 
+    def set_tail(self, n_tail: int) -> None:
+        """Leave groups [0, n_tail) to the caller (no copy, no reduce)."""
+        check(_lib.mgw_ce_set_tail(self.handle, int(n_tail)))
+
     def check(self) -> None:
         check(_lib.mgw_ce_check(self.handle))
 

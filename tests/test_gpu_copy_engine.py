@@ -37,7 +37,11 @@ def _flat(counts, arrays, dtype=torch.float32):
 
 @pytest.mark.parametrize("P", [2, 4, 8])
 @pytest.mark.parametrize("merged", [False, True])
-def test_copy_engine_bit_exact(P, merged):
+@pytest.mark.parametrize("tail", [0, 1])
+def test_copy_engine_bit_exact(P, merged, tail):
+    """3 iterations; with tail = 1 the last-ready group goes through the
+    fused full-width kernel after the backward, the rest through the copy
+    engines."""
     rng = np.random.default_rng(900 + P)
     counts = RAGGED
     g_np = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(P)]
@@ -50,6 +54,7 @@ def test_copy_engine_bit_exact(P, merged):
     comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
     dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
     ce = rt.CopyEngine(dp, 0.01)
+    ce.set_tail(tail)
     s = torch.cuda.current_stream()
     for it in range(3):
         # a new "backward" each iteration: fresh gradients, groups ready in backward order
@@ -61,6 +66,8 @@ def test_copy_engine_bit_exact(P, merged):
         ce.begin(s)
         for g in reversed(range(dp.n_groups)):
             ce.mark_ready(g, s)
+        for g in reversed(range(tail)):
+            dp.group_allreduce(g, 0.01, rt.SGD, "auto", s)
         ce.join(s)
         pyoracle.allreduce_sgd(g_np, w_np, tags, 0.01)
     torch.cuda.synchronize()

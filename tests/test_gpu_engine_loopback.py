@@ -285,3 +285,53 @@ def test_ready_timeout_fails_loudly_and_skips_sgd():
     gs.check(_lib.mgw_pipeline_destroy(h))
     dp.close()
     comm.close()
+
+
+@pytest.mark.parametrize("P,protocol", [(2, "chunked"), (2, "stream"), (4, "chunked"), (4, "stream"),
+                                        (8, "stream")])
+def test_ordering_stress_fresh_gradients_every_iteration(P, protocol):
+    """Memory-ordering stress (compute-sanitizer is closed on this pool): 60
+    engine iterations, NEW gradients every iteration (so a reduction that
+    read a stale arena slot, LL packet or peer push would show), a plan
+    mixing LL, one-shot and two-shot groups; after every iteration the
+    weights must equal torch fp32 rank-order ops on the GPU bit for bit:
+    w -= lr * (g_0 * s + g_1 * s + ...), separate rounded mul / add kernels."""
+    rng = np.random.default_rng(1234 + P)
+    counts = [700, 9000, 13, 70000, 4096, 1, 300000, 77, 2 << 20, 5000]
+    t_b = list(rng.uniform(1e-5, 6e-5, len(counts)))
+    tr = gs.trace_from_arrays(counts, t_b, 1e-4)
+    plan = gs.optimal_plan(tr, gs.AllReduceModel(5e-6, 1 / 600e9))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(77 + P)
+    g_dev = [[torch.empty(c, device="cuda") for c in counts] for _ in range(P)]
+    w0 = [torch.empty(c, device="cuda").uniform_(-1, 1, generator=gen) for c in counts]
+    w_dev = [[w.clone() for w in w0] for _ in range(P)]  # data parallel: identical weights on every rank
+    want = [w.clone() for w in w0]
+    comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
+    comm.set_oneshot_max(256 * 1024)
+    comm.set_ll_max(32 * 1024)
+    comm.set_protocol(protocol)
+    dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+    ll, one, two = algo_mix(dp, comm)
+    assert ll > 0 and one > 0 and two > 0, (ll, one, two)
+    pipe = rt.Pipeline(dp, tr, LR, record_group_times=False, l2_flush_bytes=0, engine_ctas=-1)
+    s = 1.0 / P
+    for it in range(60):
+        for r in range(P):
+            for g in g_dev[r]:
+                g.uniform_(-1, 1, generator=gen)
+        torch.cuda.synchronize()  # the pipeline runs on its own streams
+        pipe.run(1)
+        torch.cuda.synchronize()
+        for l in range(len(counts)):
+            red = g_dev[0][l] * s
+            for r in range(1, P):
+                red = red + g_dev[r][l] * s
+            want[l] = want[l] - LR * red
+        for r in range(P):
+            for l in range(len(counts)):
+                assert torch.equal(w_dev[r][l], want[l]), (it, r, l)
+    assert not comm.failed()
+    pipe.close()
+    dp.close()
+    comm.close()

@@ -78,10 +78,16 @@ def main():
     trace = gs.load_trace(os.path.join(ROOT, "traces", f"{args.model}.json"))
     results = {}
 
+    phase_ev = []  # (after forward, after backward) event pairs of the timed steps
+
     def fwd_bwd(model):
         with torch.autocast("cuda", dtype=torch.bfloat16):
             loss = loss_of(args.model, model, batch)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e[0].record()
         loss.backward()
+        e[1].record()
+        phase_ev.append(e)
 
     for strat in args.strategies.split(","):
         torch.manual_seed(0)
@@ -147,13 +153,25 @@ def main():
                 sync.check()
 
             def step():
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record()
                 sync.begin()
                 fwd_bwd(model)
                 sync.end()
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record()
+                phase_ev[-1].insert(0, e0)
+                phase_ev[-1].append(e1)
 
+            phase_ev.clear()
             ms = time_loop(step, args.iters, args.warmup)
+            ph = phase_ev[-args.iters:]
+            fwd = statistics.median(p[0].elapsed_time(p[1]) for p in ph)
+            bwd = statistics.median(p[1].elapsed_time(p[2]) for p in ph)
+            post = statistics.median(p[2].elapsed_time(p[3]) for p in ph)
             sync.check()
-            results[strat] = {"iter_ms": ms, "host_ms": time_loop.host_ms, "groups": len(plan.groups()), **extra}
+            results[strat] = {"iter_ms": ms, "host_ms": time_loop.host_ms, "groups": len(plan.groups()),
+                              "fwd_ms": fwd, "bwd_ms": bwd, "post_bwd_ms": post, **extra}
             sync.close()
             comm.close()
         results[strat]["samples_per_s"] = N * args.batch / (results[strat]["iter_ms"] / 1e3)
