@@ -471,7 +471,8 @@ def main():
         print(f"[bench] rank {rank}/{N}: {peers} ranks mapped over NVLink (CUDA IPC)", file=sys.stderr, flush=True)
     if args.oneshot_max > 0:
         comm.set_oneshot_max(args.oneshot_max)
-    comm.set_protocol(args.protocol)
+    if N > 1:
+        comm.set_protocol(args.protocol)  # (P = 1 always runs the TMA-fed single-rank engine)
 
     # ---- N1: on-box calibration of the fused engine kernel at this N
     sizes = calibration_sizes(total_bytes, 4 * padded)

@@ -1389,6 +1389,175 @@ __device__ __forceinline__ void warm_group(const RankView& v, const Tile* tiles,
   }
 }
 
+// ---- P = 1: TMA-fed gradient -> SGD pipeline ---------------------------------
+// The single-rank engine (no exchange: W -= lr * round(g * 1/P)) is HBM-bound;
+// its loads are decoupled from the math: the producer warp streams each
+// tile's gradient and weight bodies into a kP1Stages ring of shared-memory
+// stages with TMA bulk copies (one mbarrier complete_tx per stage) while the
+// data warps apply SGD from shared memory and store the weights — the
+// tile-descriptor -> pointer -> data dependency chain and the HBM latency
+// leave the critical path. Tiles TMA cannot take (unaligned views, no
+// weights) go through the data warps' registers.
+constexpr uint32_t kP1Stages = 3;
+constexpr uint32_t kP1StageBytes = 2 * kStageBytes;  // gradient body (<= 32 KiB) + weight body (32 KiB)
+constexpr size_t kSmemP1 = static_cast<size_t>(kP1Stages) * kP1StageBytes;
+
+template <typename T>
+__device__ __forceinline__ bool p1_tma_able(const Tile& t, const float* w, int epi) {
+  return !(t.layer & (kGradUnaligned | kWeightUnaligned)) && w != nullptr && (epi & MGW_SGD) &&
+         t.len >= Elem<T>::kVec;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(done)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
+template <typename T>
+__device__ __noinline__ void engine_p1(const EngineLaunch& E, const RankView& v, uint8_t* dsmem, uint64_t* full,
+                                       uint64_t* empty, uint32_t* s_abort, uint32_t iter, uint32_t slot, size_t row) {
+  const uint32_t ncta = gridDim.x;
+  const uint32_t target = iter + 1;
+  const bool producer = threadIdx.x >= kThreads;
+  const uint32_t s0 = smem_u32(dsmem);
+  if (producer) {
+    if ((threadIdx.x & 31) != 0) return;
+    uint32_t n = 0, pe = 0;
+    for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
+      const uint32_t gi = E.G - 1 - k;
+      const EngineGroup grp = E.groups[gi];
+      const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;
+      if (j >= grp.units) continue;
+      if (!E.no_wait) {
+        const uint32_t* flag = E.ready + gi;
+        if (!spin_until(v, [&] { return static_cast<int32_t>(ld_acquire_gpu(flag) - target) >= 0; })) {
+          atomicExch(E.pipe + 3, 1u);
+          *s_abort = 1u;
+        }
+      }
+      if (*reinterpret_cast<volatile uint32_t*>(s_abort)) return;
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // gradients written by generic stores
+      const Tile* tiles = E.tiles + grp.tile_first;
+      for (uint32_t ti = j; ti < grp.n_tiles; ti += ncta) {
+        const Tile t = tiles[ti];
+        const uint32_t layer = t.layer & kLayerMask;
+        const float* w = v.weights[layer];
+        if (!p1_tma_able<T>(t, w, E.epilogue)) continue;
+        const uint32_t st = n % kP1Stages;
+        if (n >= kP1Stages) {
+          if (!spin_until(v, [&] { return mbar_try(smem_u32(empty + st), (pe >> st) & 1u); })) {
+            *s_abort = 1u;
+            return;
+          }
+          pe ^= 1u << st;
+        }
+        const uint32_t body = tma_body<T>(t);
+        const uint32_t gb = body * static_cast<uint32_t>(sizeof(T)), wb = body * 4u;
+        const uint32_t bar = smem_u32(full + st);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(gb + wb) : "memory");
+        const uint32_t dst = s0 + st * kP1StageBytes;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+            "l"(as<T>(v.grads[layer]) + t.src), "r"(gb), "r"(bar)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                dst + kStageBytes),
+            "l"(w + t.src), "r"(wb), "r"(bar)
+            : "memory");
+        ++n;
+      }
+    }
+    return;
+  }
+  uint32_t m = 0, pf = 0;
+  const int tid = static_cast<int>(threadIdx.x);
+  for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
+    const uint32_t gi = E.G - 1 - k;
+    const EngineGroup grp = E.groups[gi];
+    const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;
+    if (j >= grp.units) continue;
+    if (tid == 0) {
+      if (!E.no_wait && !*reinterpret_cast<volatile uint32_t*>(s_abort)) {
+        const uint32_t* flag = E.ready + gi;
+        if (!spin_until(v, [&] { return static_cast<int32_t>(ld_acquire_gpu(flag) - target) >= 0; })) {
+          atomicExch(E.pipe + 3, 1u);
+          *s_abort = 1u;
+        }
+      }
+      if (E.stamps != nullptr) E.stamps[(gi * row + slot) * 2] = globaltimer_ns();
+    }
+    data_bar();
+    if (*reinterpret_cast<volatile uint32_t*>(s_abort)) return;
+    const Tile* tiles = E.tiles + grp.tile_first;
+    for (uint32_t ti = j; ti < grp.n_tiles; ti += ncta) {
+      const Tile t = tiles[ti];
+      const uint32_t layer = t.layer & kLayerMask;
+      float* w = v.weights[layer];
+      T* g = as<T>(v.grads[layer]);
+      if (p1_tma_able<T>(t, w, E.epilogue)) {
+        const uint32_t st = m % kP1Stages;
+        const uint32_t bar = smem_u32(full + st);
+        if (!spin_until(v, [&] { return mbar_try(bar, (pf >> st) & 1u); })) *s_abort = 1u;
+        pf ^= 1u << st;
+        const uint8_t* sg = dsmem + st * kP1StageBytes;
+        const float4* sw = reinterpret_cast<const float4*>(sg + kStageBytes);
+        const uint32_t body = tma_body<T>(t);
+        for (uint32_t i = tid; i < body / 4; i += kThreads) {
+          float4 x;
+          if constexpr (sizeof(T) == 4) {
+            x = reinterpret_cast<const float4*>(sg)[i];
+          } else {
+            const uint2 u = reinterpret_cast<const uint2*>(sg)[i];
+            x = unpack_bf16x4(u.x, u.y);
+          }
+          x = round4<T>(mul4(x, E.scale));
+          float4 wv = sw[i];
+          wv.x = sgd1(wv.x, x.x, E.lr);
+          wv.y = sgd1(wv.y, x.y, E.lr);
+          wv.z = sgd1(wv.z, x.z, E.lr);
+          wv.w = sgd1(wv.w, x.w, E.lr);
+          st_v4(w + t.src + i * 4, wv);
+          if (E.epilogue & MGW_WRITE_GRAD) st4<T>(g + t.src + i * 4, x);
+        }
+        if (tid == 0) {  // the < one-vector tail from global memory
+          for (uint32_t e = body; e < t.len; e += 4) {
+            const float4 x = round4<T>(mul4(ld4_tail<T>(g + t.src + e, t.len - e), E.scale));
+            epilogue<T>(t, e, x, w, g, E.lr, E.epilogue);
+          }
+        }
+        data_bar();  // every data thread has read the stage
+        if (tid == 0) mbar_arrive(smem_u32(empty + st));
+        ++m;
+      } else {
+        const bool aligned = !(t.layer & kGradUnaligned);
+        const uint32_t nvec = (t.len + 3) >> 2;
+        for (uint32_t i = tid; i < nvec; i += kThreads) {
+          const uint32_t e = i * 4;
+          float4 x[1], wv[1];
+          x[0] = (aligned && e + 4 <= t.len) ? ld4_stream<T>(g + t.src + e) : ld4_tail<T>(g + t.src + e, t.len - e);
+          load_w_batch<1>(t, i, kThreads, w, E.epilogue, wv);
+          x[0] = round4<T>(mul4(x[0], E.scale));
+          apply_batch<1, T>(t, i, kThreads, x, wv, w, g, E.lr, E.epilogue);
+        }
+      }
+    }
+    if (E.stamps != nullptr) {
+      data_bar();
+      if (tid == 0) E.stamps[(gi * row + slot) * 2 + 1] = globaltimer_ns();
+    }
+  }
+}
+
 // The engine's streamed body (P > 1): the producer warp walks the groups
 // pushing tiles (waiting for each group's ready flag, after publishing what
 // it has in flight), the data warps walk the same groups consuming them.
@@ -1493,7 +1662,20 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
     engine_stream<P, T>(E, v, cx, iter, slot, row, s_stream);
     __syncthreads();
   }
-  for (uint32_t k = 0; k + E.g_lo < E.G && !(P > 1 && STREAM); ++k) {
+  if constexpr (P == 1 && STREAM) {
+    __shared__ __align__(8) uint64_t p1_empty[kP1Stages];
+    if (threadIdx.x == kThreads) {
+      for (uint32_t k = 0; k < kP1Stages; ++k) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + k)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(p1_empty + k)) : "memory");
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    engine_p1<T>(E, v, dsmem, bars, p1_empty, &s_abort, iter, slot, row);
+    __syncthreads();
+  }
+  for (uint32_t k = 0; k + E.g_lo < E.G && !STREAM; ++k) {
     const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
     const EngineGroup grp = E.groups[gi];
     const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;  // this CTA's index inside the group
@@ -1723,6 +1905,8 @@ constexpr size_t kSmemBytes =
     static_cast<size_t>(kStages) * kStageBytes + static_cast<size_t>(kThreads) * kStageSlots * 16;
 
 constexpr size_t smem_for(int P) { return P > 1 ? kSmemBytes : 0; }
+// The engine: P > 1 the push ring + staging; P = 1 with STREAM the TMA SGD ring.
+constexpr size_t smem_for_engine(int P, bool stream) { return P > 1 ? kSmemBytes : (stream ? kSmemP1 : 0); }
 
 template <int P, bool TWO, bool LB, typename T>
 cudaError_t launch_t(const GroupLaunch& L, dim3 grid, cudaStream_t stream) {
@@ -1751,7 +1935,7 @@ cudaError_t launch_lb(const GroupLaunch& L, dim3 grid, bool two, cudaStream_t s)
 template <typename T, bool S>
 const void* engine_fn_t(int nranks) {
   switch (nranks) {
-    case 1: return reinterpret_cast<const void*>(engine_kernel<1, T, false>);
+    case 1: return reinterpret_cast<const void*>(engine_kernel<1, T, S>);
     case 2: return reinterpret_cast<const void*>(engine_kernel<2, T, S>);
     case 4: return reinterpret_cast<const void*>(engine_kernel<4, T, S>);
     case 8: return reinterpret_cast<const void*>(engine_kernel<8, T, S>);
@@ -1804,13 +1988,14 @@ cudaError_t launch_engine(const EngineLaunch& E, int ctas, int ranks, cudaStream
   const void* fn = engine_fn(E.nranks, E.dtype, E.stream != 0);
   if (fn == nullptr) return cudaErrorInvalidValue;
   void* args[] = {const_cast<EngineLaunch*>(&E)};
-  return cudaLaunchKernel(fn, dim3(ctas, ranks), dim3(kBlock), args, smem_for(E.nranks), stream);
+  return cudaLaunchKernel(fn, dim3(ctas, ranks), dim3(kBlock), args, smem_for_engine(E.nranks, E.stream != 0),
+                          stream);
 }
 
 cudaError_t engine_ctas_per_sm(int nranks, int dtype, int* out) {
   const void* fn = engine_fn(nranks, dtype, true);
   if (fn == nullptr) return cudaErrorInvalidValue;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kBlock, smem_for(nranks));
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kBlock, smem_for_engine(nranks, true));
 }
 
 cudaError_t max_ctas_per_sm(int nranks, bool two_shot, bool loopback, int dtype, int* out) {
@@ -1898,6 +2083,9 @@ cudaError_t preload_kernels() {
         // the TMA ring lives in dynamic shared memory (> the 48 KiB default)
         if (e == cudaSuccess && p > 1) {
           e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+        }
+        if (e == cudaSuccess && p == 1 && f == engine_fn(1, dt, true)) {
+          e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemP1));
         }
         if (e != cudaSuccess) return e;
       }

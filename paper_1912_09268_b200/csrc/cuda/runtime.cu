@@ -448,6 +448,7 @@ int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_co
     c->rank = rank;
     c->nranks = nranks;
     c->oneshot_max = mgw::default_oneshot_max(nranks);
+    c->proto_stream = nranks == 1 ? 1u : 0u;  // P = 1: the TMA-fed engine; P > 1: chunked
     c->ll_max = mgw::default_ll_max(nranks);
     c->small_tile_max = mgw::kDefaultSmallTileMax;
     mgw::init_common(c, device, arena_bytes);
@@ -470,6 +471,7 @@ int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_com
     auto* c = new mgw_comm();
     c->nranks = nranks;
     c->oneshot_max = mgw::default_oneshot_max(nranks);
+    c->proto_stream = nranks == 1 ? 1u : 0u;  // P = 1: the TMA-fed engine; P > 1: chunked
     c->ll_max = mgw::default_ll_max(nranks);
     c->small_tile_max = mgw::kDefaultSmallTileMax;
     c->loopback = true;
