@@ -38,7 +38,7 @@ class MGWFBP:
     def __init__(self, model: torch.nn.Module, comm: Comm, lr: float, plan: Optional[MergePlan] = None,
                  algo: str = "auto", engine_ctas: int = 8, record_group_times: bool = False,
                  params: Optional[List[torch.nn.Parameter]] = None, tail_groups: int = 1,
-                 mode: str = "engine", launch_ctas: int = 16):
+                 mode: str = "auto", launch_ctas: int = 16):
         """params: the layer order of the plan / trace (forward order; the
         backward visits it last to first). Default: model.parameters().
         tail_groups: the last groups the backward makes ready (groups
@@ -47,12 +47,15 @@ class MGWFBP:
         mode: "engine" — the persistent comm engine (engine_ctas CTAs for the
         whole backward); "launch" — one fused launch per group on a comm
         stream the moment the group is complete (launch_ctas CTAs, SMs held
-        only while a group is in flight); "ce" — copy-engine mode: each
+        only while a group is in flight); "auto" — "ce" at P > 1, else
+        "engine"; "ce" — copy-engine mode: each
         finished group's gradients go to the peers' arenas as DMA copies (no
         SM taken from the backward), one full-width reduce + SGD after it
         (runtime.CopyEngine; P > 1)."""
+        if mode == "auto":  # measured fastest (DESIGN.md §7b): copy engines at P > 1
+            mode = "ce" if comm.nranks > 1 else "engine"
         if mode not in ("engine", "launch", "ce"):
-            raise ValueError("mode must be 'engine', 'launch' or 'ce'")
+            raise ValueError("mode must be 'auto', 'engine', 'launch' or 'ce'")
         self.mode, self.launch_ctas, self.comm = mode, int(launch_ctas), comm
         self.params: List[torch.nn.Parameter] = (list(params) if params is not None else
                                                  [p for p in model.parameters() if p.requires_grad])

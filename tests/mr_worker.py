@@ -130,12 +130,12 @@ def main():
     L = len(list(model.parameters()))
     mplan = gs.MergePlan([gs.LayerTag(0 if i % 2 == 0 else 1) for i in range(L)])
     gen = torch.Generator(device="cuda").manual_seed(100 + rank)
-    for step in range(6):
-        if step % 3 == 0:  # steps 0-2: persistent engine; 3-5: one launch per group
+    for step in range(9):
+        if step % 3 == 0:  # steps 0-2: persistent engine; 3-5: one launch per group; 6-8: copy engines
             if step:
                 sync.check()
                 sync.close()
-            sync = MGWFBP(model, comm, LR, plan=mplan, engine_ctas=8, mode="engine" if step == 0 else "launch",
+            sync = MGWFBP(model, comm, LR, plan=mplan, engine_ctas=8, mode=("engine", "launch", "ce")[step // 3],
                           launch_ctas=4)
         w_before = [p.detach().cpu().numpy().copy() for p in model.parameters()]
         x = torch.randn(16, 64, device="cuda", generator=gen)
@@ -156,6 +156,42 @@ def main():
                 failures.append(f"real backward step {step} param {li}")
     sync.check()
     sync.close()
+
+    # memory-ordering stress over real NVLink: 30 engine iterations with NEW
+    # gradients every iteration (every rank regenerates all ranks' gradients
+    # from the shared seeds), both protocols, bit-exact vs torch fp32
+    # rank-order ops after every iteration
+    for protocol in ("chunked", "stream"):
+        comm.set_protocol(protocol)
+        gens = [torch.Generator(device="cuda").manual_seed(500 + r) for r in range(P)]
+        wgen = torch.Generator(device="cuda").manual_seed(499)
+        g_all = [[torch.empty(c, device="cuda") for c in COUNTS] for _ in range(P)]
+        w_dev = [torch.empty(c, device="cuda").uniform_(-1, 1, generator=wgen) for c in COUNTS]
+        want = [w.clone() for w in w_dev]
+        g_dev = [torch.empty(c, device="cuda") for c in COUNTS]
+        dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+        pipe = rt.Pipeline(dp, tr, LR, record_group_times=False, l2_flush_bytes=0, engine_ctas=-1)
+        sc = 1.0 / P
+        for it in range(30):
+            for r in range(P):
+                for g in g_all[r]:
+                    g.uniform_(-1, 1, generator=gens[r])
+            for l in range(len(COUNTS)):
+                g_dev[l].copy_(g_all[rank][l])
+            torch.cuda.synchronize()
+            pipe.run(1)
+            torch.cuda.synchronize()
+            for l in range(len(COUNTS)):
+                red = g_all[0][l] * sc
+                for r in range(1, P):
+                    red = red + g_all[r][l] * sc
+                want[l] = want[l] - LR * red
+                if not torch.equal(w_dev[l], want[l]):
+                    failures.append(f"stress {protocol} iteration {it} layer {l}")
+                    want[l] = w_dev[l].clone()
+        pipe.close()
+        dp.close()
+    comm.set_protocol("chunked")
 
     meas = comm.calibrate([4096 << k for k in range(0, 12, 2)], warmup=2, reps=5)  # <= arena
     meas_e = comm.calibrate_engine([4096 << k for k in range(0, 12, 2)], warmup=1, reps=3)
