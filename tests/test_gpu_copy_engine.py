@@ -101,3 +101,44 @@ def test_copy_engine_calibration_is_monotone():
     model = gs.fit_model(meas)
     assert model.a > 0 and model.b > 0
     comm.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_copy_engine_bf16_bit_exact(P):
+    """bf16 gradients: the copies move bf16 bytes, the reduce widens to fp32,
+    sums in rank order, rounds once to bf16 and applies it to the fp32
+    master weights — the bf16 oracle's semantics."""
+    rng = np.random.default_rng(950 + P)
+    counts = RAGGED
+    g_np = [[pyoracle.f32_to_bf16(rng.uniform(-1, 1, c).astype(np.float32)) for c in counts] for _ in range(P)]
+    w_np = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(P)]
+    offs = [0]
+    for c in counts:
+        offs.append(offs[-1] + ((c + 7) & ~7))  # 16-byte aligned bf16 layers
+    g_dev = []
+    for per in g_np:
+        b = torch.zeros(offs[-1], dtype=torch.bfloat16, device="cuda")
+        for l, a in enumerate(per):
+            b[offs[l]:offs[l] + counts[l]] = torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16)
+        g_dev.append([b[offs[l]:offs[l] + counts[l]] for l in range(len(counts))])
+    w_dev = [[torch.from_numpy(a.copy()).cuda() for a in per] for per in w_np]
+    plan = gs.MergePlan.all_normal(len(counts))
+    comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
+    dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+    assert dp.dtype == rt.BF16
+    ce = rt.CopyEngine(dp, 0.01)
+    s = torch.cuda.current_stream()
+    for _ in range(2):
+        ce.begin(s)
+        for g in reversed(range(dp.n_groups)):
+            ce.mark_ready(g, s)
+        ce.join(s)
+        pyoracle.allreduce_sgd_bf16(g_np, w_np, [int(t) for t in plan.tags], 0.01)
+    torch.cuda.synchronize()
+    ce.check()
+    for r in range(P):
+        for l in range(len(counts)):
+            assert np.array_equal(w_dev[r][l].cpu().numpy(), w_np[r][l]), (r, l)
+    ce.close()
+    dp.close()
+    comm.close()

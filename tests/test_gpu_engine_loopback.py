@@ -335,3 +335,46 @@ def test_ordering_stress_fresh_gradients_every_iteration(P, protocol):
     pipe.close()
     dp.close()
     comm.close()
+
+
+@pytest.mark.parametrize("P,protocol", [(1, "stream"), (1, "chunked"), (2, "chunked"), (2, "stream"),
+                                        (4, "chunked"), (4, "stream")])
+def test_engine_pipeline_bf16_bit_exact(P, protocol):
+    """bf16 gradients through the persistent engine (P = 1: the TMA-fed
+    single-rank engine — `stream` — and the register engine — `chunked`),
+    3 replayed iterations, vs the bf16 oracle (fp32 rank-order sum, one
+    rounding to bf16, fp32 master weights)."""
+    rng = np.random.default_rng(1500 + P)
+    counts = RAGGED
+    t_b = list(rng.uniform(2e-5, 2e-4, len(counts)))
+    tr = gs.trace_from_arrays(counts, t_b, 3e-4)
+    tr.bytes_per_element = 2
+    plan = gs.optimal_plan(tr, gs.AllReduceModel(6e-6, 1 / 600e9))
+    tags = [int(t) for t in plan.tags]
+    g_np = [[pyoracle.f32_to_bf16(rng.uniform(-1, 1, c).astype(np.float32)) for c in counts] for _ in range(P)]
+    w_np = _np(rng, counts, P)
+    g_dev = [[torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16) for a in per] for per in g_np]
+    w_dev = _dev(w_np)
+    if P == 1:
+        comm = rt.Comm(0, 1, 0, 4 * rt.padded_elems(counts))
+        comm.set_protocol(protocol)
+        dp = rt.DevicePlan(comm, g_dev[0], w_dev[0], plan)
+    else:
+        comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
+        comm.set_oneshot_max(256 * 1024)
+        comm.set_ll_max(16 * 1024)
+        comm.set_protocol(protocol)
+        dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+    assert dp.dtype == rt.BF16
+    pipe = rt.Pipeline(dp, tr, LR, record_group_times=False, l2_flush_bytes=32 << 20, engine_ctas=-1)
+    pipe.run(3)
+    for _ in range(3):
+        pyoracle.allreduce_sgd_bf16(g_np, w_np, tags, LR)
+    torch.cuda.synchronize()
+    for r in range(P):
+        for l in range(len(counts)):
+            assert np.array_equal(w_dev[r][l].cpu().numpy(), w_np[r][l]), (r, l)
+    assert not comm.failed()
+    pipe.close()
+    dp.close()
+    comm.close()
