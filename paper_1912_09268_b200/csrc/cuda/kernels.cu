@@ -886,7 +886,9 @@ struct Producer {
   uint64_t cur;       // items per destination (byte q) of the open batch
   uint64_t prev;      // items per destination of the closed batch still in flight
   uint32_t n_cur;     // items in the open batch
-  uint32_t batch;     // items per batch (kCreditBatch unless tuned: 1, 2, 4, 8)
+  uint32_t batch;     // items per batch at full speed (kCreditBatch unless tuned: 1, 2, 4, 8)
+  uint32_t cur_batch; // size of the open batch: ramps 1, 2, 4, ... up to `batch` from each group's
+                      // first item, so a group's first tiles are published after ~3 items, not 2 batches
   uint64_t epoch_hi;  // launch epoch << 32
   uint32_t* done;     // shared [kMaxRanks]: counts published so far (this launch)
 };
@@ -920,8 +922,8 @@ __device__ __forceinline__ uint64_t mask_counts(uint32_t mask) {
 template <int P>
 __device__ __forceinline__ void committed(const RankView& v, Producer<P>& pr, uint32_t mask) {
   pr.cur += mask_counts(mask);
-  if (++pr.n_cur == pr.batch) {
-    switch (pr.batch) {
+  if (++pr.n_cur == pr.cur_batch) {
+    switch (pr.cur_batch) {
       case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
       case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
       case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
@@ -931,6 +933,7 @@ __device__ __forceinline__ void committed(const RankView& v, Producer<P>& pr, ui
     pr.prev = pr.cur;
     pr.cur = 0;
     pr.n_cur = 0;
+    if (pr.cur_batch < pr.batch) pr.cur_batch *= 2;
   }
 }
 
@@ -985,6 +988,7 @@ __device__ __forceinline__ void produce_group(const RankView& v, const Tile* til
   const uint32_t s0 = smem_u32(cx.stages);
   auto item = [&](uint32_t i) { return stream_item<P>(tiles, n_tiles, two_shot, j, ncta, me, i); };
   uint32_t iL = 0, iS = 0, nl = 0, ns = 0;  // next item to load / store; TMA loads / stores issued
+  if (lane == 0 && pr.n_cur == 0) pr.cur_batch = 1;  // ramp the publication batch for this group
   for (;;) {
     // loads ahead, up to the first register-path item
     while (iL < n && (nl < kStages || nl + 2 <= ns + kStages)) {
@@ -1178,8 +1182,10 @@ __device__ __forceinline__ void consume_group(const RankView& v, const Tile* til
   const uint32_t mine = j < n_super ? (n_super - j + ncta - 1) / ncta : 0;
   uint32_t prev_lo = 0, prev_n = 0;
 #pragma unroll 1
-  const uint32_t agb = cs.ag_batch;
-  for (uint32_t b0 = 0; b0 < mine; b0 += agb) {
+  // all-gather publication batches ramp 1, 2, 4, ... up to ag_batch from the
+  // group's first owned super-tile (the peers' first AP is not held back)
+  uint32_t agb = 1;
+  for (uint32_t b0 = 0; b0 < mine; b0 += agb, agb = agb * 2 < cs.ag_batch ? agb * 2 : cs.ag_batch) {
     const uint32_t nb = mine - b0 < agb ? mine - b0 : agb;
     uint32_t owned = 0;
 #pragma unroll 1
@@ -1337,6 +1343,7 @@ __global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid
           pr.epoch_hi = epoch_hi;
           pr.done = s_stream;
           pr.batch = L.credit_batch;
+          pr.cur_batch = 1;
           if ((threadIdx.x & 31) == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
           produce_group<P, T>(v, L.tiles, L.n_tiles, TWO_SHOT, blockIdx.x, gridDim.x,
                               static_cast<uint64_t>(v.rank) * L.slot_stride, pr, cx);
@@ -1356,6 +1363,53 @@ __global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid
                     L.chunk, L.min_chunks, L.ll_pkt, L.mbase};
   run_group<P, T>(TWO_SHOT, v, a, blockIdx.x, gridDim.x, cx);
   cta_exit<P>(v, cx);
+}
+
+// Group descriptors are read-only for the engine's lifetime: every CTA walks
+// the whole table (skipping the groups it has no unit in), so the loads go
+// through the non-coherent L1 path and the table is prefetched into L1 at
+// launch — a skipped group costs an L1 hit, not an L2 round trip (many-group
+// plans: DenseNet-201 has 604 groups).
+__device__ __forceinline__ EngineGroup ld_group(const EngineGroup* g) {
+  static_assert(sizeof(EngineGroup) == 32, "two 16-byte loads");
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(g));
+  const uint4 b = __ldg(reinterpret_cast<const uint4*>(g) + 1);
+  EngineGroup r;
+  r.tile_first = a.x;
+  r.n_tiles = a.y;
+  r.two_shot = a.z;
+  r.ll_pkt = a.w;
+  r.mbase = b.x;
+  r.cta0 = b.y;
+  r.units = b.z;
+  r.pad = b.w;
+  return r;
+}
+
+// Every CTA walks the whole group list and skips the groups it has no unit
+// in; a skip must not cost an L2 round trip (measured: ~0.28 us per skipped
+// group when the descriptor came from global memory — GoogLeNet's 173-group
+// drain took 62 us). The (cta0, units) pairs of the first kSkipTable groups
+// are staged in shared memory at launch; a participating group's full
+// descriptor is then loaded once.
+constexpr uint32_t kSkipTable = 1024;
+
+__device__ __forceinline__ uint2 skip_entry(const EngineGroup& g) {
+  return make_uint2(g.cta0, g.units | ((!g.two_shot && g.ll_pkt != kNoLL) ? 0x80000000u : 0u));
+}
+
+__device__ __forceinline__ void load_skip_table(const EngineLaunch& E, uint2* t) {
+  const uint32_t n = E.G < kSkipTable ? E.G : kSkipTable;
+  for (uint32_t g = threadIdx.x; g < n; g += blockDim.x) t[g] = skip_entry(ld_group(E.groups + g));
+}
+
+// This CTA's unit j in group gi (false: not a participant); ll: a one-shot LL group.
+__device__ __forceinline__ bool my_unit(const EngineLaunch& E, const uint2* t, uint32_t gi, uint32_t& j, bool& ll) {
+  const uint2 e = gi < kSkipTable ? t[gi] : skip_entry(ld_group(E.groups + gi));
+  const uint32_t b = blockIdx.x;
+  j = b >= e.x ? b - e.x : b + gridDim.x - e.x;
+  ll = (e.y >> 31) != 0;
+  return j < (e.y & 0x7fffffffu);
 }
 
 // Off the critical path of a group: while thread 0 waits for the group's
@@ -1424,7 +1478,8 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 
 template <typename T>
 __device__ __noinline__ void engine_p1(const EngineLaunch& E, const RankView& v, uint8_t* dsmem, uint64_t* full,
-                                       uint64_t* empty, uint32_t* s_abort, uint32_t iter, uint32_t slot, size_t row) {
+                                       uint64_t* empty, uint32_t* s_abort, uint32_t iter, uint32_t slot, size_t row,
+                                       const uint2* s_skip) {
   const uint32_t ncta = gridDim.x;
   const uint32_t target = iter + 1;
   const bool producer = threadIdx.x >= kThreads;
@@ -1434,9 +1489,10 @@ __device__ __noinline__ void engine_p1(const EngineLaunch& E, const RankView& v,
     uint32_t n = 0, pe = 0;
     for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
       const uint32_t gi = E.G - 1 - k;
-      const EngineGroup grp = E.groups[gi];
-      const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;
-      if (j >= grp.units) continue;
+      uint32_t j;
+      bool ll;
+      if (!my_unit(E, s_skip, gi, j, ll)) continue;
+      const EngineGroup grp = ld_group(E.groups + gi);
       if (!E.no_wait) {
         const uint32_t* flag = E.ready + gi;
         if (!spin_until(v, [&] { return static_cast<int32_t>(ld_acquire_gpu(flag) - target) >= 0; })) {
@@ -1483,9 +1539,10 @@ __device__ __noinline__ void engine_p1(const EngineLaunch& E, const RankView& v,
   const int tid = static_cast<int>(threadIdx.x);
   for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
     const uint32_t gi = E.G - 1 - k;
-    const EngineGroup grp = E.groups[gi];
-    const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;
-    if (j >= grp.units) continue;
+    uint32_t j;
+    bool ll;
+    if (!my_unit(E, s_skip, gi, j, ll)) continue;
+    const EngineGroup grp = ld_group(E.groups + gi);
     if (tid == 0) {
       if (!E.no_wait && !*reinterpret_cast<volatile uint32_t*>(s_abort)) {
         const uint32_t* flag = E.ready + gi;
@@ -1563,7 +1620,7 @@ __device__ __noinline__ void engine_p1(const EngineLaunch& E, const RankView& v,
 // it has in flight), the data warps walk the same groups consuming them.
 template <int P, typename T>
 __device__ __forceinline__ void engine_stream(const EngineLaunch& E, const RankView& v, CtaCtx& cx, uint32_t iter,
-                                              uint32_t slot, size_t row, uint32_t* s_stream) {
+                                              uint32_t slot, size_t row, uint32_t* s_stream, const uint2* s_skip) {
   const uint32_t ncta = gridDim.x;
   const uint64_t epoch_hi = static_cast<uint64_t>(cx.epoch) << 32;
   const uint32_t target = iter + 1;
@@ -1573,12 +1630,14 @@ __device__ __forceinline__ void engine_stream(const EngineLaunch& E, const RankV
     pr.epoch_hi = epoch_hi;
     pr.done = s_stream;
     pr.batch = E.credit_batch;
+    pr.cur_batch = 1;
     const uint64_t my_slot = static_cast<uint64_t>(v.rank) * E.slot_stride;
     for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
       const uint32_t gi = E.G - 1 - k;
-      const EngineGroup grp = E.groups[gi];
-      const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;
-      if (j >= grp.units || (!grp.two_shot && grp.ll_pkt != kNoLL)) continue;
+      uint32_t j;
+      bool ll;
+      if (!my_unit(E, s_skip, gi, j, ll) || ll) continue;
+      const EngineGroup grp = ld_group(E.groups + gi);
       uint32_t abort = 0;
       if (lane == 0) {
         abort = *reinterpret_cast<volatile uint32_t*>(cx.s_abort);
@@ -1604,9 +1663,10 @@ __device__ __forceinline__ void engine_stream(const EngineLaunch& E, const RankV
   Consumer cs{0, 0, 0, 0, 0, E.ag_batch, epoch_hi, s_stream + kMaxRanks};
   for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
     const uint32_t gi = E.G - 1 - k;
-    const EngineGroup grp = E.groups[gi];
-    const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;
-    if (j >= grp.units) continue;
+    uint32_t j;
+    bool ll;
+    if (!my_unit(E, s_skip, gi, j, ll)) continue;
+    const EngineGroup grp = ld_group(E.groups + gi);
     if (threadIdx.x >= 32 && threadIdx.x < 64) warm_group<P>(v, E.tiles, grp, j, E.lr);
     if (threadIdx.x == 0) {
       if (!E.no_wait && !cx.abort) {
@@ -1650,6 +1710,8 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
   if (threadIdx.x < 3 * kMaxRanks) s_stream[threadIdx.x] = 0u;
   const RankView& v = E.views[blockIdx.y];
   if (threadIdx.x == 0) s_iter = ld_volatile_u32(E.pipe + 1);
+  __shared__ uint2 s_skip[kSkipTable];
+  load_skip_table(E, s_skip);  // (published by cta_ctx_init's __syncthreads)
   // Entry barrier inside (runs while the compute stream replays the forward
   // pass): every peer has finished every older launch before any push.
   CtaCtx cx;
@@ -1659,7 +1721,7 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
   const uint32_t slot = blockIdx.y * gridDim.x + blockIdx.x;      // stamp column
   const size_t row = static_cast<size_t>(gridDim.x) * gridDim.y;  // stamp row width
   if constexpr (P > 1 && STREAM) {
-    engine_stream<P, T>(E, v, cx, iter, slot, row, s_stream);
+    engine_stream<P, T>(E, v, cx, iter, slot, row, s_stream, s_skip);
     __syncthreads();
   }
   if constexpr (P == 1 && STREAM) {
@@ -1672,14 +1734,15 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    engine_p1<T>(E, v, dsmem, bars, p1_empty, &s_abort, iter, slot, row);
+    engine_p1<T>(E, v, dsmem, bars, p1_empty, &s_abort, iter, slot, row, s_skip);
     __syncthreads();
   }
   for (uint32_t k = 0; k + E.g_lo < E.G && !STREAM; ++k) {
     const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
-    const EngineGroup grp = E.groups[gi];
-    const uint32_t j = (blockIdx.x + ncta - grp.cta0) % ncta;  // this CTA's index inside the group
-    if (j >= grp.units) continue;  // same on every rank: no barrier to skip
+    uint32_t j;  // this CTA's index inside the group
+    bool ll;
+    if (!my_unit(E, s_skip, gi, j, ll)) continue;  // same on every rank: no barrier to skip
+    const EngineGroup grp = ld_group(E.groups + gi);
     if (threadIdx.x >= 32 && threadIdx.x < 64) warm_group<P>(v, E.tiles, grp, j, E.lr);
     if (threadIdx.x == 0) {
       // group gi is ready for iteration `iter` once its flag reached iter+1
@@ -1889,16 +1952,21 @@ __global__ void replay_kernel(unsigned long long* clock, unsigned long long dead
   }
 }
 
-// L2 eviction between iterations: streaming stores over a buffer larger
-// than L2 from a FEW CTAs, so the flush never occupies every SM (a full-grid
-// memset delayed the concurrently launched one-thread replay kernel by the
-// whole flush, measured ~40 us per iteration).
+// L2 eviction between iterations: READS of a buffer larger than L2 from a
+// FEW CTAs, so the flush never occupies every SM (a full-grid memset delayed
+// the concurrently launched one-thread replay kernel by the whole flush,
+// measured ~40 us per iteration). Reads, not stores: a store flush leaves up
+// to the whole L2 DIRTY, and the next kernel would pay its write-back (~126
+// MB at HBM speed, ~20 us: a third of a small plan's drain); a read flush
+// writes back the previous kernel's dirty lines itself and leaves clean ones.
 __global__ void __launch_bounds__(512) l2_flush_kernel(float4* buf, size_t n_vec, uint32_t salt) {
-  const float4 v = make_float4(__uint_as_float(salt), 0.0f, 0.0f, 0.0f);
+  float acc = 0.0f;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n_vec;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    __stcs(buf + i, v);
+    const float4 x = __ldcg(buf + i);
+    acc += x.x + x.y + x.z + x.w;
   }
+  if (__float_as_uint(acc) == salt) buf[0].y = acc;  // (keeps the loads; practically never taken)
 }
 
 constexpr size_t kSmemBytes =

@@ -1047,6 +1047,7 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
     ck(cudaMemset(pipe->d_clock, 0, 2 * sizeof(unsigned long long)), "memset(clock)");
     if (l2_flush_bytes > 0) {
       ck(cudaMalloc(&pipe->flush_buf, l2_flush_bytes), "cudaMalloc(l2 flush)");
+      ck(cudaMemset(pipe->flush_buf, 0, l2_flush_bytes), "memset(l2 flush)");  // the flush reads it
       pipe->flush_bytes = l2_flush_bytes;
     }
 
@@ -1517,7 +1518,7 @@ void ce_worker(mgw_ce* e) {
       std::unique_lock<std::mutex> lk(e->mu);
       e->cv.wait(lk, [&] { return e->stop.load() || e->active.load() ||
                                   e->tail.load() != e->head.load(std::memory_order_acquire); });
-      if (e->stop.load() && e->tail.load() == e->head.load()) return;
+      if (e->stop.load()) return;  // destroy: copies still queued are moot
     }
     // spin while the iteration is open: a hook's append is picked up at once
     while (!e->stop.load(std::memory_order_relaxed)) {

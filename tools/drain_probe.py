@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--P", type=int, default=1)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--flush-mib", type=int, default=256)
+    ap.add_argument("--stamps", action="store_true", help="per-group device stamps of the last drain")
     args = ap.parse_args()
     tr = gs.load_trace(os.path.join(ROOT, "traces", f"{args.trace}.json"))
     calib = os.path.join(ROOT, "profiles", "calib", f"calib_{args.trace}_P{args.P}.csv")
@@ -44,8 +45,22 @@ def main():
     else:
         comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
         dp = rt.DevicePlan(comm, grads, weights, plan)
-    pipe = rt.Pipeline(dp, tr, 0.01, l2_flush_bytes=args.flush_mib << 20, engine_ctas=-1)
+    pipe = rt.Pipeline(dp, tr, 0.01, l2_flush_bytes=args.flush_mib << 20, engine_ctas=-1,
+                       record_group_times=args.stamps)
     ms = pipe.drain(args.iters)
+    if args.stamps:
+        import ctypes as C
+
+        from paper_1912_09268_b200 import _lib
+
+        G = dp.n_groups
+        st = (C.c_uint64 * (2 * G))()
+        gs.check(_lib.mgw_pipeline_stamps(pipe.handle, st))
+        t0 = min(st[2 * g] for g in range(G) if st[2 * g])
+        rows = [((st[2 * g] - t0) / 1e3, (st[2 * g + 1] - t0) / 1e3, dp.group_span(g)[2]) for g in range(G)]
+        for g in list(range(G - 1, G - 12, -1)) + list(range(min(10, G) - 1, -1, -1)):
+            print(f"group {g:4d} bytes {rows[g][2]:10d} start {rows[g][0]:8.2f} us end {rows[g][1]:8.2f} us")
+        print("span us", max(r[1] for r in rows), "sum of group durations us", sum(r[1] - r[0] for r in rows))
     S = sum(dp.group_span(g)[2] for g in range(dp.n_groups))
     hbm = 3 * S * P
     print(json.dumps({"trace": args.trace, "P": P, "groups": dp.n_groups, "grad_bytes_per_rank": S,
