@@ -77,6 +77,8 @@ def parse_args():
     ap.add_argument("--protocol", default="chunked", choices=["chunked", "stream"],
                     help="fused all-reduce protocol at N > 1: chunked (per-chunk cross-rank barrier) or stream "
                          "(per-tile delivery counts, producer/consumer decoupled)")
+    ap.add_argument("--stream-batches", default="",
+                    help="CREDIT,AG: streamed-protocol publication batches (default: the library's 8,4)")
     ap.add_argument("--engine-ctas", type=int, default=-1,
                     help="-1: persistent comm engine, one CTA per SM; >0: that many CTAs; "
                          "0: one fused kernel launch per group")
@@ -473,6 +475,8 @@ def main():
         comm.set_oneshot_max(args.oneshot_max)
     if N > 1:
         comm.set_protocol(args.protocol)  # (P = 1 always runs the TMA-fed single-rank engine)
+        if args.stream_batches:
+            comm.set_stream_batches(*(int(x) for x in args.stream_batches.split(",")))
 
     # ---- N1: on-box calibration of the fused engine kernel at this N
     sizes = calibration_sizes(total_bytes, 4 * padded)
