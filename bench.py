@@ -56,8 +56,8 @@ L2_BYTES = 126 << 20
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)   # >= 200 timed iterations after 20 warm-up
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="mgwfbp", choices=["mgwfbp", "reference"])
     ap.add_argument("--trace", default="bert_large")
     ap.add_argument("--plan-source", default="committed", choices=["committed", "onbox"],
@@ -366,8 +366,10 @@ def run_reference(args):
     a, b, fit_kind = ref_fit(os.path.join(ROOT, calib))
     tags, plan_kind = ref_plan(tr, a, b, bpe)
     threads = os.cpu_count() or 1
-    cpu_pipeline_sample(tr, tags, N, args.lr, threads, 0.0, iters_cap=max(1, args.warmup))
-    times = cpu_pipeline_sample(tr, tags, N, args.lr, threads, 1e9, iters_cap=args.steps)
+    # bounded sample: at most --steps iterations and about a minute of CPU work
+    # (N = 8 BERT-large reduces 8 x 1.34 GB per iteration on the host)
+    cpu_pipeline_sample(tr, tags, N, args.lr, threads, 0.0, iters_cap=max(1, min(args.warmup, 3)))
+    times = cpu_pipeline_sample(tr, tags, N, args.lr, threads, 60.0, iters_cap=args.steps)
     total = sum(times)
     value = N * len(times) / total
     ms = total / len(times) * 1e3
@@ -577,6 +579,11 @@ def main():
             strat[name]["device_tail_us"] = D.max_over_ranks(tl["tail_us"], dev)
             strat[name]["device_replay_ms"] = tl["replay_us"] / 1e3
     compute_ms = (trace.forward_time + sum(l.backward_time for l in trace.layers)) * 1e3
+    # iteration lower bound: max(compute, t_f + t_b of
+    # the first layer the backward finishes + every group at its bus roofline)
+    gb_plan = [dplans["mgwfbp"].group_span(g)[2] for g in range(dplans["mgwfbp"].n_groups)]
+    roof_comm_s = sum(2 * (N - 1) / N * b for b in gb_plan) / (NVLINK_GBS * 1e9)
+    bound_ms = max(compute_ms, (trace.forward_time + trace.layers[-1].backward_time + roof_comm_s) * 1e3)
 
     # ---- e2e through the public API with host buffers
     # Each step: the step's gradients H2D from pinned host memory (captured in
@@ -693,6 +700,8 @@ def main():
                      + "; backward replayed from B200-measured per-tensor t_b"),
             "config": cfg,
             "exposed_comm_ms": ms_step - cfg["compute_ms"],
+            "iteration_bound": {"ms": bound_ms, "frac": bound_ms / ms_step,
+                                "formula": "max(t_f + sum t_b, t_f + t_b[last layer] + sum_g 2(P-1)/P*S_g / 900 GB/s)"},
             "gpu": {"comm": ("persistent engine, %s CTAs" % ("1/SM" if args.engine_ctas < 0 else args.engine_ctas))
                             if args.engine_ctas else "one fused kernel launch per group",
                     "algo": args.algo, "tuning": comm.tuning(), "ipc_ranks_mapped": peers,
