@@ -294,6 +294,9 @@ int mgw_pipeline_drain(mgw_pipeline* pipe, int iters, float* ms_out);
  * (start, end) %globaltimer stamps of every group, 2*G values in group
  * order (zero for groups without tiles). */
 int mgw_pipeline_stamps(mgw_pipeline* pipe, uint64_t* stamps_2g);
+/* Debug: the raw per-(group, CTA) (start, end) %globaltimer stamps of the
+ * last engine launch, [G][cols][2] (cols = CTAs of all emulated ranks). */
+int mgw_pipeline_stamps_raw(mgw_pipeline* pipe, uint64_t* out, size_t cap, size_t* cols_out);
 
 /* Host-driven persistent comm engine for a REAL backward (SURVEY §8f row
  * 2; paper Algorithm 2 with the daemon thread on the GPU): instead of the

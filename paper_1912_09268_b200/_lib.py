@@ -130,6 +130,7 @@ mgw_pipeline_group_times = _proto("mgw_pipeline_group_times", [vp, f32p])
 mgw_pipeline_stream = _proto("mgw_pipeline_stream", [vp, C.POINTER(vp)])
 mgw_pipeline_debug = _proto("mgw_pipeline_debug", [vp, C.POINTER(C.c_uint32), u64p])
 mgw_pipeline_stamps = _proto("mgw_pipeline_stamps", [vp, u64p])
+mgw_pipeline_stamps_raw = _proto("mgw_pipeline_stamps_raw", [vp, u64p, C.c_size_t, C.POINTER(C.c_size_t)])
 mgw_pipeline_drain = _proto("mgw_pipeline_drain", [vp, C.c_int, f32p])
 mgw_engine_create = _proto("mgw_engine_create", [vp, C.c_float, C.c_int, C.c_int, C.c_int, C.POINTER(vp)])
 mgw_engine_begin = _proto("mgw_engine_begin", [vp, vp])

@@ -1386,31 +1386,15 @@ __device__ __forceinline__ EngineGroup ld_group(const EngineGroup* g) {
   return r;
 }
 
-// Every CTA walks the whole group list and skips the groups it has no unit
-// in; a skip must not cost an L2 round trip (measured: ~0.28 us per skipped
-// group when the descriptor came from global memory — GoogLeNet's 173-group
-// drain took 62 us). The (cta0, units) pairs of the first kSkipTable groups
-// are staged in shared memory at launch; a participating group's full
-// descriptor is then loaded once.
-constexpr uint32_t kSkipTable = 1024;
-
-__device__ __forceinline__ uint2 skip_entry(const EngineGroup& g) {
-  return make_uint2(g.cta0, g.units | ((!g.two_shot && g.ll_pkt != kNoLL) ? 0x80000000u : 0u));
-}
-
-__device__ __forceinline__ void load_skip_table(const EngineLaunch& E, uint2* t) {
-  const uint32_t n = E.G < kSkipTable ? E.G : kSkipTable;
-  for (uint32_t g = threadIdx.x; g < n; g += blockDim.x) t[g] = skip_entry(ld_group(E.groups + g));
-}
-
-// This CTA's unit j in group gi (false: not a participant); ll: a one-shot LL group.
-__device__ __forceinline__ bool my_unit(const EngineLaunch& E, const uint2* t, uint32_t gi, uint32_t& j, bool& ll) {
-  const uint2 e = gi < kSkipTable ? t[gi] : skip_entry(ld_group(E.groups + gi));
+// CTA b walks only its own schedule (host-built: the groups it has a unit
+// in, FIFO order); j = its unit index inside the group (groups rotate over
+// the CTAs from cta0).
+__device__ __forceinline__ uint32_t unit_of(const EngineGroup& g) {
   const uint32_t b = blockIdx.x;
-  j = b >= e.x ? b - e.x : b + gridDim.x - e.x;
-  ll = (e.y >> 31) != 0;
-  return j < (e.y & 0x7fffffffu);
+  return b >= g.cta0 ? b - g.cta0 : b + gridDim.x - g.cta0;
 }
+
+__device__ __forceinline__ bool is_ll_oneshot(const EngineGroup& g) { return !g.two_shot && g.ll_pkt != kNoLL; }
 
 // Off the critical path of a group: while thread 0 waits for the group's
 // ready flag, warp 1 warms what the first tile of this CTA needs — its
@@ -1478,8 +1462,7 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 
 template <typename T>
 __device__ __noinline__ void engine_p1(const EngineLaunch& E, const RankView& v, uint8_t* dsmem, uint64_t* full,
-                                       uint64_t* empty, uint32_t* s_abort, uint32_t iter, uint32_t slot, size_t row,
-                                       const uint2* s_skip) {
+                                       uint64_t* empty, uint32_t* s_abort, uint32_t iter, uint32_t slot, size_t row) {
   const uint32_t ncta = gridDim.x;
   const uint32_t target = iter + 1;
   const bool producer = threadIdx.x >= kThreads;
@@ -1487,12 +1470,12 @@ __device__ __noinline__ void engine_p1(const EngineLaunch& E, const RankView& v,
   if (producer) {
     if ((threadIdx.x & 31) != 0) return;
     uint32_t n = 0, pe = 0;
-    for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
-      const uint32_t gi = E.G - 1 - k;
-      uint32_t j;
-      bool ll;
-      if (!my_unit(E, s_skip, gi, j, ll)) continue;
+    const uint32_t e_end = E.sched_off[blockIdx.x + 1];
+    for (uint32_t e = E.sched_off[blockIdx.x]; e < e_end; ++e) {
+      const uint32_t gi = E.sched[e];
+      if (gi < E.g_lo) break;  // FIFO order: the caller's tail groups come last
       const EngineGroup grp = ld_group(E.groups + gi);
+      const uint32_t j = unit_of(grp);
       if (!E.no_wait) {
         const uint32_t* flag = E.ready + gi;
         if (!spin_until(v, [&] { return static_cast<int32_t>(ld_acquire_gpu(flag) - target) >= 0; })) {
@@ -1501,7 +1484,10 @@ __device__ __noinline__ void engine_p1(const EngineLaunch& E, const RankView& v,
         }
       }
       if (*reinterpret_cast<volatile uint32_t*>(s_abort)) return;
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // gradients written by generic stores
+      // gradients written by generic-proxy stores and published by the ready
+      // flag just acquired: visible to the TMA (a drain — every group ready at
+      // launch — has them ordered by the kernel boundary)
+      if (!E.no_wait) asm volatile("fence.proxy.async.global;" ::: "memory");
       const Tile* tiles = E.tiles + grp.tile_first;
       for (uint32_t ti = j; ti < grp.n_tiles; ti += ncta) {
         const Tile t = tiles[ti];
@@ -1537,12 +1523,12 @@ __device__ __noinline__ void engine_p1(const EngineLaunch& E, const RankView& v,
   }
   uint32_t m = 0, pf = 0;
   const int tid = static_cast<int>(threadIdx.x);
-  for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
-    const uint32_t gi = E.G - 1 - k;
-    uint32_t j;
-    bool ll;
-    if (!my_unit(E, s_skip, gi, j, ll)) continue;
+  const uint32_t e_end = E.sched_off[blockIdx.x + 1];
+  for (uint32_t e = E.sched_off[blockIdx.x]; e < e_end; ++e) {
+    const uint32_t gi = E.sched[e];
+    if (gi < E.g_lo) break;  // FIFO order: the caller's tail groups come last
     const EngineGroup grp = ld_group(E.groups + gi);
+    const uint32_t j = unit_of(grp);
     if (tid == 0) {
       if (!E.no_wait && !*reinterpret_cast<volatile uint32_t*>(s_abort)) {
         const uint32_t* flag = E.ready + gi;
@@ -1620,7 +1606,7 @@ __device__ __noinline__ void engine_p1(const EngineLaunch& E, const RankView& v,
 // it has in flight), the data warps walk the same groups consuming them.
 template <int P, typename T>
 __device__ __forceinline__ void engine_stream(const EngineLaunch& E, const RankView& v, CtaCtx& cx, uint32_t iter,
-                                              uint32_t slot, size_t row, uint32_t* s_stream, const uint2* s_skip) {
+                                              uint32_t slot, size_t row, uint32_t* s_stream) {
   const uint32_t ncta = gridDim.x;
   const uint64_t epoch_hi = static_cast<uint64_t>(cx.epoch) << 32;
   const uint32_t target = iter + 1;
@@ -1632,12 +1618,13 @@ __device__ __forceinline__ void engine_stream(const EngineLaunch& E, const RankV
     pr.batch = E.credit_batch;
     pr.cur_batch = 1;
     const uint64_t my_slot = static_cast<uint64_t>(v.rank) * E.slot_stride;
-    for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
-      const uint32_t gi = E.G - 1 - k;
-      uint32_t j;
-      bool ll;
-      if (!my_unit(E, s_skip, gi, j, ll) || ll) continue;
+    const uint32_t e_end = E.sched_off[blockIdx.x + 1];
+    for (uint32_t e = E.sched_off[blockIdx.x]; e < e_end; ++e) {
+      const uint32_t gi = E.sched[e];
+      if (gi < E.g_lo) break;  // FIFO order: the caller's tail groups come last
       const EngineGroup grp = ld_group(E.groups + gi);
+      if (is_ll_oneshot(grp)) continue;  // LL groups: the data warps alone
+      const uint32_t j = unit_of(grp);
       uint32_t abort = 0;
       if (lane == 0) {
         abort = *reinterpret_cast<volatile uint32_t*>(cx.s_abort);
@@ -1651,7 +1638,8 @@ __device__ __forceinline__ void engine_stream(const EngineLaunch& E, const RankV
           }
         }
         // gradients written by generic-proxy stores: visible to the TMA
-        asm volatile("fence.proxy.async.global;" ::: "memory");
+        // (drain: ordered by the kernel boundary)
+        if (!E.no_wait) asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       if (__shfl_sync(0xffffffffu, abort, 0)) break;
       produce_group<P, T>(v, E.tiles + grp.tile_first, grp.n_tiles, grp.two_shot != 0, j, ncta, my_slot, pr, cx);
@@ -1661,12 +1649,12 @@ __device__ __forceinline__ void engine_stream(const EngineLaunch& E, const RankV
     return;
   }
   Consumer cs{0, 0, 0, 0, 0, E.ag_batch, epoch_hi, s_stream + kMaxRanks};
-  for (uint32_t k = 0; k + E.g_lo < E.G; ++k) {
-    const uint32_t gi = E.G - 1 - k;
-    uint32_t j;
-    bool ll;
-    if (!my_unit(E, s_skip, gi, j, ll)) continue;
+  const uint32_t e_end = E.sched_off[blockIdx.x + 1];
+  for (uint32_t e = E.sched_off[blockIdx.x]; e < e_end; ++e) {
+    const uint32_t gi = E.sched[e];
+    if (gi < E.g_lo) break;  // FIFO order: the caller's tail groups come last
     const EngineGroup grp = ld_group(E.groups + gi);
+    const uint32_t j = unit_of(grp);
     if (threadIdx.x >= 32 && threadIdx.x < 64) warm_group<P>(v, E.tiles, grp, j, E.lr);
     if (threadIdx.x == 0) {
       if (!E.no_wait && !cx.abort) {
@@ -1710,8 +1698,6 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
   if (threadIdx.x < 3 * kMaxRanks) s_stream[threadIdx.x] = 0u;
   const RankView& v = E.views[blockIdx.y];
   if (threadIdx.x == 0) s_iter = ld_volatile_u32(E.pipe + 1);
-  __shared__ uint2 s_skip[kSkipTable];
-  load_skip_table(E, s_skip);  // (published by cta_ctx_init's __syncthreads)
   // Entry barrier inside (runs while the compute stream replays the forward
   // pass): every peer has finished every older launch before any push.
   CtaCtx cx;
@@ -1721,7 +1707,7 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
   const uint32_t slot = blockIdx.y * gridDim.x + blockIdx.x;      // stamp column
   const size_t row = static_cast<size_t>(gridDim.x) * gridDim.y;  // stamp row width
   if constexpr (P > 1 && STREAM) {
-    engine_stream<P, T>(E, v, cx, iter, slot, row, s_stream, s_skip);
+    engine_stream<P, T>(E, v, cx, iter, slot, row, s_stream);
     __syncthreads();
   }
   if constexpr (P == 1 && STREAM) {
@@ -1734,15 +1720,17 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    engine_p1<T>(E, v, dsmem, bars, p1_empty, &s_abort, iter, slot, row, s_skip);
+    engine_p1<T>(E, v, dsmem, bars, p1_empty, &s_abort, iter, slot, row);
     __syncthreads();
   }
-  for (uint32_t k = 0; k + E.g_lo < E.G && !STREAM; ++k) {
-    const uint32_t gi = E.G - 1 - k;  // backward order: FIFO like timeline.hpp:133-154
-    uint32_t j;  // this CTA's index inside the group
-    bool ll;
-    if (!my_unit(E, s_skip, gi, j, ll)) continue;  // same on every rank: no barrier to skip
+  // this CTA's groups in backward order: FIFO like timeline.hpp:133-154
+  // (the schedule is identical on every rank: no barrier to skip)
+  const uint32_t e_end = STREAM ? 0u : E.sched_off[blockIdx.x + 1];
+  for (uint32_t e = STREAM ? 0u : E.sched_off[blockIdx.x]; e < e_end; ++e) {
+    const uint32_t gi = E.sched[e];
+    if (gi < E.g_lo) break;
     const EngineGroup grp = ld_group(E.groups + gi);
+    const uint32_t j = unit_of(grp);  // this CTA's index inside the group
     if (threadIdx.x >= 32 && threadIdx.x < 64) warm_group<P>(v, E.tiles, grp, j, E.lr);
     if (threadIdx.x == 0) {
       // group gi is ready for iteration `iter` once its flag reached iter+1

@@ -130,6 +130,8 @@ struct EngineLaunch {
   RankView views[kMaxRanks];     // [0] for a real rank; [r] per emulated rank (loopback, blockIdx.y)
   const Tile* tiles;
   const EngineGroup* groups;     // ascending group index
+  const uint32_t* sched;         // CTA b's participating groups in FIFO order: sched[sched_off[b] ..
+  const uint32_t* sched_off;     //   sched_off[b+1]) (host-built; identical on every rank)
   uint32_t G;
   uint32_t g_lo;                 // the engine runs groups [g_lo, G) (the rest: caller's tail launches)
   int nranks;

@@ -61,6 +61,17 @@ def main():
         for g in list(range(G - 1, G - 12, -1)) + list(range(min(10, G) - 1, -1, -1)):
             print(f"group {g:4d} bytes {rows[g][2]:10d} start {rows[g][0]:8.2f} us end {rows[g][1]:8.2f} us")
         print("span us", max(r[1] for r in rows), "sum of group durations us", sum(r[1] - r[0] for r in rows))
+        cap = G * 4096 * 2
+        raw = (C.c_uint64 * cap)()
+        cols = C.c_size_t()
+        gs.check(_lib.mgw_pipeline_stamps_raw(pipe.handle, raw, cap, C.byref(cols)))
+        nc = cols.value
+        # the CTA that ran the FIFO-last group: its own timeline
+        for cta in sorted({c for g in range(G) for c in range(nc) if raw[(g * nc + c) * 2]}, key=lambda c: -max(
+                (raw[(g * nc + c) * 2 + 1] for g in range(G) if raw[(g * nc + c) * 2]), default=0))[:2]:
+            seq = sorted((raw[(g * nc + cta) * 2] - t0, raw[(g * nc + cta) * 2 + 1] - t0, g) for g in range(G)
+                         if raw[(g * nc + cta) * 2])
+            print(f"CTA {cta}: " + "  ".join(f"g{g}[{a / 1e3:.2f}-{b / 1e3:.2f}]" for a, b, g in seq))
     S = sum(dp.group_span(g)[2] for g in range(dp.n_groups))
     hbm = 3 * S * P
     print(json.dumps({"trace": args.trace, "P": P, "groups": dp.n_groups, "grad_bytes_per_rank": S,
