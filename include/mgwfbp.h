@@ -343,7 +343,10 @@ int mgw_ce_begin(mgw_ce* ce, void* after_stream);
 int mgw_ce_mark_ready(mgw_ce* ce, int group, void* stream);
 int mgw_ce_join(mgw_ce* ce, void* stream);
 /* Groups [0, n_tail) (the last the backward makes ready) are left to the
- * caller (e.g. mgw_group_allreduce after the backward): no copy, no reduce. */
+ * caller (e.g. mgw_group_allreduce after the backward): no copy, no reduce.
+ * Launch those fused kernels AFTER mgw_ce_join on the same stream: a fused
+ * launch pairs its CTAs with the peers' and may hold every SM while waiting,
+ * which must not starve a peer's signal kernel. */
 int mgw_ce_set_tail(mgw_ce* ce, int n_tail);
 /* Synchronise and report a timed-out wait as an error. */
 int mgw_ce_check(mgw_ce* ce);

@@ -25,7 +25,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-from typing import List, Optional
+from typing import Callable, List, Optional
 
 import torch
 
@@ -184,11 +184,15 @@ class MGWFBP:
         if self.mode == "ce":
             for g in missing:  # parameters that got no gradient this iteration
                 self.ce.mark_ready(g, torch.cuda.current_stream())
-            # the tail groups' fused launches first: they run next to the
-            # copy-engine reduce (NVLink-bound vs HBM-bound)
+            # the copy-engine reduce first, THEN the tail groups' fused launches:
+            # a fused launch pairs its CTAs with the peers' and may hold every
+            # SM while it waits, so it must never be able to run ahead of a
+            # peer's signal kernel (deadlock: rank r's reduce spins for rank
+            # q's signal while rank q's SMs are held by its tail kernel waiting
+            # for rank r's tail CTAs, measured at N = 4)
+            self.ce.join(torch.cuda.current_stream())
             for g in reversed(range(self.tail)):
                 check(_lib.mgw_group_allreduce(self.dplan.handle, g, self.lr, 1, ALGO[self.algo], stream))
-            self.ce.join(torch.cuda.current_stream())
         elif self.mode == "launch":
             for g in range(self._next, self.tail - 1, -1):  # the rest in order (incl. groups without gradients)
                 self._launch(g, torch.cuda.current_stream())
@@ -235,3 +239,63 @@ class MGWFBP:
             check(_lib.mgw_pipeline_destroy(self.handle))
             self.handle = None
         self.dplan.close()
+
+
+def autotune_plan(model: torch.nn.Module, comm: Comm, lr: float, trace, step: Callable[[], None],
+                  params: Optional[List[torch.nn.Parameter]] = None, scales=(1, 3, 10, 30, 100, 300),
+                  iters: int = 8, warmup: int = 3, **kw):
+    """In-situ calibration of the merge plan for a real training loop.
+
+    The planner's cost model is the reference's `a + b*M` (comm_model.hpp:
+    194-199); its `(a, b)` come from an isolated copy-engine sweep
+    (`Comm.calibrate_ce`). In a host-bound training loop a group also costs
+    host time on the critical path, which that sweep cannot see, so the
+    effective `a` is larger. This runs the loop for `iters` steps under the
+    reference `optimal_plan` (planner.hpp:63-98) with `a` scaled by each of
+    `scales` (distinct plans only), times each on the device (max over
+    ranks, so every rank picks the same plan) and returns
+    (best plan, {scale: (groups, ms)}). `step()` must run one iteration with
+    the MGWFBP object passed to it via `autotune_plan.current` (begin, forward,
+    backward, end). The steps train the model (SGD is applied)."""
+    import statistics
+
+    import torch.distributed as dist
+
+    from .gradsched import AllReduceModel, CommMeasurement, fit_model, optimal_plan
+
+    params = list(params) if params is not None else [p for p in model.parameters() if p.requires_grad]
+    counts = [p.numel() for p in params]
+    sizes = [4096 << k for k in range(0, 20, 2) if (4096 << k) <= 4 * padded_elems(counts)]
+    meas = comm.calibrate_ce(sizes, warmup=2, reps=5)
+    t = torch.tensor([m.time_sec for m in meas], dtype=torch.float64, device=params[0].device)
+    if dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    base = fit_model([CommMeasurement(m.size_bytes, float(v)) for m, v in zip(meas, t.tolist())])
+    results, seen, best = {}, set(), None
+    for sc in scales:
+        plan = optimal_plan(trace, AllReduceModel(base.a * sc, base.b))
+        key = tuple(int(x) for x in plan.tags)
+        if key in seen:
+            continue
+        seen.add(key)
+        sync = MGWFBP(model, comm, lr, plan=plan, params=params, **kw)
+        autotune_plan.current = sync
+        for _ in range(warmup):
+            step()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
+        evs[0].record()
+        for i in range(iters):
+            step()
+            evs[i + 1].record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(iters))],
+                          dtype=torch.float64, device=params[0].device)
+        if dist.is_initialized():
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        sync.check()
+        sync.close()
+        results[sc] = (len(plan.groups()), float(ms.item()))
+        if best is None or results[sc][1] < best[1]:
+            best = (plan, results[sc][1])
+    autotune_plan.current = None
+    return best[0], results

@@ -66,9 +66,9 @@ def test_copy_engine_bit_exact(P, merged, tail):
         ce.begin(s)
         for g in reversed(range(dp.n_groups)):
             ce.mark_ready(g, s)
-        for g in reversed(range(tail)):
-            dp.group_allreduce(g, 0.01, rt.SGD, "auto", s)
         ce.join(s)
+        for g in reversed(range(tail)):  # the tail after the join (see mgw_ce_set_tail)
+            dp.group_allreduce(g, 0.01, rt.SGD, "auto", s)
         pyoracle.allreduce_sgd(g_np, w_np, tags, 0.01)
     torch.cuda.synchronize()
     ce.check()

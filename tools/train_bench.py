@@ -132,6 +132,19 @@ def main():
                 plan = gs.optimal_plan(trace, model_ab)
                 D.agree_plan(plan.tags)
                 extra = {"a_us": model_ab.a * 1e6, "b_ps_per_byte": model_ab.b * 1e12}
+            elif base == "tuned":  # in-situ calibration of the plan (ddp.autotune_plan)
+                from paper_1912_09268_b200.ddp import autotune_plan
+
+                def tstep():
+                    s_ = autotune_plan.current
+                    s_.begin()
+                    fwd_bwd(model)
+                    s_.end()
+
+                plan, tune = autotune_plan(model, comm, args.lr, trace, tstep, params=params,
+                                           engine_ctas=args.engine_ctas, tail_groups=args.tail_groups,
+                                           mode=args.mode, launch_ctas=args.launch_ctas)
+                extra = {"autotune": {str(k): v for k, v in tune.items()}}
             elif base == "merged":  # every layer in one group, in this mode
                 plan, extra = gs.MergePlan.all_merged(len(params)), {}
             elif strat == "wfbp":
