@@ -344,10 +344,16 @@ int mgw_ce_mark_ready(mgw_ce* ce, int group, void* stream);
 int mgw_ce_join(mgw_ce* ce, void* stream);
 /* Groups [0, n_tail) (the last the backward makes ready) are left to the
  * caller (e.g. mgw_group_allreduce after the backward): no copy, no reduce.
- * Launch those fused kernels AFTER mgw_ce_join on the same stream: a fused
- * launch pairs its CTAs with the peers' and may hold every SM while waiting,
- * which must not starve a peer's signal kernel. */
+ * Launch those fused kernels after mgw_ce_join on the same stream unless
+ * mgw_ce_signals_without_sm: a fused launch pairs its CTAs with the peers'
+ * and may hold every SM while waiting, which must not starve a peer's
+ * signal kernel. */
 int mgw_ce_set_tail(mgw_ce* ce, int n_tail);
+/* 1 in *out when "iteration delivered" is signalled with stream memory
+ * operations (cuStreamWriteValue64: no SM needed). Then the tail groups'
+ * fused launches may go BEFORE mgw_ce_join and overlap the reduce; with 0
+ * (a 1-thread signal kernel) they must follow it. */
+int mgw_ce_signals_without_sm(const mgw_ce* ce, int* out);
 /* Synchronise and report a timed-out wait as an error. */
 int mgw_ce_check(mgw_ce* ce);
 int mgw_ce_destroy(mgw_ce* ce);

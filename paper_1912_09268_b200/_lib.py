@@ -143,6 +143,7 @@ mgw_ce_begin = _proto("mgw_ce_begin", [vp, vp])
 mgw_ce_mark_ready = _proto("mgw_ce_mark_ready", [vp, C.c_int, vp])
 mgw_ce_join = _proto("mgw_ce_join", [vp, vp])
 mgw_ce_set_tail = _proto("mgw_ce_set_tail", [vp, C.c_int])
+mgw_ce_signals_without_sm = _proto("mgw_ce_signals_without_sm", [vp, C.POINTER(C.c_int)])
 mgw_ce_check = _proto("mgw_ce_check", [vp])
 mgw_ce_destroy = _proto("mgw_ce_destroy", [vp])
 mgw_calibrate_ce = _proto("mgw_calibrate_ce", [vp, u64p, C.c_size_t, C.c_int, C.c_int, C.POINTER(Meas)])

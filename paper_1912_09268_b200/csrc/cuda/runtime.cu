@@ -21,6 +21,7 @@
 #include <thread>
 #include <vector>
 
+#include <cuda.h>  // driver types only (cuStreamWriteValue64 is fetched with cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 #include "capi_common.hpp"
@@ -1538,6 +1539,11 @@ struct mgw_ce {
   int n_views = 1;
   int reduce_ctas = 0;
   int n_tail = 0;  // groups [0, n_tail) are not copied nor reduced here (the caller's full-width launches)
+  // "iteration delivered" signals as stream memory operations (no SM):
+  // per (view, peer) the peer's ce_pushed word; nullptr fn: signal kernel
+  using WriteValue64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+  WriteValue64 write_value = nullptr;
+  std::vector<CUdeviceptr> signal_words;
   bool begun = false;
   // daemon
   std::vector<int> ring;              // G + 1 slots (each group at most once per iteration)
@@ -1652,6 +1658,31 @@ int mgw_ce_create(mgw_plan* p, float lr, mgw_ce** out) {
     ck(cudaMemset(e->d_done, 0, sizeof(uint32_t) * mgw::kMaxRanks), "memset(ce done)");
     C.done = e->d_done;
     e->reduce_ctas = c->num_sms;
+    // SM-free signalling: cuStreamWriteValue64 (a system-scope memory fence
+    // before the write, scoped to the stream — the copies ahead of it on the
+    // comm stream are visible before the flag). Without it, a 1-thread
+    // signal kernel (then a fused tail launch must follow mgw_ce_join).
+    {
+      int ok = 0;
+      cudaDeviceGetAttribute(&ok, static_cast<cudaDeviceAttr>(CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS),
+                             c->device);
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+      if (ok && cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess && fn != nullptr) {
+        e->write_value = reinterpret_cast<mgw_ce::WriteValue64>(fn);
+      }
+      cudaGetLastError();
+      for (int r = 0; r < p->n_views; ++r) {
+        const int me = c->loopback ? r : c->rank;
+        for (int q2 = 0; q2 < c->nranks; ++q2) {
+          if (q2 == me) continue;
+          uint32_t* sig = c->loopback ? c->signals[q2] : c->peer_signal[q2];
+          e->signal_words.push_back(reinterpret_cast<CUdeviceptr>(sig + mgw::kCeWord) +
+                                    static_cast<CUdeviceptr>(me) * sizeof(uint64_t));
+        }
+      }
+    }
     ck(cudaStreamCreateWithFlags(&e->comm, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming), "event");
@@ -1725,12 +1756,35 @@ int mgw_ce_join(mgw_ce* e, void* stream) {
       std::lock_guard<std::mutex> lk(e->mu);
       if (!e->error.empty()) throw mgw::CudaFailure(e->error);
     }
-    ck(mgw::launch_ce(1, e->args, e->n_views, 1, e->comm), "ce signal");
+    bool signalled = false;
+    if (e->write_value != nullptr) {
+      signalled = true;
+      for (CUdeviceptr w : e->signal_words) {
+        if (e->write_value(reinterpret_cast<CUstream>(e->comm), w, e->args.iter, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+            CUDA_SUCCESS) {
+          signalled = false;  // the kernel below re-signals every peer (same value: idempotent)
+          e->write_value = nullptr;
+          break;
+        }
+      }
+    }
+    if (!signalled) {
+      ck(mgw::launch_ce(1, e->args, e->n_views, 1, e->comm), "ce signal");
+      mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    }
     ck(mgw::launch_ce(2, e->args, e->n_views, e->reduce_ctas, e->comm), "ce reduce");
-    mgw::g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
+    mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     ck(cudaEventRecord(e->join, e->comm), "join");
     ck(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), e->join, 0), "join wait");
     e->begun = false;
+  }
+  MGW_CATCH
+}
+
+int mgw_ce_signals_without_sm(const mgw_ce* e, int* out) {
+  MGW_TRY {
+    require(e != nullptr && out != nullptr, "NULL argument");
+    *out = e->write_value != nullptr ? 1 : 0;
   }
   MGW_CATCH
 }

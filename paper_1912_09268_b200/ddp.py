@@ -86,6 +86,7 @@ class MGWFBP:
             self.ce = CopyEngine(self.dplan, lr)
             self.tail = max(0, min(int(tail_groups), len(self.groups) - 1))
             self.ce.set_tail(self.tail)
+            self._ce_overlap = self.ce.signals_without_sm
         else:
             h = C.c_void_p()
             check(_lib.mgw_engine_create(self.dplan.handle, lr, ALGO[algo], engine_ctas,
@@ -184,15 +185,20 @@ class MGWFBP:
         if self.mode == "ce":
             for g in missing:  # parameters that got no gradient this iteration
                 self.ce.mark_ready(g, torch.cuda.current_stream())
-            # the copy-engine reduce first, THEN the tail groups' fused launches:
-            # a fused launch pairs its CTAs with the peers' and may hold every
-            # SM while it waits, so it must never be able to run ahead of a
-            # peer's signal kernel (deadlock: rank r's reduce spins for rank
-            # q's signal while rank q's SMs are held by its tail kernel waiting
-            # for rank r's tail CTAs, measured at N = 4)
-            self.ce.join(torch.cuda.current_stream())
+            # With a signal KERNEL the copy-engine reduce must come first, THEN
+            # the tail groups' fused launches: a fused launch pairs its CTAs with
+            # the peers' and may hold every SM while it waits, so it must never
+            # run ahead of a peer's signal kernel (deadlock: rank r's reduce
+            # spins for rank q's signal while rank q's SMs are held by its tail
+            # kernel waiting for rank r's tail CTAs, measured at N = 4). With
+            # stream-memop signals (no SM) the tail overlaps the reduce.
+            overlap = self._ce_overlap  # SM-free signals: the tail may overlap the reduce
+            if not overlap:
+                self.ce.join(torch.cuda.current_stream())
             for g in reversed(range(self.tail)):
                 check(_lib.mgw_group_allreduce(self.dplan.handle, g, self.lr, 1, ALGO[self.algo], stream))
+            if overlap:
+                self.ce.join(torch.cuda.current_stream())
         elif self.mode == "launch":
             for g in range(self._next, self.tail - 1, -1):  # the rest in order (incl. groups without gradients)
                 self._launch(g, torch.cuda.current_stream())

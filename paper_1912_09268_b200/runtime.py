@@ -397,6 +397,14 @@ class CopyEngine:
     def join(self, stream=None) -> None:
         check(_lib.mgw_ce_join(self.handle, _stream_ptr(stream)))
 
+    @property
+    def signals_without_sm(self) -> bool:
+        """True: the delivery signals are stream memory operations (no SM), so
+        fused tail launches may precede join() and overlap the reduce."""
+        v = C.c_int()
+        check(_lib.mgw_ce_signals_without_sm(self.handle, C.byref(v)))
+        return bool(v.value)
+
     def set_tail(self, n_tail: int) -> None:
         """Leave groups [0, n_tail) to the caller (no copy, no reduce)."""
         check(_lib.mgw_ce_set_tail(self.handle, int(n_tail)))

@@ -37,7 +37,7 @@ def _flat(counts, arrays, dtype=torch.float32):
 
 @pytest.mark.parametrize("P", [2, 4, 8])
 @pytest.mark.parametrize("merged", [False, True])
-@pytest.mark.parametrize("tail", [0, 1])
+@pytest.mark.parametrize("tail", [0, 1, "1-overlap"])
 def test_copy_engine_bit_exact(P, merged, tail):
     """3 iterations; with tail = 1 the last-ready group goes through the
     fused full-width kernel after the backward, the rest through the copy
@@ -53,8 +53,12 @@ def test_copy_engine_bit_exact(P, merged, tail):
     tags = [int(t) for t in plan.tags]
     comm = rt.Comm.create_loopback(P, 0, 4 * rt.padded_elems(counts))
     dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+    overlap = tail == "1-overlap"
+    tail = 1 if overlap else tail
     ce = rt.CopyEngine(dp, 0.01)
     ce.set_tail(tail)
+    if overlap and not ce.signals_without_sm:
+        pytest.skip("no stream memory operations: the tail must follow join()")
     s = torch.cuda.current_stream()
     for it in range(3):
         # a new "backward" each iteration: fresh gradients, groups ready in backward order
@@ -66,9 +70,12 @@ def test_copy_engine_bit_exact(P, merged, tail):
         ce.begin(s)
         for g in reversed(range(dp.n_groups)):
             ce.mark_ready(g, s)
-        ce.join(s)
-        for g in reversed(range(tail)):  # the tail after the join (see mgw_ce_set_tail)
+        if not overlap:
+            ce.join(s)
+        for g in reversed(range(tail)):  # after the join unless the signals need no SM
             dp.group_allreduce(g, 0.01, rt.SGD, "auto", s)
+        if overlap:
+            ce.join(s)
         pyoracle.allreduce_sgd(g_np, w_np, tags, 0.01)
     torch.cuda.synchronize()
     ce.check()

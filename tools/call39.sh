@@ -1,0 +1,9 @@
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+O=gpurun_out/r2hh; mkdir -p $O
+CUDA_VISIBLE_DEVICES=0 timeout 600 python -m pytest tests/test_gpu_copy_engine.py -q -x > $O/ce.log 2>&1; echo "ce tests rc=$?"; tail -n 1 $O/ce.log
+show() { tail -n 1 $1 | python -c "
+import json,sys
+d=json.loads(sys.stdin.read()); [print(' ', k, {q:(round(v[q],3) if isinstance(v[q],float) else v[q]) for q in ('iter_ms','bwd_ms','post_bwd_ms','groups','autotune') if q in v}) for k,v in d['results'].items()]"; }
+for M in bert_large resnet152; do
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29565 tools/train_bench.py --model $M --batch 32 --iters 40 --warmup 5 --mode ce --tail-groups 1 --strategies ddp,single,mgwfbp,wfbp,tuned > $O/${M}_n4.log 2>&1; echo "$M rc=$?"; show $O/${M}_n4.log
+done
