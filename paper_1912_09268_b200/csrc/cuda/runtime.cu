@@ -1629,7 +1629,14 @@ int mgw_ce_create(mgw_plan* p, float lr, mgw_ce** out) {
     const int G = p->G();
     e->copies.resize(G);
     for (int g = 0; g < G; ++g) {
-      const uint64_t lo = p->offs[p->heads[g]], hi = p->offs[p->heads[g + 1]];
+      // the group's data span: its first layer's start to the end of its last
+      // non-empty layer (not the padded end: the caller's buffer may stop
+      // at the last element)
+      const uint64_t lo = p->offs[p->heads[g]];
+      uint64_t hi = lo;
+      for (size_t l = p->heads[g]; l < p->heads[g + 1]; ++l) {
+        if (p->counts[l] > 0) hi = p->offs[l] + p->counts[l];
+      }
       const size_t bytes = (hi - lo) * p->esize;
       if (bytes == 0) continue;
       for (int r = 0; r < p->n_views; ++r) {

@@ -27,7 +27,8 @@ def _flat(counts, arrays, dtype=torch.float32):
         offs.append(offs[-1] + ((c + 3) & ~3))
     bufs, views = [], []
     for per in arrays:
-        b = torch.zeros(max(offs[-1], 4), dtype=dtype, device="cuda")
+        # exactly to the last element (no tail padding: the copies must not read past it)
+        b = torch.zeros(max(offs[-2] + counts[-1], 4), dtype=dtype, device="cuda")
         for l, a in enumerate(per):
             b[offs[l]:offs[l] + counts[l]] = torch.from_numpy(a)
         bufs.append(b)
