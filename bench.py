@@ -74,9 +74,10 @@ def parse_args():
                          "the comm-bound regime of the paper); 1.0 = the B200-measured trace")
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"],
                     help="gradient / merge-arena type (bf16: fp32 accumulation, fp32 master weights)")
-    ap.add_argument("--protocol", default="chunked", choices=["chunked", "stream"],
-                    help="fused all-reduce protocol at N > 1: chunked (per-chunk cross-rank barrier) or stream "
-                         "(per-tile delivery counts, producer/consumer decoupled)")
+    ap.add_argument("--protocol", default="auto", choices=["auto", "chunked", "stream"],
+                    help="fused all-reduce protocol at N > 1: auto (the library default: streamed engine, the "
+                         "last-ready group as a chunked launch), chunked (per-chunk cross-rank barriers "
+                         "everywhere) or stream (per-tile delivery counts everywhere)")
     ap.add_argument("--stream-batches", default="",
                     help="CREDIT,AG: streamed-protocol publication batches (default: the library's 8,4)")
     ap.add_argument("--engine-ctas", type=int, default=-1,

@@ -211,15 +211,21 @@ int mgw_comm_get_oneshot_max(const mgw_comm* comm, uint64_t* bytes);
  *    packets; 0 disables LL.
  *  small_tile_max: groups below this many bytes are cut into 8 KiB tiles
  *    (more CTAs) instead of 32 KiB tiles.
- *  protocol: MGW_PROTO_STREAM — the producer warp streams tiles
- *    and publishes per-tile delivery counts, the data warps consume them as
- *    they arrive (no barrier after the launch's entry barrier);
- *    MGW_PROTO_CHUNKED (default) — a CTA's tiles run in pipelined chunks with one
- *    cross-rank barrier per chunk (chunk_tiles / min_chunks: at most
- *    chunk_tiles tiles per chunk, two-shot chunk_tiles / P super-tiles, and
- *    at least min_chunks chunks when the CTA owns enough tiles). */
+ *  protocol: MGW_PROTO_AUTO (default) — persistent engines run streamed
+ *    (their replay pipelines launch the last-ready group as a chunked
+ *    standalone launch after the engine), standalone group launches run
+ *    chunked; MGW_PROTO_STREAM — everything streamed: the producer warp
+ *    streams tiles and publishes per-tile delivery counts, the data warps
+ *    consume them as they arrive (no barrier after the launch's entry
+ *    barrier); MGW_PROTO_CHUNKED — everything chunked: a CTA's tiles run in
+ *    pipelined chunks with one cross-rank barrier per chunk (chunk_tiles /
+ *    min_chunks: at most chunk_tiles tiles per chunk, two-shot chunk_tiles /
+ *    P super-tiles, and at least min_chunks chunks when the CTA owns enough
+ *    tiles). At P = 1, CHUNKED selects the register engine instead of the
+ *    TMA-fed one. */
 #define MGW_PROTO_STREAM 0
 #define MGW_PROTO_CHUNKED 1
+#define MGW_PROTO_AUTO 2
 int mgw_comm_set_ll_max(mgw_comm* comm, uint64_t bytes);
 int mgw_comm_set_small_tile_max(mgw_comm* comm, uint64_t bytes);
 int mgw_comm_set_chunk_tiles(mgw_comm* comm, uint32_t max_tiles, uint32_t min_chunks);

@@ -1334,6 +1334,11 @@ __global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid
   if (threadIdx.x < 3 * kMaxRanks) s_stream[threadIdx.x] = 0u;
   CtaCtx cx;
   cta_ctx_init<P>(cx, v, dsmem, bars, &s_abort);
+  // a pipeline's tail group: stamps in the engine's layout (only CTAs that
+  // fit the engine's row are stamped; min start / max end is the group span)
+  const uint32_t stamp_col = (LOOPBACK ? blockIdx.y : 0u) * (L.stamp_row / (LOOPBACK ? gridDim.y : 1u)) + blockIdx.x;
+  const bool stamped = L.stamps != nullptr && threadIdx.x == 0 && blockIdx.x < L.stamp_row / (LOOPBACK ? gridDim.y : 1u);
+  if (stamped) L.stamps[(static_cast<size_t>(L.stamp_group) * L.stamp_row + stamp_col) * 2] = globaltimer_ns();
   if constexpr (P > 1) {
     if (L.stream) {
       const uint64_t epoch_hi = static_cast<uint64_t>(cx.epoch) << 32;
@@ -1355,6 +1360,7 @@ __global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid
                             L.epilogue, blockIdx.x, gridDim.x, cs, cx);
       }
       __syncthreads();
+      if (stamped) L.stamps[(static_cast<size_t>(L.stamp_group) * L.stamp_row + stamp_col) * 2 + 1] = globaltimer_ns();
       cta_exit<P>(v, cx);
       return;
     }
@@ -1362,6 +1368,10 @@ __global__ void __launch_bounds__(kBlock, 1) group_allreduce_kernel(const __grid
   const GroupArgs a{L.tiles, L.n_tiles, L.slot_stride, L.scale, L.lr, L.epilogue,
                     L.chunk, L.min_chunks, L.ll_pkt, L.mbase};
   run_group<P, T>(TWO_SHOT, v, a, blockIdx.x, gridDim.x, cx);
+  if (L.stamps != nullptr) {
+    __syncthreads();
+    if (stamped) L.stamps[(static_cast<size_t>(L.stamp_group) * L.stamp_row + stamp_col) * 2 + 1] = globaltimer_ns();
+  }
   cta_exit<P>(v, cx);
 }
 

@@ -107,6 +107,9 @@ struct GroupLaunch {
   uint32_t credit_batch; // streamed: bulk items per published delivery count (1, 2, 4, 8)
   uint32_t ag_batch;     // streamed two-shot: owned super-tiles per all-gather publication
   int dtype;             // MGW_DTYPE_* of the gradients / arena
+  unsigned long long* stamps;  // optional: engine-layout stamps [G][row][2] of group stamp_group
+  uint32_t stamp_group;        //   (a pipeline's tail group launched standalone after the engine)
+  uint32_t stamp_row;          //   row width (engine CTAs x emulated ranks)
   RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
 };
 

@@ -91,7 +91,8 @@ struct mgw_comm {
   uint32_t min_chunks = 1;    // a CTA splits its tiles into at least this many chunks (mgw_comm_set_chunk_tiles)
   uint32_t credit_batch = 8;  // streamed: bulk items per published delivery count (mgw_comm_set_stream_batches)
   uint32_t ag_batch = 4;      // streamed two-shot: owned super-tiles per all-gather publication
-  uint32_t proto_stream = 0;  // 1: streamed protocol, 0: chunked with per-chunk barriers (mgw_comm_set_protocol)
+  int protocol = MGW_PROTO_AUTO;  // mgw_comm_set_protocol: STREAM, CHUNKED or AUTO (engines streamed,
+                                 // standalone launches chunked; P = 1: the TMA-fed engine)
   uint64_t ll_max = 64 << 10; // one-shot groups up to this many bytes use LL packets (mgw_comm_set_ll_max)
   int max_ctas = 0;           // cap on the CTAs of a standalone group launch (0: one per SM)
   uint64_t small_tile_max = 0; // groups below this many bytes use kTileElems / 4 tiles (mgw_comm_set_small_tile_max)
@@ -165,6 +166,9 @@ struct mgw_pipeline {
   uint32_t* d_ready = nullptr;            // G ready flags (iteration stamps)
   mgw::EngineLaunch args{};               // engine kernel arguments
   bool manual = false;                    // host-driven engine (real backward), no graph
+  int tail_launch = 0;                    // replay pipelines, streamed protocol: groups [0, tail_launch)
+                                          // run as chunked standalone launches after the engine
+  cudaEvent_t replay_done = nullptr;
 };
 
 namespace mgw {
@@ -279,7 +283,8 @@ uint64_t group_bytes(const mgw_plan* p, int g) {
 }
 
 // Fused pack -> all-reduce -> unpack+SGD for group g.
-void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStream_t stream) {
+void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStream_t stream,
+                  bool force_chunked = false, unsigned long long* stamps = nullptr, uint32_t stamp_row = 0) {
   mgw_comm* c = p->comm;
   require(c->loopback || c->nranks == 1 || c->peers_ready,
           "communicator peers not opened (call mgw_comm_open_peers)");
@@ -294,10 +299,13 @@ void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStre
   L.slot_stride = p->slot_stride;
   L.chunk = c->chunk_tiles;
   L.min_chunks = c->min_chunks;
-  L.stream = c->proto_stream;
+  L.stream = (!force_chunked && c->protocol == MGW_PROTO_STREAM) ? 1u : 0u;  // AUTO: chunked when standalone
   L.credit_batch = c->credit_batch;
   L.ag_batch = c->ag_batch;
   L.dtype = p->dtype;
+  L.stamps = stamps;
+  L.stamp_group = static_cast<uint32_t>(g);
+  L.stamp_row = stamp_row;
   for (int r = 0; r < p->n_views; ++r) {
     L.views[r] = make_view(c, r, p->d_grads + static_cast<size_t>(r) * p->L,
                            p->d_weights + static_cast<size_t>(r) * p->L);
@@ -451,7 +459,6 @@ int mgw_comm_create(int rank, int nranks, int device, size_t arena_bytes, mgw_co
     c->rank = rank;
     c->nranks = nranks;
     c->oneshot_max = mgw::default_oneshot_max(nranks);
-    c->proto_stream = nranks == 1 ? 1u : 0u;  // P = 1: the TMA-fed engine; P > 1: chunked
     c->ll_max = mgw::default_ll_max(nranks);
     c->small_tile_max = mgw::kDefaultSmallTileMax;
     mgw::init_common(c, device, arena_bytes);
@@ -474,7 +481,6 @@ int mgw_comm_create_loopback(int nranks, int device, size_t arena_bytes, mgw_com
     auto* c = new mgw_comm();
     c->nranks = nranks;
     c->oneshot_max = mgw::default_oneshot_max(nranks);
-    c->proto_stream = nranks == 1 ? 1u : 0u;  // P = 1: the TMA-fed engine; P > 1: chunked
     c->ll_max = mgw::default_ll_max(nranks);
     c->small_tile_max = mgw::kDefaultSmallTileMax;
     c->loopback = true;
@@ -586,9 +592,9 @@ int mgw_comm_set_chunk_tiles(mgw_comm* c, uint32_t max_tiles, uint32_t min_chunk
 int mgw_comm_set_protocol(mgw_comm* c, int protocol) {
   MGW_TRY {
     require(c != nullptr, "comm is NULL");
-    require(protocol == MGW_PROTO_STREAM || protocol == MGW_PROTO_CHUNKED,
-            "protocol must be MGW_PROTO_STREAM or MGW_PROTO_CHUNKED");
-    c->proto_stream = protocol == MGW_PROTO_STREAM ? 1u : 0u;
+    require(protocol == MGW_PROTO_STREAM || protocol == MGW_PROTO_CHUNKED || protocol == MGW_PROTO_AUTO,
+            "protocol must be MGW_PROTO_STREAM, MGW_PROTO_CHUNKED or MGW_PROTO_AUTO");
+    c->protocol = protocol;
   }
   MGW_CATCH
 }
@@ -608,7 +614,7 @@ int mgw_comm_set_stream_batches(mgw_comm* c, uint32_t credit_batch, uint32_t ag_
 int mgw_comm_get_protocol(const mgw_comm* c, int* protocol) {
   MGW_TRY {
     require(c != nullptr && protocol != nullptr, "NULL argument");
-    *protocol = c->proto_stream ? MGW_PROTO_STREAM : MGW_PROTO_CHUNKED;
+    *protocol = c->protocol;
   }
   MGW_CATCH
 }
@@ -774,7 +780,7 @@ int mgw_allreduce(mgw_comm* c, float* buf, size_t n, int algo, void* stream) {
     L.slot_stride = p->slot_stride;
     L.chunk = c->chunk_tiles;
     L.min_chunks = c->min_chunks;
-    L.stream = c->proto_stream;
+    L.stream = c->protocol == MGW_PROTO_STREAM ? 1u : 0u;
     L.credit_batch = c->credit_batch;
     L.ag_batch = c->ag_batch;
     L.dtype = MGW_DTYPE_F32;
@@ -986,7 +992,8 @@ void setup_engine(mgw_pipeline* pipe, mgw_plan* p, int algo, int engine_ctas, fl
   E.slot_stride = p->slot_stride;
   E.chunk = c->chunk_tiles;
   E.min_chunks = c->min_chunks;
-  E.stream = c->proto_stream;
+  // engines: streamed unless CHUNKED is asked for (P = 1: the TMA-fed engine)
+  E.stream = c->protocol != MGW_PROTO_CHUNKED ? 1u : 0u;
   E.credit_batch = c->credit_batch;
   E.ag_batch = c->ag_batch;
   E.dtype = p->dtype;
@@ -1048,6 +1055,15 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
     mgw_comm* c = p->comm;
     if (pipe->engine) {
       setup_engine(pipe, p, algo, engine_ctas, lr, timed);
+      // Streamed protocol: it wins where groups follow each other and loses
+      // on an isolated large group — the last group the
+      // backward makes ready is exactly that, and the only one exposed. It
+      // runs as a chunked standalone launch (full grid) after the engine and
+      // the replay; the engine takes groups [1, G).
+      if (c->nranks > 1 && pipe->args.stream && G > 1) {
+        pipe->tail_launch = 1;
+        pipe->args.g_lo = 1;
+      }
       // ready time of every group head, in backward (comm) order
       std::vector<unsigned long long> dl;
       for (int g = G - 1; g >= 0; --g) {
@@ -1105,6 +1121,16 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
         ck(launch_replay_all(pipe->d_clock, pipe->d_deadlines, static_cast<uint32_t>(G), pipe->d_pipe,
                              pipe->d_ready, pipe->compute),
            "replay");
+        if (pipe->tail_launch > 0) {
+          // the replay kernel ends right after marking group 0 (last in backward order) ready
+          ck(cudaEventCreateWithFlags(&pipe->replay_done, cudaEventDisableTiming), "event");
+          ck(cudaEventRecord(pipe->replay_done, pipe->compute), "replay done");
+          ck(cudaStreamWaitEvent(pipe->comm, pipe->replay_done, 0), "replay done wait");
+          for (int g = pipe->tail_launch - 1; g >= 0; --g) {
+            launch_group(p, g, lr, MGW_SGD, algo, pipe->comm, /*force_chunked=*/true,
+                         pipe->timed_groups ? pipe->d_stamps : nullptr, static_cast<uint32_t>(pipe->stamp_cols));
+          }
+        }
       }
       bool first = true;
       for (int g = G - 1; g >= 0 && !pipe->engine; --g) {
@@ -1143,8 +1169,11 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
       // the capture counted kernels once; graph replays add per launch
       g_kernel_launches.fetch_sub(static_cast<uint64_t>(G), std::memory_order_relaxed);
     }
-    // engine + replay, or replay + group kernel per group; plus the L2 flush
-    pipe->kernels_per_iter = (pipe->engine ? 2 : 2 * G) + (pipe->flush_bytes > 0 ? 1 : 0);
+    if (pipe->engine && pipe->tail_launch > 0) {
+      g_kernel_launches.fetch_sub(static_cast<uint64_t>(pipe->tail_launch), std::memory_order_relaxed);
+    }
+    // engine + replay (+ tail launches), or replay + group kernel per group; plus the L2 flush
+    pipe->kernels_per_iter = (pipe->engine ? 2 + pipe->tail_launch : 2 * G) + (pipe->flush_bytes > 0 ? 1 : 0);
     return pipe;
   }
 }
@@ -1167,6 +1196,7 @@ int mgw_pipeline_destroy(mgw_pipeline* pipe) {
     for (auto e : pipe->g_end) cudaEventDestroy(e);
     cudaEventDestroy(pipe->fork);
     cudaEventDestroy(pipe->join);
+    if (pipe->replay_done) cudaEventDestroy(pipe->replay_done);
     cudaFree(pipe->d_clock);
     if (pipe->flush_buf) cudaFree(pipe->flush_buf);
     if (pipe->d_pipe) cudaFree(pipe->d_pipe);
@@ -1433,6 +1463,7 @@ int mgw_pipeline_drain(mgw_pipeline* pipe, int iters, float* ms_out) {
     mgw_comm* c = pipe->plan->comm;
     mgw::EngineLaunch E = pipe->args;
     E.no_wait = 1;  // every group ready at launch: the engine streams the whole plan
+    if (pipe->tail_launch > 0) E.g_lo = 0;  // (including the pipeline's tail group)
     std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(iters));
     for (auto& e : ev) ck(cudaEventCreate(&e), "event");
     try {

@@ -30,7 +30,7 @@ def _stream_ptr(stream) -> int:
 
 
 F32, BF16 = 0, 1  # mgw_dtype (gradient / merge-arena element type)
-PROTOCOLS = {"stream": 0, "chunked": 1}  # MGW_PROTO_*
+PROTOCOLS = {"stream": 0, "chunked": 1, "auto": 2}  # MGW_PROTO_*
 
 
 def padded_elems(counts: Sequence[int], dtype: int = F32) -> int:
@@ -122,8 +122,9 @@ class Comm(_Owner):
         check(_lib.mgw_comm_set_chunk_tiles(self.handle, int(max_tiles), int(min_chunks)))
 
     def set_protocol(self, protocol: str) -> None:
-        """'chunked' (default: one cross-rank barrier per chunk) or 'stream'
-        (per-tile delivery counts, no barrier after the entry barrier)."""
+        """'auto' (default: engines streamed, standalone launches chunked),
+        'stream' (per-tile delivery counts, no barrier after the entry
+        barrier) or 'chunked' (one cross-rank barrier per chunk)."""
         check(_lib.mgw_comm_set_protocol(self.handle, PROTOCOLS[protocol]))
 
     def set_stream_batches(self, credit_batch: int = 8, ag_batch: int = 4) -> None:
