@@ -66,6 +66,10 @@ def parse_args():
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot"])
     ap.add_argument("--oneshot-max", type=int, default=0, help="0: the library default for N")
+    ap.add_argument("--nvls", type=float, default=0.0,
+                    help="MiB: route fp32 standalone group launches of at least this size through the NVLS "
+                         "(switch-reduced) variant (0: off, the default; N > 1 only). The bus_gbs table "
+                         "measures NVLS beside NCCL whenever the pool supports multicast objects.")
     ap.add_argument("--cost", default="linear", choices=["linear", "table"],
                     help="linear: the reference's a + b*M (bit-exact optimal_plan); table: B200 extension, the same "
                          "DP on the calibration's piecewise measured curve")
@@ -480,6 +484,16 @@ def main():
         comm.set_protocol(args.protocol)  # (P = 1 always runs the TMA-fed single-rank engine)
         if args.stream_batches:
             comm.set_stream_batches(*(int(x) for x in args.stream_batches.split(",")))
+    # NVLS (switch-reduced two-shot, opt-in): set up whenever the pool has
+    # multicast objects (the bus table measures it); the data path uses it
+    # only with --nvls
+    nvls = "n/a (N = 1)" if N == 1 else "unsupported on this pool"
+    if N > 1 and not bf16:
+        ok = torch.tensor([1.0 if comm.nvls_supported() else 0.0], device=dev)
+        torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+        if ok.item() > 0:
+            comm.enable_nvls(int(args.nvls * (1 << 20)))
+            nvls = (f"on for groups >= {args.nvls} MiB" if args.nvls > 0 else "measured only (bus_gbs)")
 
     # ---- N1: on-box calibration of the fused engine kernel at this N
     sizes = calibration_sizes(total_bytes, 4 * padded)
@@ -674,10 +688,16 @@ def main():
             ev[1].synchronize()
             ncclt.append(D.max_over_ranks(ev[0].elapsed_time(ev[1]) / 10 / 1e3, dev))
             del x
-        for m, tn in zip(big, ncclt):
+        nv = [None] * len(big)
+        if comm.nvls_ready:
+            mm = comm.calibrate([m.size_bytes for m in big], warmup=2, reps=9, algo="nvls")
+            nv = [D.max_over_ranks(x.time_sec, dev) for x in mm]
+        for m, tn, tv in zip(big, ncclt, nv):
             f = 2 * (N - 1) / N * m.size_bytes / 1e9
             bus[str(m.size_bytes)] = {"mgwfbp": f / m.time_sec, "nccl": f / tn,
                                       "mgwfbp_frac_900": f / m.time_sec / NVLINK_GBS}
+            if tv:
+                bus[str(m.size_bytes)]["nvls_standalone"] = f / tv
 
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
@@ -705,7 +725,7 @@ def main():
                                 "formula": "max(t_f + sum t_b, t_f + t_b[last layer] + sum_g 2(P-1)/P*S_g / 900 GB/s)"},
             "gpu": {"comm": ("persistent engine, %s CTAs" % ("1/SM" if args.engine_ctas < 0 else args.engine_ctas))
                             if args.engine_ctas else "one fused kernel launch per group",
-                    "algo": args.algo, "tuning": comm.tuning(), "ipc_ranks_mapped": peers,
+                    "algo": args.algo, "tuning": comm.tuning(), "ipc_ranks_mapped": peers, "nvls": nvls,
                     "l2_flush": f"{args.l2_flush_mib} MiB streaming stores on the comm stream during the forward "
                                 "replay, every iteration"},
             "calibration": {"plan_model": {"a_us": model.a * 1e6, "b_ps_per_byte": model.b * 1e12, "how": model_how},

@@ -192,7 +192,7 @@ int mgw_unpack_sgd(mgw_plan* plan, int group, const void* merge_buf, float lr, i
                    void* stream);
 
 /* Algorithm selection for the merged all-reduce. */
-typedef enum { MGW_ALGO_AUTO = 0, MGW_ALGO_ONESHOT = 1, MGW_ALGO_TWOSHOT = 2 } mgw_algo;
+typedef enum { MGW_ALGO_AUTO = 0, MGW_ALGO_ONESHOT = 1, MGW_ALGO_TWOSHOT = 2, MGW_ALGO_NVLS = 3 } mgw_algo;
 /* Epilogue flags. */
 enum { MGW_SGD = 1, MGW_WRITE_GRAD = 2 };
 
@@ -243,6 +243,37 @@ int mgw_comm_get_tuning(const mgw_comm* comm, uint64_t* oneshot_max, uint64_t* l
  * SGD epilogues). Reads host-mapped memory: no CUDA call, no sync — cheap
  * enough to poll every iteration. A failed communicator stays failed. */
 int mgw_comm_error(const mgw_comm* comm, int* failed);
+/* NVLS (NVLink SHARP, the optional switch-reduced variant of SURVEY §5):
+ * every rank's copy of one arena slot is bound to a multicast object; the
+ * owner of each vector reads the P copies' SUM through the multicast
+ * address (multimem.ld_reduce: the NVSwitch reduces) and stores it to all P
+ * copies (multimem.st), then every rank unpacks + applies SGD locally. NVLink
+ * bytes per rank: S each way instead of 2(P-1)/P*S. Numerics: the switch
+ * returns the exact sum of the P scaled fp32 values rounded once (nearest
+ * even) — the rank-order sum at P = 2, the oracle's exact-sum variant at
+ * P >= 4 (deterministic, identical on every rank). fp32 only; standalone
+ * group launches only (mgw_group_allreduce, mgw_allreduce, calibration, the
+ * pipelines' launch mode and tail launches), never the persistent engine.
+ * Setup is collective, three phases (the caller moves rank 0's handle to
+ * every rank and puts a barrier between join and bind):
+ *   mgw_comm_nvls_create  rank 0 creates + exports the multicast object into
+ *                         handle_out (mgw_nvls_handle_size() bytes; other ranks
+ *                         get zeros);
+ *   mgw_comm_nvls_join    every rank: import rank 0's handle, add its GPU;
+ *   mgw_comm_nvls_bind    every rank, after all joined: bind + map.
+ * mgw_comm_set_nvls: MGW_ALGO_AUTO sends fp32 groups of at least min_bytes
+ * through NVLS (0: never, the default); chunk_tiles (1..16, default 4): tiles
+ * per pipelined chunk of a CTA. MGW_ALGO_NVLS forces it for any size. */
+size_t mgw_nvls_handle_size(void);
+int mgw_comm_nvls_supported(const mgw_comm* comm, int* supported);
+int mgw_comm_nvls_create(mgw_comm* comm, void* handle_out);
+int mgw_comm_nvls_join(mgw_comm* comm, const void* handle0);
+int mgw_comm_nvls_bind(mgw_comm* comm);
+int mgw_comm_nvls_ready(const mgw_comm* comm, int* ready);
+int mgw_comm_set_nvls(mgw_comm* comm, uint64_t min_bytes, uint32_t chunk_tiles);
+/* Profiling aid (results are WRONG while set): 1 skips the NVLS kernel's
+ * pack / unpack (HBM) phases, 2 skips its switch reduce; 0 restores. */
+int mgw_comm_set_nvls_skip(mgw_comm* comm, uint32_t mask);
 /* Cap on the CTAs per rank of a standalone fused launch (mgw_group_allreduce,
  * mgw_allreduce); 0 = one per SM (default). A real backward that launches
  * groups while it runs leaves the other SMs to the compute kernels. */

@@ -226,6 +226,34 @@ void orc_allreduce_sgd(int P, float* const* grads, float* const* weights, const 
   }
 }
 
+/* NVLS variant (the switch-reduced all-reduce, SURVEY §5 "optional, flagged"):
+ * the NVSwitch's multimem.ld_reduce returns the EXACT sum of the P scaled
+ * fp32 values rounded once to fp32 (nearest even) — measured on B200,
+ * tools/nvls_probe.cu; at P = 2 that equals the rank-order sum. Restated
+ * with an x87 80-bit accumulator: exact whenever the P addends' exponents
+ * span <= 37 bits (64-bit significand), which holds for every test input
+ * here (uniform gradients); then one rounding to fp32. Not pinned to the
+ * reference: the reference models no runtime. */
+void orc_allreduce_sgd_nvls(int P, float* const* grads, float* const* weights, const uint64_t* counts,
+                            size_t L, const uint8_t* tags, float lr, int write_grad) {
+  const float scale = 1.0f / (float)P;
+  (void)tags;
+  for (size_t l = 0; l < L; ++l) {
+    for (uint64_t j = 0; j < counts[l]; ++j) {
+      long double exact = 0.0L;
+      for (int r = 0; r < P; ++r) exact += (long double)(grads[(size_t)r * L + l][j] * scale);
+      const float acc = (float)exact;
+      for (int r = 0; r < P; ++r) {
+        float* w = weights[(size_t)r * L + l];
+        if (w) w[j] = w[j] - lr * acc;
+      }
+      if (write_grad) {
+        for (int r = 0; r < P; ++r) grads[(size_t)r * L + l][j] = acc;
+      }
+    }
+  }
+}
+
 /* ------------------------------------------------------- bf16 gradients */
 
 uint16_t orc_f32_to_bf16(float x) {

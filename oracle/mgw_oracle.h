@@ -57,6 +57,11 @@ void orc_pack(const float* const* grads, const uint64_t* counts, const uint64_t*
 void orc_allreduce_sgd(int P, float* const* grads, float* const* weights, const uint64_t* counts,
                        size_t L, const uint8_t* tags, float lr, int write_grad);
 
+/* NVLS variant: the per-element sum is the exact sum of the P scaled values
+ * rounded once to fp32 (what the NVSwitch's multimem.ld_reduce returns). */
+void orc_allreduce_sgd_nvls(int P, float* const* grads, float* const* weights, const uint64_t* counts,
+                            size_t L, const uint8_t* tags, float lr, int write_grad);
+
 /* --- bf16 gradients (reference trace.hpp:50
  * bytes_per_element = 2). The build's semantics, restated: every source is
  * widened to fp32 (exact), times 1/P, summed in rank order in fp32; the sum

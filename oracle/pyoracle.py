@@ -45,6 +45,7 @@ if ORC is not None:
     ORC.orc_pack.argtypes = [fpp, u64p, u64p, C.c_size_t, C.c_size_t, C.c_float, C.c_void_p]
     ORC.orc_pack.restype = None
     ORC.orc_allreduce_sgd.argtypes = [C.c_int, fpp, fpp, u64p, C.c_size_t, u8p, C.c_float, C.c_int]
+    ORC.orc_allreduce_sgd_nvls.argtypes = [C.c_int, fpp, fpp, u64p, C.c_size_t, u8p, C.c_float, C.c_int]
     ORC.orc_allreduce_sgd.restype = None
     ORC.orc_pipeline_run.argtypes = [C.c_int, fpp, fpp, u64p, f64p, C.c_size_t, C.c_double, u8p,
                                      C.c_float, C.c_int, C.c_int, f64p]
@@ -157,6 +158,17 @@ def allreduce_sgd(grads: List[List[np.ndarray]], weights: List[List[np.ndarray]]
     ORC.orc_allreduce_sgd(P, _ptrs([g for per in grads for g in per]),
                           _ptrs([w for per in weights for w in per]),
                           (C.c_uint64 * L)(*counts), L, (C.c_uint8 * L)(*tags), lr, int(write_grad))
+
+
+def allreduce_sgd_nvls(grads: List[List[np.ndarray]], weights: List[List[np.ndarray]], tags, lr: float,
+                       write_grad: bool = False) -> None:
+    """allreduce_sgd with the NVLS numerics: each element's sum is the exact
+    sum of the P scaled values rounded once to fp32."""
+    P, L = len(grads), len(grads[0])
+    counts = [g.size for g in grads[0]]
+    ORC.orc_allreduce_sgd_nvls(P, _ptrs([g for per in grads for g in per]),
+                               _ptrs([w for per in weights for w in per]),
+                               (C.c_uint64 * L)(*counts), L, (C.c_uint8 * L)(*tags), lr, int(write_grad))
 
 
 # ---- bf16 gradients (SURVEY §8f row 4) -----------------------------------

@@ -88,6 +88,14 @@ mgw_comm_set_protocol = _proto("mgw_comm_set_protocol", [vp, C.c_int])
 mgw_comm_set_stream_batches = _proto("mgw_comm_set_stream_batches", [vp, C.c_uint32, C.c_uint32])
 mgw_comm_get_protocol = _proto("mgw_comm_get_protocol", [vp, C.POINTER(C.c_int)])
 mgw_comm_error = _proto("mgw_comm_error", [vp, C.POINTER(C.c_int)])
+mgw_nvls_handle_size = _proto("mgw_nvls_handle_size", [], C.c_size_t)
+mgw_comm_nvls_supported = _proto("mgw_comm_nvls_supported", [vp, C.POINTER(C.c_int)])
+mgw_comm_nvls_create = _proto("mgw_comm_nvls_create", [vp, vp])
+mgw_comm_nvls_join = _proto("mgw_comm_nvls_join", [vp, vp])
+mgw_comm_nvls_bind = _proto("mgw_comm_nvls_bind", [vp])
+mgw_comm_nvls_ready = _proto("mgw_comm_nvls_ready", [vp, C.POINTER(C.c_int)])
+mgw_comm_set_nvls = _proto("mgw_comm_set_nvls", [vp, C.c_uint64, C.c_uint32])
+mgw_comm_set_nvls_skip = _proto("mgw_comm_set_nvls_skip", [vp, C.c_uint32])
 mgw_comm_get_tuning = _proto("mgw_comm_get_tuning", [vp, u64p, u64p, u64p, C.POINTER(C.c_uint32),
                                                       C.POINTER(C.c_uint32)])
 mgw_plan_create = _proto(

@@ -1780,6 +1780,251 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
   }
 }
 
+// ---- NVLS (NVLink SHARP) two-shot ---------------------------------------------
+// The NVSwitch does the reduction: each rank packs its scaled gradients into
+// its own NVLS buffer (local HBM; the buffers of all ranks are bound to one
+// multicast object), then the owner of each vector loads it through the
+// multicast address with multimem.ld_reduce (the switch returns the sum of
+// the P copies) and stores the sum back with multimem.st (the switch writes
+// it into all P copies); every rank then unpacks + applies SGD from its local
+// copy. NVLink bytes per rank: S in and S out, against 2(P-1)/P*S each way
+// for the push two-shot — the win grows with P.
+// Numerics (measured on B200, tools/nvls_probe.cu): the switch returns the
+// EXACT sum of the P fp32 inputs rounded once to fp32 (round to nearest
+// even) — at P = 2 that is the rank-order sum bit for bit; at P >= 4 it is
+// deterministic, identical on every rank and pinned by the oracle's
+// exact-sum variant (mgw_oracle_nvls), but not the rank-order fold.
+//
+// Pipeline per CTA (its tiles j = b, b + ncta, ..., in chunks of `chunk`
+// tiles), step s: the HBM warps pack chunk s and unpack + SGD chunk s - 2,
+// the switch warps reduce chunk s - 1; ONE cross-rank barrier per step
+// certifies both "chunk s packed everywhere" and "chunk s - 1's sums landed
+// everywhere". No entry barrier: every byte a launch reads remotely was
+// certified by a barrier of the launch that wrote it, and the previous
+// launch's last remote access precedes its last barrier.
+// 256-thread CTAs, several per SM: a CTA waiting on its step barrier leaves
+// the SM to the others (the per-step latency chain — ld_reduce round trip,
+// the multicast stores' fence, the barrier round trip — is ~3 NVLink round
+// trips, and one CTA per SM would serialise them).
+constexpr uint32_t kNvlsBlock = 256;
+constexpr uint32_t kNvlsWarps = 4;                    // switch warps (the other 4: HBM warps)
+constexpr uint32_t kNvlsThreads = kNvlsWarps * 32;    // per role
+constexpr uint32_t kNvlsMaxChunk = 16;                // tiles per chunk (<= 32: one lane per tile)
+constexpr uint32_t kNvlsU = 4;                        // vectors in flight per thread and batch
+
+__device__ __forceinline__ float4 mc_ld_reduce(const float* mc) {
+  float4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(mc)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void mc_st(float* mc, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+// One chunk's tiles as a flat vector index space: entry k covers vectors
+// [pre[k], pre[k+1]) (pre[0] = 0); built by one warp, lane k = tile k.
+struct NvlsChunk {
+  uint32_t pre[kNvlsMaxChunk + 1];
+  uint32_t base[kNvlsMaxChunk];   // first vector: merge-layout vector index (reduce) / 0 (pack, unpack)
+  Tile t[kNvlsMaxChunk];
+  float* w[kNvlsMaxChunk];        // layer weights (unpack)
+  float* g[kNvlsMaxChunk];        // layer gradients
+};
+
+__device__ __forceinline__ uint32_t nvls_find(const NvlsChunk& c, uint32_t nt, uint32_t idx) {
+  uint32_t k = 0;
+  while (k + 1 < nt && idx >= c.pre[k + 1]) ++k;
+  return k;
+}
+
+// Lane k < nt of the calling warp describes tile k of chunk `m0` (CTA b's
+// tiles m0 .. m0+nt-1, stride ncta); part = true: only this rank's 1/P of
+// every tile's vectors (the switch reduce).
+template <int P>
+__device__ __forceinline__ void nvls_describe(NvlsChunk& c, const GroupLaunch& L, const RankView& v, uint32_t m0,
+                                              uint32_t nt, bool part) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t n = 0;
+  if (lane < nt) {
+    const Tile t = L.tiles[blockIdx.x + (m0 + lane) * gridDim.x];
+    const uint32_t nv = (t.len + 3) >> 2;
+    const uint32_t l = t.layer & kLayerMask;
+    c.t[lane] = t;
+    if (part) {
+      const uint32_t lo = nv * static_cast<uint32_t>(v.rank) / P;
+      const uint32_t hi = nv * static_cast<uint32_t>(v.rank + 1) / P;
+      c.base[lane] = t.moff / 4 + lo;
+      n = hi - lo;
+    } else {
+      c.base[lane] = 0;
+      c.w[lane] = v.weights[l];
+      c.g[lane] = v.grads[l];
+      n = nv;
+    }
+  }
+  // inclusive scan of n over the warp
+  uint32_t x = n;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (static_cast<int>(lane) >= d) x += y;
+  }
+  if (lane < nt) c.pre[lane + 1] = x;
+  if (lane == 0) c.pre[0] = 0;
+}
+
+// Switch warps: this rank's part of every tile of the chunk through the
+// multicast address (ld_reduce -> st), kNvlsU vectors in flight per thread.
+__device__ __forceinline__ void nvls_reduce(float* mc, const NvlsChunk& c, uint32_t nt, uint32_t tid) {
+  const uint32_t total = c.pre[nt];
+  for (uint32_t i0 = tid; i0 < total; i0 += kNvlsU * kNvlsThreads) {
+    float4 x[kNvlsU];
+    size_t at[kNvlsU];
+#pragma unroll
+    for (uint32_t u = 0; u < kNvlsU; ++u) {
+      const uint32_t i = i0 + u * kNvlsThreads;
+      if (i < total) {
+        const uint32_t k = nvls_find(c, nt, i);
+        at[u] = static_cast<size_t>(c.base[k] + (i - c.pre[k])) * 4;
+        x[u] = mc_ld_reduce(mc + at[u]);
+      }
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kNvlsU; ++u) {
+      if (i0 + u * kNvlsThreads < total) mc_st(mc + at[u], x[u]);
+    }
+  }
+}
+
+// HBM warps: pack (x 1/P into this rank's copy), 2 kNvlsU vectors in flight.
+__device__ __forceinline__ void nvls_pack(float* uc, const NvlsChunk& c, uint32_t nt, float scale, uint32_t tid) {
+  constexpr uint32_t U = 2 * kNvlsU;
+  const uint32_t total = c.pre[nt];
+  for (uint32_t i0 = tid; i0 < total; i0 += U * kNvlsThreads) {
+    float4 x[U];
+    float* dst[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      const uint32_t i = i0 + u * kNvlsThreads;
+      if (i < total) {
+        const uint32_t k = nvls_find(c, nt, i);
+        const Tile& t = c.t[k];
+        const uint32_t e = (i - c.pre[k]) * 4;
+        const float* src = c.g[k] + t.src + e;
+        x[u] = (!(t.layer & kGradUnaligned) && e + 4 <= t.len) ? ld_stream_v4(src) : load_tail(src, t.len - e);
+        dst[u] = uc + t.moff + e;
+      }
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      if (i0 + u * kNvlsThreads < total) st_v4(dst[u], mul4(x[u], scale));
+    }
+  }
+}
+
+// HBM warps: unpack + SGD from this rank's copy of the sums.
+__device__ __forceinline__ void nvls_unpack(const float* uc, const NvlsChunk& c, uint32_t nt, float lr, int epi,
+                                            uint32_t tid) {
+  const uint32_t total = c.pre[nt];
+  for (uint32_t i0 = tid; i0 < total; i0 += kNvlsU * kNvlsThreads) {
+    float4 sv[kNvlsU], wv[kNvlsU];
+    uint32_t kk[kNvlsU], ee[kNvlsU];
+    bool fast[kNvlsU];
+#pragma unroll
+    for (uint32_t u = 0; u < kNvlsU; ++u) {
+      const uint32_t i = i0 + u * kNvlsThreads;
+      fast[u] = false;
+      if (i < total) {
+        const uint32_t k = nvls_find(c, nt, i);
+        const Tile& t = c.t[k];
+        const uint32_t e = (i - c.pre[k]) * 4;
+        kk[u] = k;
+        ee[u] = e;
+        sv[u] = ld_cg_v4(uc + t.moff + e);
+        fast[u] = (epi & MGW_SGD) && c.w[k] != nullptr && e + 4 <= t.len && !(t.layer & kWeightUnaligned);
+        if (fast[u]) wv[u] = ld_v4(c.w[k] + t.src + e);
+      }
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kNvlsU; ++u) {
+      if (i0 + u * kNvlsThreads >= total) continue;
+      const Tile& t = c.t[kk[u]];
+      if (fast[u]) {
+        float4 w = wv[u];
+        w.x = sgd1(w.x, sv[u].x, lr);
+        w.y = sgd1(w.y, sv[u].y, lr);
+        w.z = sgd1(w.z, sv[u].z, lr);
+        w.w = sgd1(w.w, sv[u].w, lr);
+        st_v4(c.w[kk[u]] + t.src + ee[u], w);
+        if (epi & MGW_WRITE_GRAD) epilogue<float>(t, ee[u], sv[u], nullptr, c.g[kk[u]], lr, MGW_WRITE_GRAD);
+      } else {
+        epilogue<float>(t, ee[u], sv[u], c.w[kk[u]], c.g[kk[u]], lr, epi);
+      }
+    }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kNvlsBlock, 2) nvls_group_kernel(const __grid_constant__ GroupLaunch L) {
+  __shared__ uint32_t s_abort;
+  __shared__ uint32_t s_init[2];
+  __shared__ NvlsChunk s_red, s_pack, s_unpack;
+  const RankView& v = L.views[0];
+  CtaCtx cx{};
+  cx.s_abort = &s_abort;
+  cx.producer = false;
+  if (threadIdx.x == 0) {
+    s_abort = 0u;
+    s_init[0] = ld_volatile_u32(v.state + kStateCtaBase + blockIdx.x);
+    s_init[1] = ld_volatile_u32(v.state + kStateSeq);
+  }
+  __syncthreads();
+  cx.count = s_init[0];
+  cx.epoch = s_init[1] + 1u;
+  // a pipeline's tail group: stamps in the engine's layout (as group_allreduce_kernel)
+  const bool stamped = L.stamps != nullptr && threadIdx.x == 0 && blockIdx.x < L.stamp_row;
+  const size_t stamp_at = (static_cast<size_t>(L.stamp_group) * L.stamp_row + blockIdx.x) * 2;
+  if (stamped) L.stamps[stamp_at] = globaltimer_ns();
+  const uint32_t ncta = gridDim.x;
+  const uint32_t b = blockIdx.x;
+  const uint32_t mine = L.n_tiles > b ? (L.n_tiles - b + ncta - 1) / ncta : 0u;  // tiles j = b + m * ncta
+  const uint32_t chunk = L.chunk < 1 ? 1u : (L.chunk > kNvlsMaxChunk ? kNvlsMaxChunk : L.chunk);
+  const uint32_t nchunks = (mine + chunk - 1) / chunk;
+  const uint32_t warp = threadIdx.x >> 5;
+  const bool hbm = threadIdx.x >= kNvlsThreads;
+  const uint32_t tid = hbm ? threadIdx.x - kNvlsThreads : threadIdx.x;
+  auto nt_of = [&](uint32_t c) { return min(chunk, mine - c * chunk); };
+  // step s: pack chunk s | reduce chunk s - 1 | unpack chunk s - 2; one barrier
+  for (uint32_t s = 0; s < nchunks + 2; ++s) {
+    const bool do_pack = s < nchunks, do_red = s >= 1 && s - 1 < nchunks, do_unpack = s >= 2;
+    if (warp == 0 && do_red) nvls_describe<P>(s_red, L, v, (s - 1) * chunk, nt_of(s - 1), true);
+    if (warp == kNvlsWarps && do_pack) nvls_describe<P>(s_pack, L, v, s * chunk, nt_of(s), false);
+    if (warp == kNvlsWarps + 1 && do_unpack) nvls_describe<P>(s_unpack, L, v, (s - 2) * chunk, nt_of(s - 2), false);
+    __syncthreads();
+    if (!cx.abort) {
+      if (!hbm) {
+        if (do_red && !(L.min_chunks & 2u)) {
+          nvls_reduce(L.nvls_mc, s_red, nt_of(s - 1), tid);
+          asm volatile("fence.acq_rel.sys;" ::: "memory");  // the multicast stores before the barrier's release
+        }
+      } else {
+        if (do_pack && !(L.min_chunks & 1u)) nvls_pack(L.nvls_uc, s_pack, nt_of(s), L.scale, tid);
+        if (do_unpack && !(L.min_chunks & 1u)) nvls_unpack(L.nvls_uc, s_unpack, nt_of(s - 2), L.lr, L.epilogue, tid);
+      }
+    }
+    if (s < nchunks + 1) cta_barrier(v, P, cx);  // the last step (unpack only) needs none
+    else __syncthreads();
+  }
+  if (stamped) L.stamps[stamp_at + 1] = globaltimer_ns();
+  cta_exit<P>(v, cx);
+}
+
 // ---- copy-engine mode ---------------------------------------------------------
 // During a real backward the gradients of each finished group travel to the
 // peers' arenas as copy-engine (DMA) writes over NVLink — no SM is taken
@@ -2050,6 +2295,23 @@ cudaError_t launch_group_allreduce(const GroupLaunch& L, int ctas_per_rank, bool
                   : launch_lb<false, float>(L, grid, two_shot, stream);
 }
 
+cudaError_t launch_nvls_group(const GroupLaunch& L, int ctas, cudaStream_t stream) {
+  switch (L.nranks) {
+    case 2: nvls_group_kernel<2><<<ctas, kNvlsBlock, 0, stream>>>(L); break;
+    case 4: nvls_group_kernel<4><<<ctas, kNvlsBlock, 0, stream>>>(L); break;
+    case 8: nvls_group_kernel<8><<<ctas, kNvlsBlock, 0, stream>>>(L); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t nvls_ctas_per_sm(int nranks, int* out) {
+  const void* fn = nranks == 2 ? reinterpret_cast<const void*>(nvls_group_kernel<2>)
+                   : nranks == 4 ? reinterpret_cast<const void*>(nvls_group_kernel<4>)
+                                 : reinterpret_cast<const void*>(nvls_group_kernel<8>);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, kNvlsBlock, 0);
+}
+
 cudaError_t launch_engine(const EngineLaunch& E, int ctas, int ranks, cudaStream_t stream) {
   const void* fn = engine_fn(E.nranks, E.dtype, E.stream != 0);
   if (fn == nullptr) return cudaErrorInvalidValue;
@@ -2129,6 +2391,9 @@ cudaError_t preload_kernels() {
       reinterpret_cast<const void*>(pack_kernel<bf16>),
       reinterpret_cast<const void*>(unpack_sgd_kernel<float>),
       reinterpret_cast<const void*>(unpack_sgd_kernel<bf16>),
+      reinterpret_cast<const void*>(nvls_group_kernel<2>),
+      reinterpret_cast<const void*>(nvls_group_kernel<4>),
+      reinterpret_cast<const void*>(nvls_group_kernel<8>),
   };
   for (const void* f : fns) {
     cudaFuncAttributes attr;

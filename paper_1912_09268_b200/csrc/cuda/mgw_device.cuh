@@ -110,6 +110,8 @@ struct GroupLaunch {
   unsigned long long* stamps;  // optional: engine-layout stamps [G][row][2] of group stamp_group
   uint32_t stamp_group;        //   (a pipeline's tail group launched standalone after the engine)
   uint32_t stamp_row;          //   row width (engine CTAs x emulated ranks)
+  float* nvls_uc;              // NVLS groups: this rank's copy of the multicast-bound buffer
+  float* nvls_mc;              //   and the multicast address of the same bytes (all P copies)
   RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
 };
 

@@ -28,9 +28,12 @@
 #include "gradsched/errors.hpp"
 #include "mgw_device.cuh"
 #include "mgwfbp.h"
+#include "nvls.hpp"
 
 namespace mgw {
 
+cudaError_t launch_nvls_group(const GroupLaunch& L, int ctas, cudaStream_t stream);
+cudaError_t nvls_ctas_per_sm(int nranks, int* out);
 cudaError_t launch_group_allreduce(const GroupLaunch& L, int ctas_per_rank, bool two_shot,
                                    bool loopback, cudaStream_t stream);
 cudaError_t max_ctas_per_sm(int nranks, bool two_shot, bool loopback, int dtype, int* out);
@@ -111,6 +114,13 @@ struct mgw_comm {
   unsigned long long* d_clock = nullptr;  // calibration spin clock
   uint64_t ce_seq = 0;  // copy-engine mode iterations run on this communicator (identical on every rank)
   int occ_cache[2][2] = {{0, 0}, {0, 0}};  // [dtype][two_shot]           // CTAs/SM of the one-shot / two-shot kernel
+  // NVLS (mgw_comm_nvls_*): multicast-bound buffer of one arena slot
+  mgw::NvlsArena* nvls = nullptr;
+  bool nvls_bound = false;
+  uint64_t nvls_min = 0;       // AUTO: fp32 groups of at least this many bytes use NVLS (0: never)
+  uint32_t nvls_chunk = 4;     // tiles per pipelined chunk of a CTA
+  int nvls_occ = 0;            // resident NVLS CTAs per SM (occupancy query, cached)
+  uint32_t nvls_skip = 0;      // profiling only (mgw_comm_set_nvls_skip): 1 skip pack/unpack, 2 skip the reduce
   // cached single-buffer plan for mgw_allreduce
   mgw_plan* ar_plan = nullptr;
   float* ar_buf = nullptr;
@@ -257,6 +267,27 @@ uint64_t default_ll_max(int nranks) {
 // 4 MiB on the 32 KiB tiles are as fast or faster (P = 2 8 MiB 24.2 vs 28.1).
 constexpr uint64_t kDefaultSmallTileMax = 3ull << 20;
 
+// NVLS: opt-in (mgw_comm_set_nvls) or forced (MGW_ALGO_NVLS); fp32 only,
+// real ranks only (a multicast object spans distinct GPUs).
+bool use_nvls(const mgw_comm* c, uint64_t bytes, int algo, int dtype) {
+  if (algo == MGW_ALGO_NVLS) {
+    require(c->nvls_bound, "MGW_ALGO_NVLS needs mgw_comm_nvls_create / _join / _bind first");
+    require(dtype == MGW_DTYPE_F32, "MGW_ALGO_NVLS reduces fp32 gradients only");
+    return true;
+  }
+  return algo == MGW_ALGO_AUTO && c->nvls_bound && c->nvls_min > 0 && bytes >= c->nvls_min &&
+         dtype == MGW_DTYPE_F32 && c->nranks > 1;
+}
+
+// NVLS grid: one CTA per tile up to (resident CTAs per SM) x SMs, capped by
+// mgw_comm_set_max_ctas.
+int nvls_grid(mgw_comm* c, uint32_t n_tiles) {
+  if (c->nvls_occ == 0) ck(nvls_ctas_per_sm(c->nranks, &c->nvls_occ), "nvls occupancy");
+  int cap = std::min(std::max(1, c->nvls_occ) * c->num_sms, kMaxCtas);
+  if (c->max_ctas > 0) cap = std::min(cap, c->max_ctas);
+  return static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(n_tiles, static_cast<uint32_t>(cap))));
+}
+
 bool use_two_shot(const mgw_comm* c, uint64_t bytes, int algo) {
   if (c->nranks == 1) return false;
   if (algo == MGW_ALGO_ONESHOT) return false;
@@ -309,6 +340,16 @@ void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStre
   for (int r = 0; r < p->n_views; ++r) {
     L.views[r] = make_view(c, r, p->d_grads + static_cast<size_t>(r) * p->L,
                            p->d_weights + static_cast<size_t>(r) * p->L);
+  }
+  if (use_nvls(c, group_bytes(p, g), algo, p->dtype)) {
+    L.nvls_uc = nvls_uc(c->nvls);
+    L.nvls_mc = nvls_mc(c->nvls);
+    L.chunk = c->nvls_chunk;
+    L.min_chunks = c->nvls_skip;  // (the NVLS kernel has no min_chunks; the field carries the profiling mask)
+    L.ll_pkt = kNoLL;
+    ck(launch_nvls_group(L, nvls_grid(c, L.n_tiles), stream), "nvls group launch");
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    return;
   }
   const bool two = use_two_shot(c, group_bytes(p, g), algo);
   L.ll_pkt = two ? kNoLL : p->ll_pkt[g];
@@ -648,12 +689,81 @@ int mgw_comm_get_oneshot_max(const mgw_comm* c, uint64_t* bytes) {
   MGW_CATCH
 }
 
+size_t mgw_nvls_handle_size(void) { return mgw::kNvlsBlobBytes; }
+
+int mgw_comm_nvls_supported(const mgw_comm* c, int* supported) {
+  MGW_TRY {
+    require(c != nullptr && supported != nullptr, "NULL argument");
+    *supported = (!c->loopback && c->nranks > 1 && mgw::nvls_supported(c->device)) ? 1 : 0;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_nvls_create(mgw_comm* c, void* handle_out) {
+  MGW_TRY {
+    require(c != nullptr && handle_out != nullptr, "NULL argument");
+    require(!c->loopback && c->nranks > 1, "NVLS needs a real communicator of P > 1 ranks");
+    require(c->nvls == nullptr, "NVLS already set up on this communicator");
+    require(c->peers_ready, "open the peers (mgw_comm_open_peers) before NVLS");
+    mgw::set_device(c);
+    c->nvls = mgw::nvls_create(c->device, c->rank, c->nranks, c->arena_elems * sizeof(float), handle_out);
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_nvls_join(mgw_comm* c, const void* handle0) {
+  MGW_TRY {
+    require(c != nullptr && handle0 != nullptr && c->nvls != nullptr, "call mgw_comm_nvls_create first");
+    mgw::set_device(c);
+    mgw::nvls_join(c->nvls, handle0);
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_nvls_bind(mgw_comm* c) {
+  MGW_TRY {
+    require(c != nullptr && c->nvls != nullptr, "call mgw_comm_nvls_create / _join first");
+    mgw::set_device(c);
+    mgw::nvls_bind(c->nvls);
+    c->nvls_bound = true;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_nvls_ready(const mgw_comm* c, int* ready) {
+  MGW_TRY {
+    require(c != nullptr && ready != nullptr, "NULL argument");
+    *ready = c->nvls_bound ? 1 : 0;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_set_nvls(mgw_comm* c, uint64_t min_bytes, uint32_t chunk_tiles) {
+  MGW_TRY {
+    require(c != nullptr, "comm is NULL");
+    require(min_bytes == 0 || c->nvls_bound, "NVLS is not set up on this communicator");
+    require(chunk_tiles >= 1 && chunk_tiles <= 16, "chunk_tiles must be in [1, 16]");
+    c->nvls_min = min_bytes;
+    c->nvls_chunk = chunk_tiles;
+  }
+  MGW_CATCH
+}
+
+int mgw_comm_set_nvls_skip(mgw_comm* c, uint32_t mask) {
+  MGW_TRY {
+    require(c != nullptr && mask <= 3, "mask must be 0..3");
+    c->nvls_skip = mask;
+  }
+  MGW_CATCH
+}
+
 int mgw_comm_destroy(mgw_comm* c) {
   MGW_TRY {
     if (c == nullptr) return 0;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     mgw::destroy_plan(c->ar_plan);
+    mgw::nvls_destroy(c->nvls);
     for (void* p : c->opened) cudaIpcCloseMemHandle(p);
     for (float* a : c->arenas) cudaFree(a);
     for (uint32_t* s : c->signals) cudaFree(s);
@@ -787,6 +897,15 @@ int mgw_allreduce(mgw_comm* c, float* buf, size_t n, int algo, void* stream) {
     L.ll_pkt = mgw::kNoLL;
     L.mbase = 0;
     L.views[0] = mgw::make_view(c, 0, p->d_grads, p->d_weights);
+    if (mgw::use_nvls(c, static_cast<uint64_t>(n) * 4, algo, MGW_DTYPE_F32)) {
+      L.nvls_uc = mgw::nvls_uc(c->nvls);
+      L.nvls_mc = mgw::nvls_mc(c->nvls);
+      L.chunk = c->nvls_chunk;
+      ck(mgw::launch_nvls_group(L, mgw::nvls_grid(c, L.n_tiles), static_cast<cudaStream_t>(stream)),
+         "nvls all-reduce launch");
+      mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+      return 0;
+    }
     const bool two = mgw::use_two_shot(c, static_cast<uint64_t>(n) * 4, algo);
     ck(mgw::launch_group_allreduce(L, mgw::grid_for(c, L.n_tiles, two), two, false,
                                    static_cast<cudaStream_t>(stream)),

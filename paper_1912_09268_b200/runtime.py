@@ -17,7 +17,7 @@ from ._lib import arr
 from .gradsched import (AllReduceModel, CommMeasurement, MergePlan, ModelTrace, check,
                         fit_model)
 
-ALGO = {"auto": 0, "oneshot": 1, "twoshot": 2}
+ALGO = {"auto": 0, "oneshot": 1, "twoshot": 2, "nvls": 3}
 SGD = 1
 WRITE_GRAD = 2
 
@@ -148,6 +148,46 @@ class Comm(_Owner):
         (host-mapped flag: no CUDA call, no sync)."""
         v = C.c_int()
         check(_lib.mgw_comm_error(self.handle, C.byref(v)))
+        return bool(v.value)
+
+    def nvls_supported(self) -> bool:
+        """Multicast objects available (NVSwitch + fabric manager) and P > 1."""
+        v = C.c_int()
+        check(_lib.mgw_comm_nvls_supported(self.handle, C.byref(v)))
+        return bool(v.value)
+
+    def enable_nvls(self, min_bytes: int = 0, chunk_tiles: int = 4, group=None, exchange=None) -> None:
+        """Collective: bind every rank's copy of one arena slot to a multicast
+        object (rank 0 creates it, the peers import it; a barrier separates
+        join and bind), then route fp32 groups of >= min_bytes through the
+        switch-reduced path (0: only when asked with algo='nvls').
+        exchange: optional callable(bytes) -> list of every rank's bytes, as
+        for the IPC handles."""
+        if exchange is None:
+            import torch.distributed as dist
+
+            def exchange(blob: bytes) -> List[bytes]:
+                got: List[Optional[bytes]] = [None] * self.nranks
+                dist.all_gather_object(got, blob, group=group)
+                return got  # type: ignore[return-value]
+
+        size = _lib.mgw_nvls_handle_size()
+        blob = (C.c_uint8 * size)()
+        check(_lib.mgw_comm_nvls_create(self.handle, blob))
+        h0 = list(exchange(bytes(blob)))[0]
+        check(_lib.mgw_comm_nvls_join(self.handle, (C.c_uint8 * size).from_buffer_copy(h0)))
+        exchange(b"joined")  # every GPU is in the multicast group before anyone binds
+        check(_lib.mgw_comm_nvls_bind(self.handle))
+        exchange(b"bound")
+        self.set_nvls(min_bytes, chunk_tiles)
+
+    def set_nvls(self, min_bytes: int, chunk_tiles: int = 4) -> None:
+        check(_lib.mgw_comm_set_nvls(self.handle, int(min_bytes), int(chunk_tiles)))
+
+    @property
+    def nvls_ready(self) -> bool:
+        v = C.c_int()
+        check(_lib.mgw_comm_nvls_ready(self.handle, C.byref(v)))
         return bool(v.value)
 
     def set_max_ctas(self, n: int) -> None:

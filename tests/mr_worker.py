@@ -35,6 +35,75 @@ def inputs(P):
     return g, w
 
 
+def group_oracle(g_np, w_np, tags, thr, write_grad):
+    """One iteration of the oracle, group by group: NVLS numerics for fp32
+    groups of >= thr bytes (thr 0: every group), rank order otherwise."""
+    heads = [i for i, t in enumerate(tags) if i == 0 or t == 0] + [len(tags)]
+    for a, b in zip(heads, heads[1:]):
+        nbytes = 4 * sum(COUNTS[a:b])
+        fn = pyoracle.allreduce_sgd_nvls if (thr == 0 or nbytes >= thr) else pyoracle.allreduce_sgd
+        gs_ = [per[a:b] for per in g_np]
+        ws_ = [per[a:b] for per in w_np]
+        fn(gs_, ws_, [0] + [1] * (b - a - 1), LR, write_grad=write_grad)
+
+
+def nvls_checks(comm, plan, tags, tr, rank, P):
+    failures = []
+    for algo, thr in (("nvls", 0), ("auto", 1 << 20)):
+        comm.set_nvls(thr if algo == "auto" else 0, 2)
+        g_np, w_np = inputs(P)
+        g_dev = [torch.from_numpy(a.copy()).cuda() for a in g_np[rank]]
+        w_dev = [torch.from_numpy(a.copy()).cuda() for a in w_np[rank]]
+        dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+        for _ in range(3):
+            for g in reversed(range(dp.n_groups)):
+                dp.group_allreduce(g, LR, rt.SGD | rt.WRITE_GRAD, algo)
+            group_oracle(g_np, w_np, tags, thr, True)
+        torch.cuda.synchronize()
+        for l in range(len(COUNTS)):
+            if not np.array_equal(w_dev[l].cpu().numpy(), w_np[rank][l]):
+                failures.append(f"nvls {algo} weights layer {l}")
+            if not np.array_equal(g_dev[l].cpu().numpy(), g_np[rank][l]):
+                failures.append(f"nvls {algo} grads layer {l}")
+        dp.close()
+    # pipeline: engine (AUTO protocol: streamed) + the last-ready group as a
+    # standalone launch, NVLS when it is >= 1 MiB
+    comm.set_nvls(1 << 20, 2)
+    g_np, w_np = inputs(P)
+    g_dev = [torch.from_numpy(a.copy()).cuda() for a in g_np[rank]]
+    w_dev = [torch.from_numpy(a.copy()).cuda() for a in w_np[rank]]
+    dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
+    pipe = rt.Pipeline(dp, tr, LR, record_group_times=True, l2_flush_bytes=0, engine_ctas=-1)
+    pipe.run(3)
+    torch.cuda.synchronize()
+    heads = [i for i, t in enumerate(tags) if i == 0 or t == 0] + [len(tags)]
+    tail_bytes = 4 * sum(COUNTS[heads[0]:heads[1]])
+    for _ in range(3):  # the engine's groups [1, G) are push groups; group 0 is the tail launch
+        for a, b in zip(heads, heads[1:]):
+            fn = pyoracle.allreduce_sgd_nvls if (a == 0 and tail_bytes >= (1 << 20)) else pyoracle.allreduce_sgd
+            fn([per[a:b] for per in g_np], [per[a:b] for per in w_np], [0] + [1] * (b - a - 1), LR)
+    for l in range(len(COUNTS)):
+        if not np.array_equal(w_dev[l].cpu().numpy(), w_np[rank][l]):
+            failures.append(f"nvls pipeline weights layer {l}")
+    pipe.close()
+    dp.close()
+    # plain SUM all-reduce through the switch vs NCCL (norm-wise bound)
+    for n in (1 << 10, (1 << 20) + 3, 16 << 20):
+        x = torch.rand(n, device="cuda") * 2 - 1 + rank
+        mine, ref = x.clone(), x.clone()
+        comm.allreduce_(mine, algo="nvls")
+        dist.all_reduce(ref)
+        absx = x.abs()
+        dist.all_reduce(absx)
+        torch.cuda.synchronize()
+        if not bool(((mine - ref).abs() <= 1e-6 * absx + 1e-30).all()):
+            failures.append(f"nvls allreduce vs nccl n={n}")
+    meas = comm.calibrate([1 << 20, 16 << 20, 64 << 20], warmup=2, reps=5, algo="nvls")
+    if rank == 0:
+        print("nvls calibration", [(m.size_bytes, round(m.time_sec * 1e6, 1)) for m in meas], flush=True)
+    return failures
+
+
 def main():
     rank, P, local = D.init("nccl")
     torch.cuda.set_device(local)
@@ -192,6 +261,18 @@ def main():
         pipe.close()
         dp.close()
     comm.set_protocol("chunked")
+
+    # NVLS (switch-reduced, opt-in): bit-exact vs the oracle's exact-sum
+    # variant (== the rank-order oracle at P = 2). Every group forced through
+    # NVLS; then AUTO with a 1 MiB threshold (mixed NVLS / push groups), the
+    # pipeline (persistent engine + the tail group as a standalone NVLS
+    # launch), and the plain SUM all-reduce vs NCCL.
+    if comm.nvls_supported():
+        comm.enable_nvls(min_bytes=0, chunk_tiles=2)
+        failures += nvls_checks(comm, plan, tags, tr, rank, P)
+        comm.set_nvls(0)
+    else:
+        print(f"rank {rank}: NVLS unsupported, skipped", flush=True)
 
     meas = comm.calibrate([4096 << k for k in range(0, 12, 2)], warmup=2, reps=5)  # <= arena
     meas_e = comm.calibrate_engine([4096 << k for k in range(0, 12, 2)], warmup=1, reps=3)

@@ -90,6 +90,36 @@ def test_oracle_reduction_matches_numpy_rank_order(P):
             assert np.array_equal(grads[r][l], want_g[l])
 
 
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_oracle_nvls_variant_is_the_exact_sum_rounded_once(P):
+    """NVLS numerics (the NVSwitch's multimem.ld_reduce, measured on B200 by
+    tools/nvls_probe.cu): the exact sum of the P scaled fp32 values, rounded
+    once to fp32 — checked against rational arithmetic; at P = 2 it is the
+    rank-order sum bit for bit."""
+    from fractions import Fraction
+
+    rng = np.random.default_rng(100 + P)
+    counts = [0, 1, 7, 300, 33]
+    grads = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(P)]
+    weights = [[rng.uniform(-1, 1, c).astype(np.float32) for c in counts] for _ in range(P)]
+    s = np.float32(1.0 / P)
+    exact = [np.array([float(sum(Fraction(float(grads[r][l][j] * s)) for r in range(P)))
+                       for j in range(counts[l])], dtype=np.float64).astype(np.float32) for l in range(len(counts))]
+    want_w = [[(weights[r][l] - np.float32(0.01) * exact[l]).astype(np.float32) for l in range(len(counts))]
+              for r in range(P)]
+    g_rank = [[g.copy() for g in per] for per in grads]
+    w_rank = [[w.copy() for w in per] for per in weights]
+    pyoracle.allreduce_sgd(g_rank, w_rank, [0, 1, 0, 1, 0], 0.01, write_grad=True)
+    pyoracle.allreduce_sgd_nvls(grads, weights, [0, 1, 0, 1, 0], 0.01, write_grad=True)
+    for l in range(len(counts)):
+        for r in range(P):
+            assert np.array_equal(grads[r][l], exact[l])
+            assert np.array_equal(weights[r][l], want_w[r][l])
+            if P == 2:
+                assert np.array_equal(grads[r][l], g_rank[r][l])
+                assert np.array_equal(weights[r][l], w_rank[r][l])
+
+
 def test_oracle_pack_layout():
     rng = np.random.default_rng(7)
     grads = [rng.uniform(-1, 1, c).astype(np.float32) for c in (5, 0, 9)]

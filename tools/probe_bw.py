@@ -43,14 +43,22 @@ for knob, proto in [(k, p) for p in os.environ.get("PROTOS", "stream").split(","
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             out.append((f"engine {algo} ctas={ctas}{tag}", [f * s / tt / 1e9 for s, tt in zip(sizes, t.tolist())],
                         [tt * 1e6 for tt in t.tolist()]))
-for algo in os.environ.get("STANDALONE", "twoshot").split(","):
-    if not algo:
-        continue
-    m = comm.calibrate(sizes, warmup=2, reps=5, algo=algo)
+standalone = [a for a in os.environ.get("STANDALONE", "twoshot").split(",") if a]
+if "nvls" in standalone:  # NVLS_CHUNKS: tiles per pipelined chunk of the NVLS kernel
+    comm.enable_nvls(0, 4)
+runs = [(a, c, k) for a in standalone for c in ([int(x) for x in os.environ.get("NVLS_CHUNKS", "4").split(",")]
+                                                  if a == "nvls" else [0])
+        for k in ([int(x) for x in os.environ.get("NVLS_SKIP", "0").split(",")] if a == "nvls" else [0])]
+for algo, chunk, skip in runs:
+    if algo == "nvls":
+        comm.set_nvls(0, chunk)
+        from paper_1912_09268_b200 import _lib
+        rt.check(_lib.mgw_comm_set_nvls_skip(comm.handle, skip))
+    m = comm.calibrate(sizes, warmup=2, reps=int(os.environ.get("SREPS", "5")), algo=algo)
     t = torch.tensor([x.time_sec for x in m], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    out.append((f"standalone {algo} (grid=occ*SMs)", [f * s / tt / 1e9 for s, tt in zip(sizes, t.tolist())],
-                [tt * 1e6 for tt in t.tolist()]))
+    name = f"standalone {algo}" + (f" chunk={chunk} skip={skip}" if algo == "nvls" else " (grid=occ*SMs)")
+    out.append((name, [f * s / tt / 1e9 for s, tt in zip(sizes, t.tolist())], [tt * 1e6 for tt in t.tolist()]))
 nccl = []
 for s in sizes:
     x = torch.ones(s // 4, device=dev)
