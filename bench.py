@@ -68,8 +68,8 @@ def parse_args():
     ap.add_argument("--oneshot-max", type=int, default=0, help="0: the library default for N")
     ap.add_argument("--nvls", type=float, default=0.0,
                     help="MiB: route fp32 standalone group launches of at least this size through the NVLS "
-                         "(switch-reduced) variant (0: off, the default; N > 1 only). The bus_gbs table "
-                         "measures NVLS beside NCCL whenever the pool supports multicast objects.")
+                         "(switch-reduced) variant (N > 1 only; 0: off, the default). A negative value sets "
+                         "NVLS up for the bus_gbs table only (measured beside NCCL), data path unchanged.")
     ap.add_argument("--cost", default="linear", choices=["linear", "table"],
                     help="linear: the reference's a + b*M (bit-exact optimal_plan); table: B200 extension, the same "
                          "DP on the calibration's piecewise measured curve")
@@ -484,15 +484,15 @@ def main():
         comm.set_protocol(args.protocol)  # (P = 1 always runs the TMA-fed single-rank engine)
         if args.stream_batches:
             comm.set_stream_batches(*(int(x) for x in args.stream_batches.split(",")))
-    # NVLS (switch-reduced two-shot, opt-in): set up whenever the pool has
-    # multicast objects (the bus table measures it); the data path uses it
-    # only with --nvls
-    nvls = "n/a (N = 1)" if N == 1 else "unsupported on this pool"
-    if N > 1 and not bf16:
+    # NVLS (switch-reduced two-shot, opt-in): --nvls X routes
+    # groups >= X MiB through it; --nvls -1 only measures it (bus_gbs)
+    nvls = "off" if N > 1 else "n/a (N = 1)"
+    if N > 1 and not bf16 and args.nvls != 0:
+        nvls = "unsupported on this pool"
         ok = torch.tensor([1.0 if comm.nvls_supported() else 0.0], device=dev)
         torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
         if ok.item() > 0:
-            comm.enable_nvls(int(args.nvls * (1 << 20)))
+            comm.enable_nvls(int(max(args.nvls, 0.0) * (1 << 20)))
             nvls = (f"on for groups >= {args.nvls} MiB" if args.nvls > 0 else "measured only (bus_gbs)")
 
     # ---- N1: on-box calibration of the fused engine kernel at this N

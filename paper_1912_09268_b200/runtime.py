@@ -171,14 +171,26 @@ class Comm(_Owner):
                 dist.all_gather_object(got, blob, group=group)
                 return got  # type: ignore[return-value]
 
+        def phase(fn, payload=lambda: b"") -> List[bytes]:
+            # every rank reports its outcome with the phase's payload, so a
+            # failure on one rank raises on all of them (nobody is left
+            # waiting in the next exchange)
+            err = None
+            try:
+                fn()
+            except Exception as e:  # noqa: BLE001 - re-raised below on every rank
+                err = e
+            got = list(exchange((b"1" if err is None else b"0") + payload()))
+            if any(g[:1] != b"1" for g in got):
+                raise RuntimeError(f"NVLS setup failed on rank(s) "
+                                   f"{[r for r, g in enumerate(got) if g[:1] != b'1']}") from err
+            return [g[1:] for g in got]
+
         size = _lib.mgw_nvls_handle_size()
         blob = (C.c_uint8 * size)()
-        check(_lib.mgw_comm_nvls_create(self.handle, blob))
-        h0 = list(exchange(bytes(blob)))[0]
-        check(_lib.mgw_comm_nvls_join(self.handle, (C.c_uint8 * size).from_buffer_copy(h0)))
-        exchange(b"joined")  # every GPU is in the multicast group before anyone binds
-        check(_lib.mgw_comm_nvls_bind(self.handle))
-        exchange(b"bound")
+        h0 = phase(lambda: check(_lib.mgw_comm_nvls_create(self.handle, blob)), lambda: bytes(blob))[0]
+        phase(lambda: check(_lib.mgw_comm_nvls_join(self.handle, (C.c_uint8 * size).from_buffer_copy(h0))))
+        phase(lambda: check(_lib.mgw_comm_nvls_bind(self.handle)))  # every GPU joined before anyone binds
         self.set_nvls(min_bytes, chunk_tiles)
 
     def set_nvls(self, min_bytes: int, chunk_tiles: int = 4) -> None:
