@@ -2009,13 +2009,13 @@ __global__ void __launch_bounds__(kNvlsBlock, 2) nvls_group_kernel(const __grid_
     __syncthreads();
     if (!cx.abort) {
       if (!hbm) {
-        if (do_red && !(L.min_chunks & 2u)) {
+        if (do_red && !(L.nvls_skip & 2u)) {
           nvls_reduce(L.nvls_mc, s_red, nt_of(s - 1), tid);
           asm volatile("fence.acq_rel.sys;" ::: "memory");  // the multicast stores before the barrier's release
         }
       } else {
-        if (do_pack && !(L.min_chunks & 1u)) nvls_pack(L.nvls_uc, s_pack, nt_of(s), L.scale, tid);
-        if (do_unpack && !(L.min_chunks & 1u)) nvls_unpack(L.nvls_uc, s_unpack, nt_of(s - 2), L.lr, L.epilogue, tid);
+        if (do_pack && !(L.nvls_skip & 1u)) nvls_pack(L.nvls_uc, s_pack, nt_of(s), L.scale, tid);
+        if (do_unpack && !(L.nvls_skip & 1u)) nvls_unpack(L.nvls_uc, s_unpack, nt_of(s - 2), L.lr, L.epilogue, tid);
       }
     }
     if (s < nchunks + 1) cta_barrier(v, P, cx);  // the last step (unpack only) needs none

@@ -112,6 +112,7 @@ struct GroupLaunch {
   uint32_t stamp_row;          //   row width (engine CTAs x emulated ranks)
   float* nvls_uc;              // NVLS groups: this rank's copy of the multicast-bound buffer
   float* nvls_mc;              //   and the multicast address of the same bytes (all P copies)
+  uint32_t nvls_skip;          //   profiling mask (mgw_comm_set_nvls_skip; 0 in production)
   RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
 };
 
