@@ -79,9 +79,9 @@ def parse_args():
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"],
                     help="gradient / merge-arena type (bf16: fp32 accumulation, fp32 master weights)")
     ap.add_argument("--protocol", default="auto", choices=["auto", "chunked", "stream"],
-                    help="fused all-reduce protocol at N > 1: auto (the library default: streamed engine, the "
-                         "last-ready group as a chunked launch), chunked (per-chunk cross-rank barriers "
-                         "everywhere) or stream (per-tile delivery counts everywhere)")
+                    help="fused all-reduce protocol at N > 1: auto (the library default: chunked), chunked "
+                         "(per-chunk cross-rank barriers) or stream (per-tile delivery counts in the engine, the "
+                         "last-ready group as a chunked launch)")
     ap.add_argument("--stream-batches", default="",
                     help="CREDIT,AG: streamed-protocol publication batches (default: the library's 8,4)")
     ap.add_argument("--engine-ctas", type=int, default=-1,
@@ -625,8 +625,10 @@ def main():
     peaks = measured_peaks()
     gbytes = [dplans["mgwfbp"].group_span(g)[2] for g in range(dplans["mgwfbp"].n_groups)]
     roof = {}
+    engine_protocol = "none (one launch per group)"
     if args.engine_ctas != 0:
         D.barrier()
+        engine_protocol = pipes["headline"].engine_protocol
         drain = pipes["headline"].drain(max(3, min(args.steps, 20)))
         kern_s = D.max_over_ranks(statistics.mean(drain) / 1e3, dev)
         w_per_g = 4 / esz  # fp32 weight bytes per gradient byte
@@ -673,6 +675,20 @@ def main():
                                       "idle engine, cold L2)"}})
         if N > 1:
             roof["frac_vs_770"] = achieved / NVLINK_PEER_GBS
+            # the same plan drained by the other protocol's engine (the
+            # streamed one wins drains of many ready groups)
+            alt = "stream" if engine_protocol == "chunked" else "chunked"
+            comm.set_protocol(alt)
+            p_alt = rt.Pipeline(dplans["mgwfbp"], trace, args.lr, args.algo, record_group_times=False,
+                                l2_flush_bytes=flush, engine_ctas=args.engine_ctas)
+            comm.set_protocol(args.protocol)
+            D.barrier()
+            d_alt = p_alt.drain(max(3, min(args.steps, 20)))
+            p_alt.close()
+            alt_s = D.max_over_ranks(statistics.mean(d_alt) / 1e3, dev)
+            roof["other_protocol_drain"] = {"protocol": alt, "achieved": algo_bytes / alt_s / 1e9,
+                                            "frac": algo_bytes / alt_s / 1e9 / peak,
+                                            "launch_ms_mean": alt_s * 1e3}
 
     # merged all-reduce bus GB/s = 2(P-1)/P * S / t: ours (fused kernel, from
     # the calibration sweep) next to NCCL (torch.distributed.all_reduce, same
@@ -694,16 +710,16 @@ def main():
             ev[1].synchronize()
             ncclt.append(D.max_over_ranks(ev[0].elapsed_time(ev[1]) / 10 / 1e3, dev))
             del x
-        # the isolated-group path of the pipeline (its tail launch: chunked)
-        # beside the AUTO engine's streamed calibration above
-        iso = [None] * len(big)
-        if comm.protocol == "auto":
-            comm.set_protocol("chunked")
-            mm = comm.calibrate_engine([m.size_bytes for m in big], warmup=2, reps=9, algo=args.algo,
-                                       engine_ctas=args.engine_ctas if args.engine_ctas != 0 else -1,
-                                       dtype=rt.BF16 if bf16 else rt.F32)
-            comm.set_protocol("auto")
-            iso = [D.max_over_ranks(x.time_sec, dev) for x in mm]
+        # the other protocol beside this run's (the calibration above): one
+        # isolated group per size; the table reports both and the best
+        mine_proto = "chunked" if comm.protocol in ("auto", "chunked") else "stream"
+        alt_proto = "stream" if mine_proto == "chunked" else "chunked"
+        comm.set_protocol(alt_proto)
+        mm = comm.calibrate_engine([m.size_bytes for m in big], warmup=2, reps=9, algo=args.algo,
+                                   engine_ctas=args.engine_ctas if args.engine_ctas != 0 else -1,
+                                   dtype=rt.BF16 if bf16 else rt.F32)
+        comm.set_protocol(args.protocol)
+        iso = [D.max_over_ranks(x.time_sec, dev) for x in mm]
         nv = [None] * len(big)
         if comm.nvls_ready:
             mm = comm.calibrate([m.size_bytes for m in big], warmup=2, reps=9, algo="nvls")
@@ -713,11 +729,8 @@ def main():
             bus[str(m.size_bytes)] = {"mgwfbp": f / m.time_sec, "nccl": f / tn,
                                       "mgwfbp_frac_900": f / m.time_sec / NVLINK_GBS}
             if ti:
-                # best of the library's two protocols for one isolated group
-                bus[str(m.size_bytes)]["mgwfbp_streamed"] = f / m.time_sec
-                bus[str(m.size_bytes)]["mgwfbp_chunked"] = f / ti
-                bus[str(m.size_bytes)]["mgwfbp"] = f / min(ti, m.time_sec)
-                bus[str(m.size_bytes)]["mgwfbp_frac_900"] = f / min(ti, m.time_sec) / NVLINK_GBS
+                bus[str(m.size_bytes)]["mgwfbp_" + mine_proto] = f / m.time_sec
+                bus[str(m.size_bytes)]["mgwfbp_" + alt_proto] = f / ti
             if tv:
                 bus[str(m.size_bytes)]["nvls_standalone"] = f / tv
 
@@ -748,6 +761,7 @@ def main():
             "gpu": {"comm": ("persistent engine, %s CTAs" % ("1/SM" if args.engine_ctas < 0 else args.engine_ctas))
                             if args.engine_ctas else "one fused kernel launch per group",
                     "algo": args.algo, "tuning": comm.tuning(), "ipc_ranks_mapped": peers, "nvls": nvls,
+                    "engine_protocol": engine_protocol,
                     "l2_flush": f"{args.l2_flush_mib} MiB streaming stores on the comm stream during the forward "
                                 "replay, every iteration"},
             "calibration": {"plan_model": {"a_us": model.a * 1e6, "b_ps_per_byte": model.b * 1e12, "how": model_how},

@@ -211,13 +211,16 @@ int mgw_comm_get_oneshot_max(const mgw_comm* comm, uint64_t* bytes);
  *    packets; 0 disables LL.
  *  small_tile_max: groups below this many bytes are cut into 8 KiB tiles
  *    (more CTAs) instead of 32 KiB tiles.
- *  protocol: MGW_PROTO_AUTO (default) — persistent engines run streamed
- *    (their replay pipelines launch the last-ready group as a chunked
- *    standalone launch after the engine), standalone group launches run
- *    chunked; MGW_PROTO_STREAM — everything streamed: the producer warp
- *    streams tiles and publishes per-tile delivery counts, the data warps
- *    consume them as they arrive (no barrier after the launch's entry
- *    barrier); MGW_PROTO_CHUNKED — everything chunked: a CTA's tiles run in
+ *  protocol: MGW_PROTO_AUTO (default) — chunked at P > 1 (the shorter
+ *    iteration for every measured MG-WFBP plan), the TMA-fed engine at
+ *    P = 1; MGW_PROTO_STREAM — the persistent engine streams: the producer
+ *    warp streams tiles and publishes per-tile delivery counts, the data
+ *    warps consume them as they arrive (no barrier after the launch's entry
+ *    barrier), and a replay pipeline launches its last-ready group as a
+ *    chunked standalone launch after the engine (an isolated large group is
+ *    the streamed protocol's weak case); standalone launches stay chunked
+ *    unless STREAM is set; MGW_PROTO_CHUNKED — everything chunked: a CTA's
+ *    tiles run in
  *    pipelined chunks with one cross-rank barrier per chunk (chunk_tiles /
  *    min_chunks: at most chunk_tiles tiles per chunk, two-shot chunk_tiles /
  *    P super-tiles, and at least min_chunks chunks when the CTA owns enough
@@ -331,6 +334,9 @@ int mgw_pipeline_drain(mgw_pipeline* pipe, int iters, float* ms_out);
  * (start, end) %globaltimer stamps of every group, 2*G values in group
  * order (zero for groups without tiles). */
 int mgw_pipeline_stamps(mgw_pipeline* pipe, uint64_t* stamps_2g);
+/* 1 in *streamed when the pipeline's persistent engine runs the streamed
+ * protocol (0: chunked, or no engine). */
+int mgw_pipeline_streamed(const mgw_pipeline* pipe, int* streamed);
 /* Debug: the raw per-(group, CTA) (start, end) %globaltimer stamps of the
  * last engine launch, [G][cols][2] (cols = CTAs of all emulated ranks). */
 int mgw_pipeline_stamps_raw(mgw_pipeline* pipe, uint64_t* out, size_t cap, size_t* cols_out);

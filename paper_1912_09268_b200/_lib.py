@@ -85,6 +85,7 @@ mgw_comm_set_ll_max = _proto("mgw_comm_set_ll_max", [vp, C.c_uint64])
 mgw_comm_set_small_tile_max = _proto("mgw_comm_set_small_tile_max", [vp, C.c_uint64])
 mgw_comm_set_chunk_tiles = _proto("mgw_comm_set_chunk_tiles", [vp, C.c_uint32, C.c_uint32])
 mgw_comm_set_protocol = _proto("mgw_comm_set_protocol", [vp, C.c_int])
+mgw_pipeline_streamed = _proto("mgw_pipeline_streamed", [vp, C.POINTER(C.c_int)])
 mgw_comm_set_stream_batches = _proto("mgw_comm_set_stream_batches", [vp, C.c_uint32, C.c_uint32])
 mgw_comm_get_protocol = _proto("mgw_comm_get_protocol", [vp, C.POINTER(C.c_int)])
 mgw_comm_error = _proto("mgw_comm_error", [vp, C.POINTER(C.c_int)])

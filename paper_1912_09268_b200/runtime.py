@@ -122,9 +122,10 @@ class Comm(_Owner):
         check(_lib.mgw_comm_set_chunk_tiles(self.handle, int(max_tiles), int(min_chunks)))
 
     def set_protocol(self, protocol: str) -> None:
-        """'auto' (default: engines streamed, standalone launches chunked),
+        """'auto' (default: chunked at P > 1, the TMA-fed engine at P = 1),
         'stream' (per-tile delivery counts, no barrier after the entry
-        barrier) or 'chunked' (one cross-rank barrier per chunk)."""
+        barrier; pipelines launch their last-ready group chunked) or
+        'chunked' (one cross-rank barrier per chunk)."""
         check(_lib.mgw_comm_set_protocol(self.handle, PROTOCOLS[protocol]))
 
     def set_stream_batches(self, credit_batch: int = 8, ag_batch: int = 4) -> None:
@@ -409,6 +410,13 @@ class Pipeline:
         end = max(ends) if ends else rend
         return {"replay_us": (rend - t0) / 1e3, "comm_end_us": (end - t0) / 1e3,
                 "tail_us": (end - rend) / 1e3}
+
+    @property
+    def engine_protocol(self) -> str:
+        """'stream' or 'chunked' for an engine pipeline ('none' without one)."""
+        v = C.c_int()
+        check(_lib.mgw_pipeline_streamed(self.handle, C.byref(v)))
+        return "stream" if v.value else ("chunked" if self.engine_ctas != 0 else "none")
 
     def group_times_ms(self) -> List[float]:
         out = (C.c_float * max(1, self.dplan.n_groups))()
