@@ -66,10 +66,12 @@ def algo_mix(dp, comm):
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
-@pytest.mark.parametrize("protocol", ["stream", "chunked"])
+@pytest.mark.parametrize("protocol", ["stream", "chunked", "auto"])
 def test_engine_pipeline_ragged_bit_exact(P, protocol):
     """Replay pipeline, 3 iterations, LL + one-shot + two-shot groups in one
-    engine launch; the rank-order result on every emulated rank."""
+    engine launch; the rank-order result on every emulated rank. AUTO (the
+    default) runs the chunked engine at P > 1; STREAM the streamed engine
+    plus the last-ready group as a chunked launch after it."""
     rng = np.random.default_rng(700 + P)
     counts = RAGGED
     t_b = list(rng.uniform(2e-5, 2e-4, len(counts)))
@@ -85,6 +87,7 @@ def test_engine_pipeline_ragged_bit_exact(P, protocol):
     comm.set_protocol(protocol)
     dp = rt.DevicePlan(comm, g_dev, w_dev, plan)
     pipe = rt.Pipeline(dp, tr, LR, record_group_times=True, l2_flush_bytes=32 << 20, engine_ctas=-1)
+    assert pipe.engine_protocol == ("stream" if protocol == "stream" else "chunked")
     ms = pipe.run(3)
     compute_ms = (tr.forward_time + sum(t_b)) * 1e3
     assert all(m >= compute_ms * 0.999 for m in ms), (ms, compute_ms)
