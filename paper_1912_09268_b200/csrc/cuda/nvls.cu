@@ -7,6 +7,8 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <algorithm>
+#include <cerrno>
 #include <cstring>
 #include <string>
 
@@ -178,9 +180,7 @@ void nvls_join(NvlsArena* a, const void* blob0) {
     cu(r, "import");
     a->have_mc = true;
   }
-  CUdevice dev = 0;
-  dev = static_cast<CUdevice>(a->device);
-  cu(d.mc_add(a->mc, dev), "cuMulticastAddDevice");
+  cu(d.mc_add(a->mc, static_cast<CUdevice>(a->device)), "cuMulticastAddDevice");
   a->added = true;
 }
 
