@@ -23,6 +23,7 @@ namespace mgw {
 namespace {
 
 struct Driver {
+  decltype(&cuDeviceGet) dev_get = nullptr;
   decltype(&cuDeviceGetAttribute) dev_attr = nullptr;
   decltype(&cuMulticastGetGranularity) mc_gran = nullptr;
   decltype(&cuMulticastCreate) mc_create = nullptr;
@@ -58,7 +59,7 @@ bool entry(const char* name, F& fn) {
 const Driver& drv() {
   static const Driver d = [] {
     Driver x;
-    x.ok = entry("cuDeviceGetAttribute", x.dev_attr) && entry("cuMulticastGetGranularity", x.mc_gran) &&
+    x.ok = entry("cuDeviceGet", x.dev_get) && entry("cuDeviceGetAttribute", x.dev_attr) && entry("cuMulticastGetGranularity", x.mc_gran) &&
            entry("cuMulticastCreate", x.mc_create) && entry("cuMulticastAddDevice", x.mc_add) &&
            entry("cuMulticastBindMem", x.mc_bind) && entry("cuMulticastUnbind", x.mc_unbind) &&
            entry("cuMemCreate", x.mem_create) && entry("cuMemRelease", x.mem_release) &&
@@ -111,7 +112,9 @@ bool nvls_supported(int device) {
   const Driver& d = drv();
   if (!d.ok) return false;
   int v = 0;
-  if (d.dev_attr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, device) != CUDA_SUCCESS) return false;
+  CUdevice dev = 0;
+  if (d.dev_get(&dev, device) != CUDA_SUCCESS) return false;
+  if (d.dev_attr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev) != CUDA_SUCCESS) return false;
   return v != 0;
 }
 
@@ -180,7 +183,9 @@ void nvls_join(NvlsArena* a, const void* blob0) {
     cu(r, "import");
     a->have_mc = true;
   }
-  cu(d.mc_add(a->mc, static_cast<CUdevice>(a->device)), "cuMulticastAddDevice");
+  CUdevice dev = 0;
+  cu(d.dev_get(&dev, a->device), "cuDeviceGet");
+  cu(d.mc_add(a->mc, dev), "cuMulticastAddDevice");
   a->added = true;
 }
 
@@ -225,7 +230,8 @@ void nvls_destroy(NvlsArena* a) {
     if (a->mcp) d.va_free(a->mcp, a->bytes);
     if (a->uc_mapped) d.unmap(a->uc, a->bytes);
     if (a->uc) d.va_free(a->uc, a->bytes);
-    if (a->bound) d.mc_unbind(a->mc, static_cast<CUdevice>(a->device), 0, a->bytes);
+    CUdevice dev = 0;
+    if (a->bound && d.dev_get(&dev, a->device) == CUDA_SUCCESS) d.mc_unbind(a->mc, dev, 0, a->bytes);
     if (a->have_phys) d.mem_release(a->phys);
     if (a->have_mc) d.mem_release(a->mc);
   }
