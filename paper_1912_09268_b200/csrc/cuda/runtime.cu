@@ -715,7 +715,13 @@ int mgw_comm_nvls_join(mgw_comm* c, const void* handle0) {
   MGW_TRY {
     require(c != nullptr && handle0 != nullptr && c->nvls != nullptr, "call mgw_comm_nvls_create first");
     mgw::set_device(c);
-    mgw::nvls_join(c->nvls, handle0);
+    try {
+      mgw::nvls_join(c->nvls, handle0);
+    } catch (...) {  // leave the communicator without NVLS (a later create may retry)
+      mgw::nvls_destroy(c->nvls);
+      c->nvls = nullptr;
+      throw;
+    }
   }
   MGW_CATCH
 }
@@ -724,7 +730,13 @@ int mgw_comm_nvls_bind(mgw_comm* c) {
   MGW_TRY {
     require(c != nullptr && c->nvls != nullptr, "call mgw_comm_nvls_create / _join first");
     mgw::set_device(c);
-    mgw::nvls_bind(c->nvls);
+    try {
+      mgw::nvls_bind(c->nvls);
+    } catch (...) {
+      mgw::nvls_destroy(c->nvls);
+      c->nvls = nullptr;
+      throw;
+    }
     c->nvls_bound = true;
   }
   MGW_CATCH
