@@ -39,6 +39,7 @@
 // contraction, bit-exact with the CPU oracle's fl(fl(x0*s) + x1*s)... in
 // rank order.
 #include <cstdint>
+#include <cstdio>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -314,6 +315,7 @@ __device__ __forceinline__ void cta_barrier(const RankView& v, int P, CtaCtx& cx
   if (threadIdx.x < P && !cx.abort) {
     const int q = threadIdx.x;
     const uint32_t want = cx.count;
+    MGW_DCHECK(cta < static_cast<uint32_t>(kMaxCtas), "barrier flag CTA index");
     st_release_sys(v.signal[q] + cta * kMaxRanks + v.rank, want);
     const uint32_t* mine = v.signal[v.rank] + cta * kMaxRanks + q;
     if (!spin_until(v, [&] { return static_cast<int32_t>(ld_acquire_sys(mine) - want) >= 0; })) {
@@ -436,6 +438,7 @@ __device__ __forceinline__ void push_items(const RankView& v, uint32_t n_items, 
       const uint32_t bytes = tma_body<T>(it.t) * static_cast<uint32_t>(sizeof(T));
 #pragma unroll
       for (int q = 0; q < P; ++q) {
+        MGW_DCHECK((my_slot + it.t.moff) * sizeof(T) + bytes <= v.arena_bytes, "TMA push into a peer arena");
         if (it.mask & (1u << q)) tma_store(as<T>(v.arena[q]) + my_slot + it.t.moff, s0 + k * kStageBytes, bytes);
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -456,6 +459,7 @@ __device__ __forceinline__ void push_items(const RankView& v, uint32_t n_items, 
       const float4 x = ld4_tail<T>(src + e, it.t.len - e);  // (bf16 -> fp32 -> bf16 is exact)
 #pragma unroll
       for (int q = 0; q < P; ++q) {
+        MGW_DCHECK((my_slot + it.t.moff + e + 4) * sizeof(T) <= v.arena_bytes, "register push into a peer arena");
         if (it.mask & (1u << q)) st4<T>(as<T>(v.arena[q]) + my_slot + it.t.moff + e, x);
       }
     }
@@ -618,6 +622,7 @@ __device__ __forceinline__ void reduce_tile_staged(const RankView& v, const Tile
       if (push_to_peers) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
+          MGW_DCHECK((my_slot + t.moff + i * 4 + 4) * sizeof(T) <= v.arena_bytes, "all-gather push into a peer arena");
           if (q != v.rank) st4<T>(as<T>(v.arena[q]) + my_slot + t.moff + i * 4, s[0]);
         }
       }
@@ -715,6 +720,7 @@ __device__ __noinline__ void ll_group(const RankView& v, const Tile* tiles, uint
     x[0] = (!(t.layer & kGradUnaligned) && e + 4 <= t.len) ? ld4_stream<T>(own + e) : ld4_tail<T>(own + e, t.len - e);
 #pragma unroll
     for (int q = 0; q < P; ++q) {
+      MGW_DCHECK(pkt + kW <= kLLSlotPackets, "LL packet slot");
       if (q != me) ll_send<T>(ll_slot(v, q, me) + pkt, x[0], epoch);
     }
     load_w_batch<1>(t, i, kThreads, w, epi, wv);
@@ -1019,14 +1025,16 @@ __device__ __forceinline__ void produce_group(const RankView& v, const Tile* til
         const uint32_t bytes = tma_body<T>(it.t) * static_cast<uint32_t>(sizeof(T));
 #pragma unroll
         for (int q = 0; q < P; ++q) {
-          if (it.mask & (1u << q)) tma_store(as<T>(v.arena[q]) + my_slot + it.t.moff, s0 + k * kStageBytes, bytes);
+          MGW_DCHECK((my_slot + it.t.moff) * sizeof(T) + bytes <= v.arena_bytes, "TMA push into a peer arena");
+        if (it.mask & (1u << q)) tma_store(as<T>(v.arena[q]) + my_slot + it.t.moff, s0 + k * kStageBytes, bytes);
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         for (uint32_t e = tma_body<T>(it.t); e < it.t.len; e += 4) {  // tail (< one 16-byte vector)
           const float4 x = ld4_tail<T>(src + e, it.t.len - e);
 #pragma unroll
           for (int q = 0; q < P; ++q) {
-            if (it.mask & (1u << q)) st4<T>(as<T>(v.arena[q]) + my_slot + it.t.moff + e, x);
+            MGW_DCHECK((my_slot + it.t.moff + e + 4) * sizeof(T) <= v.arena_bytes, "register push into a peer arena");
+        if (it.mask & (1u << q)) st4<T>(as<T>(v.arena[q]) + my_slot + it.t.moff + e, x);
           }
         }
         committed<P>(v, pr, it.mask);
@@ -1041,7 +1049,8 @@ __device__ __forceinline__ void produce_group(const RankView& v, const Tile* til
         const float4 x = ld4_tail<T>(src + e, it.t.len - e);
 #pragma unroll
         for (int q = 0; q < P; ++q) {
-          if (it.mask & (1u << q)) st4<T>(as<T>(v.arena[q]) + my_slot + it.t.moff + e, x);
+          MGW_DCHECK((my_slot + it.t.moff + e + 4) * sizeof(T) <= v.arena_bytes, "register push into a peer arena");
+        if (it.mask & (1u << q)) st4<T>(as<T>(v.arena[q]) + my_slot + it.t.moff + e, x);
         }
       }
       __syncwarp();
@@ -1181,10 +1190,10 @@ __device__ __forceinline__ void consume_group(const RankView& v, const Tile* til
   const uint32_t n_super = (n_tiles + P - 1) / P;
   const uint32_t mine = j < n_super ? (n_super - j + ncta - 1) / ncta : 0;
   uint32_t prev_lo = 0, prev_n = 0;
-#pragma unroll 1
   // all-gather publication batches ramp 1, 2, 4, ... up to ag_batch from the
   // group's first owned super-tile (the peers' first AP is not held back)
   uint32_t agb = 1;
+#pragma unroll 1
   for (uint32_t b0 = 0; b0 < mine; b0 += agb, agb = agb * 2 < cs.ag_batch ? agb * 2 : cs.ag_batch) {
     const uint32_t nb = mine - b0 < agb ? mine - b0 : agb;
     uint32_t owned = 0;

@@ -88,6 +88,7 @@ struct RankView {
   uint32_t* host_err;            // host-mapped error word of the communicator (may be NULL)
   float* const* grads;           // this rank's layer gradient pointers
   float* const* weights;         // this rank's layer weight pointers (may hold NULLs)
+  uint64_t arena_bytes;          // size of every rank's merge arena (bounds checks)
   int rank;
 };
 
@@ -175,6 +176,26 @@ struct CeLaunch {
 };
 
 #ifdef __CUDACC__
+
+// Device bounds checks of the remote-write sites (arena stores, LL packets,
+// barrier flags), compiled in with -DMGW_BOUNDS_CHECK (make
+// EXTRA_NVCC=-DMGW_BOUNDS_CHECK): the pool has no compute-sanitizer, so a
+// checked build runs the parity suites instead (tools/bounds_check.sh). A
+// violation prints the site and traps (the test fails loudly).
+#ifdef MGW_BOUNDS_CHECK
+#define MGW_DCHECK(cond, what)                                                                       \
+  do {                                                                                              \
+    if (!(cond)) {                                                                                  \
+      printf("MGW_BOUNDS_CHECK failed: %s (block %d,%d thread %d)\n", what, blockIdx.x, blockIdx.y, \
+             threadIdx.x);                                                                          \
+      __trap();                                                                                     \
+    }                                                                                               \
+  } while (0)
+#else
+#define MGW_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;

@@ -231,6 +231,7 @@ RankView make_view(const mgw_comm* c, int r, float* const* grads, float* const* 
   v.host_err = c->host_err_d;
   v.grads = grads;
   v.weights = weights;
+  v.arena_bytes = std::max<uint64_t>(static_cast<uint64_t>(c->nranks) * c->arena_elems, 4) * sizeof(float);
   v.rank = c->loopback ? r : c->rank;
   return v;
 }
