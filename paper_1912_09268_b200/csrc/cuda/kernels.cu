@@ -1890,7 +1890,8 @@ __device__ __forceinline__ void nvls_describe(NvlsChunk& c, const GroupLaunch& L
 
 // Switch warps: this rank's part of every tile of the chunk through the
 // multicast address (ld_reduce -> st), kNvlsU vectors in flight per thread.
-__device__ __forceinline__ void nvls_reduce(float* mc, const NvlsChunk& c, uint32_t nt, uint32_t tid) {
+__device__ __forceinline__ void nvls_reduce(float* mc, const NvlsChunk& c, uint32_t nt, uint32_t tid,
+                                            uint64_t cap) {
   const uint32_t total = c.pre[nt];
   for (uint32_t i0 = tid; i0 < total; i0 += kNvlsU * kNvlsThreads) {
     float4 x[kNvlsU];
@@ -1901,6 +1902,7 @@ __device__ __forceinline__ void nvls_reduce(float* mc, const NvlsChunk& c, uint3
       if (i < total) {
         const uint32_t k = nvls_find(c, nt, i);
         at[u] = static_cast<size_t>(c.base[k] + (i - c.pre[k])) * 4;
+        MGW_DCHECK(at[u] + 4 <= cap, "NVLS multicast reduce / store");
         x[u] = mc_ld_reduce(mc + at[u]);
       }
     }
@@ -1912,7 +1914,8 @@ __device__ __forceinline__ void nvls_reduce(float* mc, const NvlsChunk& c, uint3
 }
 
 // HBM warps: pack (x 1/P into this rank's copy), 2 kNvlsU vectors in flight.
-__device__ __forceinline__ void nvls_pack(float* uc, const NvlsChunk& c, uint32_t nt, float scale, uint32_t tid) {
+__device__ __forceinline__ void nvls_pack(float* uc, const NvlsChunk& c, uint32_t nt, float scale, uint32_t tid,
+                                          uint64_t cap) {
   constexpr uint32_t U = 2 * kNvlsU;
   const uint32_t total = c.pre[nt];
   for (uint32_t i0 = tid; i0 < total; i0 += U * kNvlsThreads) {
@@ -1928,6 +1931,7 @@ __device__ __forceinline__ void nvls_pack(float* uc, const NvlsChunk& c, uint32_
         const float* src = c.g[k] + t.src + e;
         x[u] = (!(t.layer & kGradUnaligned) && e + 4 <= t.len) ? ld_stream_v4(src) : load_tail(src, t.len - e);
         dst[u] = uc + t.moff + e;
+        MGW_DCHECK(static_cast<uint64_t>(t.moff) + e + 4 <= cap, "NVLS pack into the local copy");
       }
     }
 #pragma unroll
@@ -2019,11 +2023,11 @@ __global__ void __launch_bounds__(kNvlsBlock, 2) nvls_group_kernel(const __grid_
     if (!cx.abort) {
       if (!hbm) {
         if (do_red && !(L.nvls_skip & 2u)) {
-          nvls_reduce(L.nvls_mc, s_red, nt_of(s - 1), tid);
+          nvls_reduce(L.nvls_mc, s_red, nt_of(s - 1), tid, L.nvls_elems);
           asm volatile("fence.acq_rel.sys;" ::: "memory");  // the multicast stores before the barrier's release
         }
       } else {
-        if (do_pack && !(L.nvls_skip & 1u)) nvls_pack(L.nvls_uc, s_pack, nt_of(s), L.scale, tid);
+        if (do_pack && !(L.nvls_skip & 1u)) nvls_pack(L.nvls_uc, s_pack, nt_of(s), L.scale, tid, L.nvls_elems);
         if (do_unpack && !(L.nvls_skip & 1u)) nvls_unpack(L.nvls_uc, s_unpack, nt_of(s - 2), L.lr, L.epilogue, tid);
       }
     }

@@ -114,6 +114,7 @@ struct GroupLaunch {
   float* nvls_uc;              // NVLS groups: this rank's copy of the multicast-bound buffer
   float* nvls_mc;              //   and the multicast address of the same bytes (all P copies)
   uint32_t nvls_skip;          //   profiling mask (mgw_comm_set_nvls_skip; 0 in production)
+  uint64_t nvls_elems;         //   fp32 elements of the buffer (bounds checks)
   RankView views[kMaxRanks];  // [0] for a real rank; [r] per emulated rank in loopback
 };
 

@@ -347,6 +347,7 @@ void launch_group(mgw_plan* p, int g, float lr, int epilogue, int algo, cudaStre
     L.nvls_mc = nvls_mc(c->nvls);
     L.chunk = c->nvls_chunk;
     L.nvls_skip = c->nvls_skip;
+    L.nvls_elems = nvls_bytes(c->nvls) / sizeof(float);
     L.ll_pkt = kNoLL;
     ck(launch_nvls_group(L, nvls_grid(c, L.n_tiles), stream), "nvls group launch");
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
@@ -923,6 +924,7 @@ int mgw_allreduce(mgw_comm* c, float* buf, size_t n, int algo, void* stream) {
       L.nvls_mc = mgw::nvls_mc(c->nvls);
       L.chunk = c->nvls_chunk;
       L.nvls_skip = c->nvls_skip;
+      L.nvls_elems = mgw::nvls_bytes(c->nvls) / sizeof(float);
       ck(mgw::launch_nvls_group(L, mgw::nvls_grid(c, L.n_tiles), static_cast<cudaStream_t>(stream)),
          "nvls all-reduce launch");
       mgw::g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
