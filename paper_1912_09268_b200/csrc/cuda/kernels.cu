@@ -1722,6 +1722,8 @@ __global__ void __launch_bounds__(kBlock, 1) engine_kernel(const __grid_constant
   CtaCtx cx;
   cta_ctx_init<P>(cx, v, dsmem, bars, &s_abort);
   const uint32_t iter = s_iter;
+  // past the entry barrier: a gated replay (calibration) may start its clock
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) st_release_gpu(E.pipe, iter + 1);
   const uint32_t ncta = gridDim.x;
   const uint32_t slot = blockIdx.y * gridDim.x + blockIdx.x;      // stamp column
   const size_t row = static_cast<size_t>(gridDim.x) * gridDim.y;  // stamp row width
@@ -2160,11 +2162,19 @@ __global__ void __launch_bounds__(kBlock) unpack_sgd_kernel(const Tile* tiles, u
 // mark the group ready for the comm engine. No per-group kernel launches, so
 // the emulated compute stream is continuously busy and its timing exact.
 __global__ void replay_all_kernel(unsigned long long* clock, const unsigned long long* deadlines,
-                                  uint32_t n, const uint32_t* pipe, uint32_t* flags) {
+                                  uint32_t n, const uint32_t* pipe, uint32_t* flags, int gate) {
   if (threadIdx.x != 0) return;
   // the engine of the previous iteration has finished (graph join), so the
   // iteration counter is this iteration's
   const uint32_t stamp = ld_volatile_u32(pipe + 1) + 1;
+  // gate (calibration): the replay clock starts when this rank's engine has
+  // passed its entry barrier (pipe[0]), so every rank's group becomes ready
+  // at the same time and T(M) excludes the ranks' launch skew
+  if (gate) {
+    const uint64_t w0 = globaltimer_ns();
+    while (static_cast<int32_t>(ld_acquire_gpu(pipe) - stamp) < 0 && globaltimer_ns() - w0 < kTimeoutNs) {
+    }
+  }
   const unsigned long long t0 = globaltimer_ns();
   clock[0] = t0;
   unsigned long long now = t0;
@@ -2382,8 +2392,8 @@ cudaError_t launch_l2_flush(void* buf, size_t bytes, int ctas, cudaStream_t stre
 
 cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long long* deadlines_ns,
                               uint32_t n, const uint32_t* pipe, uint32_t* flags,
-                              cudaStream_t stream) {
-  replay_all_kernel<<<1, 32, 0, stream>>>(clock, deadlines_ns, n, pipe, flags);
+                              cudaStream_t stream, int gate) {
+  replay_all_kernel<<<1, 32, 0, stream>>>(clock, deadlines_ns, n, pipe, flags, gate);
   return cudaGetLastError();
 }
 

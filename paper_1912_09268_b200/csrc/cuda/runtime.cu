@@ -47,7 +47,7 @@ cudaError_t launch_replay(unsigned long long* clock, unsigned long long deadline
 cudaError_t launch_engine(const EngineLaunch& E, int ctas, int ranks, cudaStream_t stream);
 cudaError_t launch_replay_all(unsigned long long* clock, const unsigned long long* deadlines_ns,
                               uint32_t n, const uint32_t* pipe, uint32_t* flags,
-                              cudaStream_t stream);
+                              cudaStream_t stream, int gate);
 cudaError_t launch_mark_ready(const uint32_t* pipe, uint32_t* flags, uint32_t g,
                               cudaStream_t stream);
 cudaError_t preload_kernels();
@@ -482,7 +482,7 @@ struct StepIo {
 
 mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float lr, int algo,
                              bool timed, size_t l2_flush_bytes, int engine_ctas,
-                             const StepIo& io = StepIo{});
+                             const StepIo& io = StepIo{}, bool gate_replay = false);
 
 }  // namespace
 }  // namespace mgw
@@ -1189,7 +1189,8 @@ void read_group_stamps(mgw_pipeline* pipe, std::vector<unsigned long long>& out)
 // engine_ctas != 0: ONE persistent engine kernel (engine_ctas CTAs, < 0 =
 // one per SM) that the replay kernels feed through a device ready counter.
 mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float lr, int algo,
-                             bool timed, size_t l2_flush_bytes, int engine_ctas, const StepIo& io) {
+                             bool timed, size_t l2_flush_bytes, int engine_ctas, const StepIo& io,
+                             bool gate_replay) {
   {
     require(t_f >= 0.0, "t_f must be >= 0");
     require(!p->comm->loopback || engine_ctas != 0,
@@ -1273,7 +1274,7 @@ mgw_pipeline* build_pipeline(mgw_plan* p, const double* t_b, double t_f, float l
         ck(launch_engine(pipe->args, pipe->engine_ctas, pipe->grid_y, pipe->comm), "engine launch");
         // one replay kernel walks every group head's ready time
         ck(launch_replay_all(pipe->d_clock, pipe->d_deadlines, static_cast<uint32_t>(G), pipe->d_pipe,
-                             pipe->d_ready, pipe->compute),
+                             pipe->d_ready, pipe->compute, gate_replay ? 1 : 0),
            "replay");
         if (pipe->tail_launch > 0) {
           // the replay kernel ends right after marking group 0 (last in backward order) ready
@@ -1486,7 +1487,8 @@ int mgw_calibrate_engine_ex(mgw_comm* c, const uint64_t* sizes, size_t n, int wa
           // the group becomes ready 100 us into the iteration, after the L2
           // flush: the engine is already waiting for it, as in a pipeline,
           // so T(M) is the ready -> reduced latency the planner trades
-          pipe = mgw::build_pipeline(p, tb.data(), 100e-6, 0.0f, algo, true, size_t{256} << 20, engine_ctas);
+          pipe = mgw::build_pipeline(p, tb.data(), 100e-6, 0.0f, algo, true, size_t{256} << 20, engine_ctas,
+                                     mgw::StepIo{}, /*gate_replay=*/true);
           std::vector<float> ms;
           std::vector<float> gm(R);
           for (int k = 0; k < warmup + reps; ++k) {
